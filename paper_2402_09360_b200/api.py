@@ -1,0 +1,370 @@
+"""Python mirror of the reference's `hire::` operator API for the hot path.
+
+Names, argument meaning and error behaviour follow
+/root/reference/proj/include/hire/*.hpp so parity tests read like the
+reference's own tests; every call goes through the C ABI of
+libhire_cuda.so (include/hire_cuda.h). torch is only the device-memory and
+stream plumbing. Batched: x is [B, d]; each query is an independent call of
+the reference function.
+
+Reference symbols mirrored (file:line under /root/reference/proj/include/hire):
+  ScoreMatrix linalg.hpp:44 · topk_select :157 · matvec :148 · exact_topk :184
+  ApproxScorer approx.hpp:327 (quantized :336, low_rank :332, slice_cols :415)
+  quantize_int4 approx.hpp:49 · HireConfig hire.hpp:16 · hire_topk hire.hpp:50
+  softmax_topk hire.hpp:123 · GroupedFFN ffn.hpp:19 · ffn_group_sparse :211
+  ffn_dense :65 · shard distributed.hpp:41 · da_topk :73 · da_group_sparse :145
+  recall metrics.hpp:23
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+from typing import Optional
+
+import numpy as np
+import torch
+
+from . import _lib as L
+from ._lib import check, lib
+
+_PHI = {"identity": 0, "relu": 1, "squared-relu": 2}
+
+
+def _phi(p) -> int:
+    return _PHI[p] if isinstance(p, str) else int(p)
+
+
+def _ptr(t: Optional[torch.Tensor]):
+    return C.c_void_p(t.data_ptr()) if t is not None else None
+
+
+class Context:
+    """A hire_ctx bound to one CUDA stream (default: torch's current stream)."""
+
+    def __init__(self, device: int = 0, stream: Optional[torch.cuda.Stream] = None):
+        self.device = device
+        s = stream if stream is not None else torch.cuda.current_stream(device)
+        self.stream = s
+        h = C.c_void_p()
+        check(lib().hire_ctx_create(device, C.c_void_p(s.cuda_stream), 0, C.byref(h)))
+        self.h = h
+
+    def launches(self) -> int:
+        return lib().hire_ctx_launch_count(self.h)
+
+    def synchronize(self):
+        check(lib().hire_ctx_synchronize(self.h))
+
+    def __del__(self):
+        if getattr(self, "h", None) and L._lib is not None:
+            L._lib.hire_ctx_destroy(self.h)
+
+
+_ctx_cache: dict = {}
+
+
+def default_context() -> Context:
+    dev = torch.cuda.current_device()
+    key = (dev, torch.cuda.current_stream(dev).cuda_stream)
+    c = _ctx_cache.get(key)
+    if c is None:
+        c = _ctx_cache[key] = Context(dev)
+    return c
+
+
+def _x2d(x: torch.Tensor, d: int) -> torch.Tensor:
+    if x.dim() == 1:
+        x = x.unsqueeze(0)
+    if x.dtype != torch.float32 or not x.is_cuda:
+        raise ValueError("x must be a CUDA float32 tensor [B, d]")
+    if x.shape[1] != d:
+        raise L.HireInvalidArgument(L.ERR_INVALID, f"x has dim {x.shape[1]} but the matrix has {d} rows")
+    return x.contiguous()
+
+
+class ScoreMatrix:
+    """Device-resident dense matrix W [l, d] (== the reference's d x l Z)."""
+
+    def __init__(self, w: torch.Tensor, _handle=None, _parent=None):
+        if w.dim() != 2 or not w.is_cuda:
+            raise ValueError("ScoreMatrix needs a 2-D CUDA tensor [l, d]")
+        if w.dtype not in (torch.float32, torch.bfloat16):
+            raise ValueError("ScoreMatrix dtype must be float32 or bfloat16")
+        self.tensor = w.contiguous()
+        self.rows, self.d = self.tensor.shape
+        self.dtype = L.BF16 if self.tensor.dtype == torch.bfloat16 else L.F32
+        self._parent = _parent
+        if _handle is None:
+            h = C.c_void_p()
+            check(lib().hire_matrix_view(_ptr(self.tensor), self.rows, self.d, self.dtype, C.byref(h)))
+            _handle = h
+        self.h = _handle
+
+    def slice_cols(self, first: int, count: int) -> "ScoreMatrix":
+        h = C.c_void_p()
+        check(lib().hire_matrix_slice(self.h, first, count, C.byref(h)))
+        return ScoreMatrix(self.tensor[first:first + count], _handle=h, _parent=self)
+
+    def __del__(self):
+        if getattr(self, "h", None) and L._lib is not None:
+            L._lib.hire_matrix_destroy(self.h)
+
+
+class ApproxScorer:
+    """The cheap proxy (approx.hpp:327): int4 per-row (HiRE-Q) or low-rank (HiRE-LR)."""
+
+    def __init__(self, handle, kind, rows, d, rank=0, keep=()):
+        self.h, self.kind, self.rows, self.d, self.rank = handle, kind, rows, d, rank
+        self._keep = keep
+
+    # approx.hpp:336 quantized(QuantizedMatrix)
+    @staticmethod
+    def quantized(codes: np.ndarray, scales: np.ndarray) -> "ApproxScorer":
+        codes = np.ascontiguousarray(codes, dtype=np.int8)
+        scales = np.ascontiguousarray(scales, dtype=np.float32)
+        rows, d = codes.shape
+        h = C.c_void_p()
+        check(lib().hire_scorer_create_q4_codes(codes.ctypes.data_as(C.c_void_p),
+                                                scales.ctypes.data_as(C.c_void_p), rows, d,
+                                                C.byref(h)))
+        return ApproxScorer(h, L.SCORER_Q4, rows, d)
+
+    # HIRQ payload (approx.hpp:551-564)
+    @staticmethod
+    def from_hirq(payload: np.ndarray, scales: np.ndarray, rows: int, d: int) -> "ApproxScorer":
+        payload = np.ascontiguousarray(payload, dtype=np.uint8)
+        scales = np.ascontiguousarray(scales, dtype=np.float32)
+        h = C.c_void_p()
+        check(lib().hire_scorer_create_q4_hirq(payload.ctypes.data_as(C.c_void_p),
+                                               scales.ctypes.data_as(C.c_void_p), rows, d,
+                                               C.byref(h)))
+        return ApproxScorer(h, L.SCORER_Q4, rows, d)
+
+    # approx.hpp:339 quantized(const ScoreMatrix&) — quantize_int4 on the device (K9)
+    @staticmethod
+    def quantize(z: ScoreMatrix, ctx: Optional[Context] = None) -> "ApproxScorer":
+        ctx = ctx or default_context()
+        h = C.c_void_p()
+        check(lib().hire_scorer_quantize(ctx.h, z.h, C.byref(h)))
+        return ApproxScorer(h, L.SCORER_Q4, z.rows, z.d)
+
+    # approx.hpp:332 low_rank(LowRankApprox): z1 [r, d], z2 [l, r] on the device
+    @staticmethod
+    def low_rank(z1: torch.Tensor, z2: torch.Tensor) -> "ApproxScorer":
+        if z1.dtype != z2.dtype or z1.dtype not in (torch.float32, torch.bfloat16):
+            raise ValueError("low-rank factors must share dtype float32/bfloat16")
+        r, d = z1.shape
+        rows, r2 = z2.shape
+        if r2 != r:
+            raise L.HireInvalidArgument(L.ERR_INVALID, f"ApproxScorer: low-rank factors do not match rank {r}")
+        dt = L.BF16 if z1.dtype == torch.bfloat16 else L.F32
+        z1c, z2c = z1.contiguous(), z2.contiguous()
+        h = C.c_void_p()
+        check(lib().hire_scorer_create_lowrank(_ptr(z1c), _ptr(z2c), d, rows, r, dt, 1, C.byref(h)))
+        return ApproxScorer(h, L.SCORER_LOWRANK, rows, d, r)
+
+    def slice_cols(self, first: int, count: int) -> "ApproxScorer":
+        h = C.c_void_p()
+        check(lib().hire_scorer_slice(self.h, first, count, C.byref(h)))
+        return ApproxScorer(h, self.kind, count, self.d, self.rank, keep=(self,))
+
+    def input_dim(self) -> int:
+        return self.d
+
+    def output_dim(self) -> int:
+        return self.rows
+
+    def export_q4(self):
+        codes = np.empty((self.rows, self.d), dtype=np.int8)
+        scales = np.empty(self.rows, dtype=np.float32)
+        check(lib().hire_scorer_export_q4(self.h, codes.ctypes.data_as(C.c_void_p),
+                                          scales.ctypes.data_as(C.c_void_p)))
+        return codes, scales
+
+    # approx.hpp:382 scores(x, phi), batched
+    def scores(self, x: torch.Tensor, phi="identity", x_mode: int = L.X_FP32, strict: bool = False,
+               ctx: Optional[Context] = None) -> torch.Tensor:
+        ctx = ctx or default_context()
+        x = _x2d(x, self.d)
+        out = torch.empty(x.shape[0], self.rows, dtype=torch.float32, device=x.device)
+        check(lib().hire_scores(ctx.h, self.h, _ptr(x), x.shape[0], _phi(phi), x_mode, int(strict), _ptr(out)))
+        return out
+
+    def __del__(self):
+        if getattr(self, "h", None) and L._lib is not None:
+            L._lib.hire_scorer_destroy(self.h)
+
+
+@dataclass
+class HireConfig:
+    """hire.hpp:16-20 plus the B200 knobs (see hire_topk_params)."""
+    k: int = 1
+    k_prime: int = 1
+    phi: object = "identity"
+    x_mode: int = L.X_FP32
+    select: int = L.SELECT_EXACT
+    strict: bool = False
+    n_buckets: int = 0
+    bucket_t: int = 0
+
+    def params(self) -> L.TopkParams:
+        return L.TopkParams(self.k, self.k_prime, _phi(self.phi), self.x_mode, self.select,
+                            int(self.strict), self.n_buckets, self.bucket_t)
+
+
+@dataclass
+class HireResult:
+    """hire.hpp:41-44: top-k (rank order) and the candidate set (ascending)."""
+    top_idx: torch.Tensor   # [B, n_top] int32
+    top_val: torch.Tensor   # [B, n_top] float32, exact against Z
+    cand: Optional[torch.Tensor]  # [B, n_cand] int32 ascending
+    clamped: bool
+    top_prob: Optional[torch.Tensor] = None
+
+
+def hire_topk(x: torch.Tensor, z: ScoreMatrix, a: ApproxScorer, cfg: HireConfig,
+              ctx: Optional[Context] = None, want_candidates: bool = True,
+              _probs: bool = False) -> HireResult:
+    """hire.hpp:50-86 for a batch of queries."""
+    ctx = ctx or default_context()
+    x = _x2d(x, z.d)
+    B = x.shape[0]
+    cand = torch.empty(B, max(cfg.k_prime, 1), dtype=torch.int32, device=x.device) if want_candidates else None
+    kk = max(cfg.k, 1)
+    ti = torch.empty(B, kk, dtype=torch.int32, device=x.device)
+    tv = torch.empty(B, kk, dtype=torch.float32, device=x.device)
+    tp = torch.empty(B, kk, dtype=torch.float32, device=x.device) if _probs else None
+    nc, nt, cl = C.c_int64(), C.c_int64(), C.c_int()
+    p = cfg.params()
+    check(lib().hire_topk_run(ctx.h, z.h, a.h, _ptr(x), B, C.byref(p), _ptr(cand), _ptr(ti), _ptr(tv),
+                              _ptr(tp), C.byref(nc), C.byref(nt), C.byref(cl)))
+    return HireResult(ti[:, :nt.value], tv[:, :nt.value],
+                      cand[:, :nc.value] if cand is not None else None, bool(cl.value),
+                      tp[:, :nt.value] if tp is not None else None)
+
+
+def softmax_topk(w: ScoreMatrix, x: torch.Tensor, a: ApproxScorer, cfg: HireConfig,
+                 ctx: Optional[Context] = None):
+    """hire.hpp:123-144: (indices [B,k] by probability desc, probabilities)."""
+    if _phi(cfg.phi) != 0:
+        raise L.HireInvalidArgument(L.ERR_INVALID, "softmax_topk: phi must be identity")
+    r = hire_topk(x, w, a, cfg, ctx, want_candidates=False, _probs=True)
+    return r.top_idx, r.top_prob
+
+
+def matvec(z: ScoreMatrix, x: torch.Tensor, phi="identity", strict: bool = False,
+           ctx: Optional[Context] = None) -> torch.Tensor:
+    """linalg.hpp:148-154 (batched). Shares the exact-recompute reduction."""
+    ctx = ctx or default_context()
+    x = _x2d(x, z.d)
+    out = torch.empty(x.shape[0], z.rows, dtype=torch.float32, device=x.device)
+    check(lib().hire_matvec(ctx.h, z.h, _ptr(x), x.shape[0], _phi(phi), int(strict), _ptr(out)))
+    return out
+
+
+def topk_select(v: torch.Tensor, k: int, ctx: Optional[Context] = None):
+    """linalg.hpp:157-176 on each row of v [B, n]: (idx, val, clamped)."""
+    ctx = ctx or default_context()
+    if v.dim() == 1:
+        v = v.unsqueeze(0)
+    v = v.contiguous().float()
+    B, n = v.shape
+    kk = min(k, n) if k >= 1 else 1
+    idx = torch.empty(B, kk, dtype=torch.int32, device=v.device)
+    val = torch.empty(B, kk, dtype=torch.float32, device=v.device)
+    cl = C.c_int()
+    check(lib().hire_topk_select(ctx.h, _ptr(v), B, n, k, _ptr(idx), _ptr(val), C.byref(cl)))
+    return idx, val, bool(cl.value)
+
+
+def exact_topk(z: ScoreMatrix, x: torch.Tensor, k: int, phi="identity", strict: bool = False,
+               ctx: Optional[Context] = None):
+    """linalg.hpp:184-188."""
+    return topk_select(matvec(z, x, phi, strict, ctx), k, ctx)
+
+
+@dataclass
+class GroupedFFN:
+    """ffn.hpp:19-28: U, V [m, d] (the reference's d x m), group size, phi."""
+    u: ScoreMatrix
+    v: ScoreMatrix
+    group_size: int = 1
+    phi: object = "relu"
+
+    def dim(self) -> int:
+        return self.u.d
+
+    def hidden(self) -> int:
+        return self.u.rows
+
+
+def ffn_group_sparse(f: GroupedFFN, x: torch.Tensor, a: ApproxScorer, k: int, k_prime: int,
+                     x_mode: int = L.X_FP32, strict: bool = False, ctx: Optional[Context] = None):
+    """ffn.hpp:211-219: (output [B, d], selected group ids [B, k/g] ascending)."""
+    ctx = ctx or default_context()
+    x = _x2d(x, f.u.d)
+    B = x.shape[0]
+    g = f.group_size
+    sel = torch.empty(B, max(k // max(g, 1), 1), dtype=torch.int32, device=x.device)
+    out = torch.empty(B, f.u.d, dtype=torch.float32, device=x.device)
+    p = L.FfnParams(k, k_prime, g, _phi(f.phi), x_mode, int(strict), 0)
+    check(lib().hire_ffn_run(ctx.h, f.u.h, f.v.h, a.h, _ptr(x), B, C.byref(p), _ptr(sel), _ptr(out)))
+    return out, sel
+
+
+def ffn_dense(f: GroupedFFN, x: torch.Tensor, strict: bool = False, ctx: Optional[Context] = None):
+    """ffn.hpp:65-76."""
+    ctx = ctx or default_context()
+    x = _x2d(x, f.u.d)
+    out = torch.empty(x.shape[0], f.u.d, dtype=torch.float32, device=x.device)
+    check(lib().hire_ffn_dense_run(ctx.h, f.u.h, f.v.h, _ptr(x), x.shape[0], _phi(f.phi), int(strict), _ptr(out)))
+    return out
+
+
+def shard_range(l: int, s: int, i: int):
+    """distributed.hpp:53-57: (first, width) of shard i of s."""
+    base, extra = divmod(l, s)
+    return i * base + min(i, extra), base + (1 if i < extra else 0)
+
+
+def da_topk_emulated(z: ScoreMatrix, a: ApproxScorer, x: torch.Tensor, s: int, cfg: HireConfig,
+                     merge: int = L.MERGE_PER_SHARD, uneven: bool = False,
+                     ctx: Optional[Context] = None):
+    """distributed.hpp:73-134 with all s shards on this GPU (no collective)."""
+    ctx = ctx or default_context()
+    x = _x2d(x, z.d)
+    B = x.shape[0]
+    cap = max(cfg.k, 1)
+    ti = torch.empty(B, cap, dtype=torch.int32, device=x.device)
+    tv = torch.empty(B, cap, dtype=torch.float32, device=x.device)
+    n, cl = C.c_int64(), C.c_int()
+    p = cfg.params()
+    check(lib().hire_da_topk_emulated(ctx.h, z.h, a.h, s, _ptr(x), B, C.byref(p), merge, int(uneven),
+                                      _ptr(ti), _ptr(tv), C.byref(n), C.byref(cl)))
+    return ti[:, :n.value], tv[:, :n.value], bool(cl.value)
+
+
+def da_group_sparse_emulated(f: GroupedFFN, x: torch.Tensor, a: ApproxScorer, k: int, k_prime: int,
+                             s: int, x_mode: int = L.X_FP32, strict: bool = False,
+                             uneven: bool = False, ctx: Optional[Context] = None):
+    """distributed.hpp:145-206 with all s shards on this GPU."""
+    ctx = ctx or default_context()
+    x = _x2d(x, f.u.d)
+    B = x.shape[0]
+    g = f.group_size
+    sel = torch.empty(B, max(k // max(g, 1), 1), dtype=torch.int32, device=x.device)
+    out = torch.empty(B, f.u.d, dtype=torch.float32, device=x.device)
+    p = L.FfnParams(k, k_prime, g, _phi(f.phi), x_mode, int(strict), 0)
+    check(lib().hire_da_ffn_emulated(ctx.h, f.u.h, f.v.h, a.h, s, _ptr(x), B, C.byref(p), int(uneven),
+                                     _ptr(sel), _ptr(out)))
+    return out, sel
+
+
+def recall(cand: np.ndarray, exact_idx: np.ndarray):
+    """metrics.hpp:23-34 for one query: (recall, intersection_k, top1_agree)."""
+    cand = np.asarray(cand)
+    exact_idx = np.asarray(exact_idx)
+    if exact_idx.size == 0:
+        return 0.0, 0, False
+    hit = np.isin(exact_idx, cand)
+    return float(hit.mean()), int(hit.sum()), bool(hit[0])

@@ -1,0 +1,119 @@
+// common.cuh — shared device helpers for the HiRE sm_100a kernels.
+#pragma once
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace hire_dev {
+
+constexpr int kWarp = 32;
+
+enum Phi : int { kIdentity = 0, kRelu = 1, kSqRelu = 2 };
+
+// linalg.hpp:31-38 (apply_activation).
+__device__ __forceinline__ float apply_phi(int phi, float z) {
+  if (phi == kRelu) return z > 0.0f ? z : 0.0f;
+  if (phi == kSqRelu) return z > 0.0f ? __fmul_rn(z, z) : 0.0f;
+  return z;
+}
+
+// ---------------------------------------------------------------------
+// Rank keys. The reference orders every selection by value descending,
+// ties by ascending index (linalg.hpp:129-133, `va != vb` so -0 == +0).
+// A 64-bit key = orderable(value) << 32 | (0xFFFFFFFF - index) turns that
+// total order into plain unsigned '>' : larger key ranks first. Key 0 never
+// encodes a real (non-NaN) score and is used as padding.
+// ---------------------------------------------------------------------
+__host__ __device__ __forceinline__ uint32_t ord_of(float v) {
+  uint32_t u;
+#ifdef __CUDA_ARCH__
+  u = __float_as_uint(v);
+#else
+  __builtin_memcpy(&u, &v, 4);
+#endif
+  if (u == 0x80000000u) u = 0;  // -0.0 ranks equal to +0.0
+  return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+
+__host__ __device__ __forceinline__ float value_of_ord(uint32_t o) {
+  const uint32_t u = (o & 0x80000000u) ? (o & 0x7FFFFFFFu) : ~o;
+#ifdef __CUDA_ARCH__
+  return __uint_as_float(u);
+#else
+  float f;
+  __builtin_memcpy(&f, &u, 4);
+  return f;
+#endif
+}
+
+__host__ __device__ __forceinline__ uint64_t make_key(float v, uint32_t idx) {
+  return (static_cast<uint64_t>(ord_of(v)) << 32) | (0xFFFFFFFFu - idx);
+}
+__host__ __device__ __forceinline__ uint32_t key_index(uint64_t k) {
+  return 0xFFFFFFFFu - static_cast<uint32_t>(k);
+}
+__host__ __device__ __forceinline__ float key_value(uint64_t k) {
+  return value_of_ord(static_cast<uint32_t>(k >> 32));
+}
+
+// --------------------------------------------------------------- loads --
+__device__ __forceinline__ uint4 ldg_stream(const void* p) {
+  uint4 r;
+  asm("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p));
+  return r;
+}
+
+__device__ __forceinline__ float bf16_lo(uint32_t w) { return __uint_as_float(w << 16); }
+__device__ __forceinline__ float bf16_hi(uint32_t w) { return __uint_as_float(w & 0xFFFF0000u); }
+
+// ------------------------------------------------------ warp reductions --
+__device__ __forceinline__ int warp_sum_i32(int v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// Fixed butterfly tree: identical association on every call, every launch
+// configuration — so every exact-score producer that uses it (gather
+// recompute, dense exact, FFN activations) yields bit-identical values.
+__device__ __forceinline__ float warp_sum_f32(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = __fadd_rn(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+__device__ __forceinline__ float warp_max_f32(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+__device__ __forceinline__ uint64_t warp_max_u64(uint64_t v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const uint64_t w = __shfl_xor_sync(0xffffffffu, v, o);
+    v = w > v ? w : v;
+  }
+  return v;
+}
+
+template <typename T>
+__device__ __forceinline__ float load_elem(const T* p, int64_t i);
+template <>
+__device__ __forceinline__ float load_elem<float>(const float* p, int64_t i) { return p[i]; }
+template <>
+__device__ __forceinline__ float load_elem<__nv_bfloat16>(const __nv_bfloat16* p, int64_t i) {
+  return __bfloat162float(p[i]);
+}
+
+// Round half away from zero, clamped — approx.hpp:41-45. `v + 0.5f` is one
+// IEEE fp32 add exactly as on the host.
+__device__ __forceinline__ int rhaz_clamp(float v, int lim) {
+  const float r = v >= 0.0f ? floorf(__fadd_rn(v, 0.5f)) : ceilf(__fsub_rn(v, 0.5f));
+  int c = static_cast<int>(r);
+  return c < -lim ? -lim : (c > lim ? lim : c);
+}
+
+}  // namespace hire_dev

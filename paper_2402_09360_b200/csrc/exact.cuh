@@ -1,0 +1,177 @@
+// exact.cuh — row-gather exact recompute (K4), dense exact scores (K8) and
+// the sparse FFN down-projection (K6).
+//
+// Reference semantics:
+//   column_score  linalg.hpp:140-146 (every exact value goes through it;
+//                 hire.hpp:71-72, ffn.hpp:125-131, ffn.hpp:165)
+//   matvec        linalg.hpp:148-154
+//   ffn_apply_groups ffn.hpp:154-171: out[i] += act_j * V_j[i], j ascending
+//
+// fast   : one warp per row, 128-bit loads, fp32 FMA per lane in column
+//          order, fixed butterfly tree (common.cuh warp_sum_f32). The same
+//          routine serves the gather recompute and the dense exact pass, so
+//          HiRE values equal dense values bit for bit on the GPU — the
+//          reference's own design rule (linalg.hpp:137-139).
+// strict : one thread per row, ascending columns, __fmul_rn/__fadd_rn —
+//          bit-identical to the reference's sequential fp32 loop.
+#pragma once
+#include "common.cuh"
+
+namespace hire_dev {
+
+template <typename T>
+struct Vec16;
+template <>
+struct Vec16<__nv_bfloat16> {
+  static constexpr int kElems = 8;
+  __device__ __forceinline__ static void expand(uint4 u, float* f) {
+    f[0] = bf16_lo(u.x); f[1] = bf16_hi(u.x); f[2] = bf16_lo(u.y); f[3] = bf16_hi(u.y);
+    f[4] = bf16_lo(u.z); f[5] = bf16_hi(u.z); f[6] = bf16_lo(u.w); f[7] = bf16_hi(u.w);
+  }
+};
+template <>
+struct Vec16<float> {
+  static constexpr int kElems = 4;
+  __device__ __forceinline__ static void expand(uint4 u, float* f) {
+    f[0] = __uint_as_float(u.x); f[1] = __uint_as_float(u.y);
+    f[2] = __uint_as_float(u.z); f[3] = __uint_as_float(u.w);
+  }
+};
+
+// grid = (tiles, B); 8 warps per CTA; warp-strided over the n_cand rows of
+// query b. cand == nullptr means row i itself (dense exact, K8).
+template <typename T, int CPL>
+__global__ void __launch_bounds__(256) recompute_fast(
+    const T* __restrict__ w, int d, const uint32_t* __restrict__ cand, int64_t cand_stride,
+    int n_cand, const float* __restrict__ x, int phi, float* __restrict__ out,
+    int64_t out_stride) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  float* s_x = reinterpret_cast<float*>(smem);
+  constexpr int E = Vec16<T>::kElems;
+  const int b = blockIdx.y;
+  for (int i = threadIdx.x; i < d; i += blockDim.x) s_x[i] = x[static_cast<int64_t>(b) * d + i];
+  __syncthreads();
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int64_t pitch_vec = static_cast<int64_t>(d) / E;  // 16-byte vectors per row
+  for (int i = blockIdx.x * 8 + wid; i < n_cand; i += gridDim.x * 8) {
+    const int64_t row = cand ? cand[b * cand_stride + i] : i;
+    const uint4* rp = reinterpret_cast<const uint4*>(w) + row * pitch_vec;
+    uint4 v[CPL];
+#pragma unroll
+    for (int c = 0; c < CPL; ++c) v[c] = ldg_stream(rp + lane + 32 * c);
+    float acc = 0.0f;
+#pragma unroll
+    for (int c = 0; c < CPL; ++c) {
+      float f[E];
+      Vec16<T>::expand(v[c], f);
+      const float* xs = s_x + (lane + 32 * c) * E;
+#pragma unroll
+      for (int e = 0; e < E; ++e) acc = fmaf(f[e], xs[e], acc);
+    }
+    acc = warp_sum_f32(acc);
+    if (lane == 0) out[b * out_stride + i] = apply_phi(phi, acc);
+  }
+}
+
+// strict / generic: one thread per row; any d.
+template <typename T>
+__global__ void __launch_bounds__(128) recompute_seq(
+    const T* __restrict__ w, int d, const uint32_t* __restrict__ cand, int64_t cand_stride,
+    int n_cand, const float* __restrict__ x, int phi, float* __restrict__ out,
+    int64_t out_stride) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  float* s_x = reinterpret_cast<float*>(smem);
+  const int b = blockIdx.y;
+  for (int i = threadIdx.x; i < d; i += blockDim.x) s_x[i] = x[static_cast<int64_t>(b) * d + i];
+  __syncthreads();
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n_cand) return;
+  const int64_t row = cand ? cand[b * cand_stride + i] : i;
+  const T* rp = w + row * d;
+  float acc = 0.0f;
+  for (int c = 0; c < d; ++c) acc = __fadd_rn(acc, __fmul_rn(load_elem<T>(rp, c), s_x[c]));
+  out[b * out_stride + i] = apply_phi(phi, acc);
+}
+
+// ---------------------------------------------------------------------
+// K6 fast: split over selected units. grid = (n_chunks, B), 256 threads;
+// chunk c sums units [c*CH, c*CH+CH) of query b (ascending) for all d
+// columns; each thread owns 8 (bf16) / 4 (fp32) consecutive columns per
+// pass. partial[b][c][d] is then reduced over c ascending (deterministic).
+// ---------------------------------------------------------------------
+template <typename T>
+__global__ void __launch_bounds__(256) ffn_down_partial(
+    const T* __restrict__ v, int d, const uint32_t* __restrict__ sel,
+    const float* __restrict__ act, int64_t sel_stride, int n_sel, int ch,
+    float* __restrict__ partial) {
+  constexpr int E = Vec16<T>::kElems;
+  const int c = blockIdx.x, b = blockIdx.y;
+  const int lo = c * ch, hi = min(n_sel, lo + ch);
+  const int64_t pitch_vec = d / E;
+  float* pout = partial + (static_cast<int64_t>(b) * gridDim.x + c) * d;
+  for (int col0 = threadIdx.x; col0 < pitch_vec; col0 += blockDim.x) {
+    float acc[E];
+#pragma unroll
+    for (int e = 0; e < E; ++e) acc[e] = 0.0f;
+    int j = lo;
+    for (; j + 4 <= hi; j += 4) {
+      uint4 u[4];
+      float a[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int64_t row = sel[b * sel_stride + j + q];
+        a[q] = act[b * sel_stride + j + q];
+        u[q] = ldg_stream(reinterpret_cast<const uint4*>(v) + row * pitch_vec + col0);
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        float f[E];
+        Vec16<T>::expand(u[q], f);
+#pragma unroll
+        for (int e = 0; e < E; ++e) acc[e] = fmaf(a[q], f[e], acc[e]);
+      }
+    }
+    for (; j < hi; ++j) {
+      const int64_t row = sel[b * sel_stride + j];
+      const float a = act[b * sel_stride + j];
+      float f[E];
+      Vec16<T>::expand(ldg_stream(reinterpret_cast<const uint4*>(v) + row * pitch_vec + col0), f);
+#pragma unroll
+      for (int e = 0; e < E; ++e) acc[e] = fmaf(a, f[e], acc[e]);
+    }
+#pragma unroll
+    for (int e = 0; e < E; ++e) pout[col0 * E + e] = acc[e];
+  }
+}
+
+__global__ void __launch_bounds__(256) ffn_down_reduce(const float* __restrict__ partial,
+                                                       int n_chunks, int d, int B,
+                                                       float* __restrict__ out) {
+  const int64_t id = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (id >= static_cast<int64_t>(B) * d) return;
+  const int b = static_cast<int>(id / d), col = static_cast<int>(id % d);
+  const float* p = partial + static_cast<int64_t>(b) * n_chunks * d + col;
+  float s = 0.0f;
+  for (int c = 0; c < n_chunks; ++c) s = __fadd_rn(s, p[static_cast<int64_t>(c) * d]);
+  out[id] = s;
+}
+
+// strict: one thread per (column, query); units ascending; no contraction.
+// Bit-identical to ffn.hpp:160-169 given identical activations.
+template <typename T>
+__global__ void __launch_bounds__(256) ffn_down_seq(const T* __restrict__ v, int d,
+                                                    const uint32_t* __restrict__ sel,
+                                                    const float* __restrict__ act,
+                                                    int64_t sel_stride, int n_sel,
+                                                    float* __restrict__ out) {
+  const int col = blockIdx.x * blockDim.x + threadIdx.x, b = blockIdx.y;
+  if (col >= d) return;
+  float acc = 0.0f;
+  for (int j = 0; j < n_sel; ++j) {
+    const int64_t row = sel[b * sel_stride + j];
+    acc = __fadd_rn(acc, __fmul_rn(act[b * sel_stride + j], load_elem<T>(v + row * d, col)));
+  }
+  out[static_cast<int64_t>(b) * d + col] = acc;
+}
+
+}  // namespace hire_dev

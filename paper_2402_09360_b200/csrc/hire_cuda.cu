@@ -1,0 +1,1505 @@
+// hire_cuda.cu — C ABI (include/hire_cuda.h) and host orchestration of the
+// HiRE approximate top-k path on B200 (sm_100a).
+//
+// One call = a fixed chain of stream-ordered kernels, no host sync:
+//   [prep_x] -> proxy scores (K1/K2) -> [bucket survivors] -> candidate
+//   select (K3) -> gather + exact recompute (K4) -> final top-k / softmax (K5)
+//   [-> FFN down-projection (K6)] [-> NCCL all-gather/all-reduce + merge (K7)]
+// Reference orchestration replaced: hire_topk hire.hpp:50-86, softmax_topk
+// hire.hpp:123-144, ffn_group_sparse ffn.hpp:211-219 (select_groups :175-201,
+// ffn_apply_groups :154-171), da_topk distributed.hpp:73-134,
+// da_group_sparse distributed.hpp:145-206.
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <cstdlib>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/hire_cuda.h"
+#include "common.cuh"
+#include "exact.cuh"
+#include "score.cuh"
+#include "select.cuh"
+
+using namespace hire_dev;
+
+// ------------------------------------------------------------ plumbing --
+namespace {
+thread_local std::string g_err;
+
+int set_err(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+int invalid(const std::string& msg) { return set_err(HIRE_ERR_INVALID, msg); }
+
+#define CK(call)                                                                   \
+  do {                                                                             \
+    cudaError_t e_ = (call);                                                       \
+    if (e_ != cudaSuccess)                                                         \
+      return set_err(HIRE_ERR_RUNTIME, std::string(#call) + ": " + cudaGetErrorString(e_)); \
+  } while (0)
+
+#define CKN(call)                                                                  \
+  do {                                                                             \
+    ncclResult_t r_ = (call);                                                      \
+    if (r_ != ncclSuccess)                                                         \
+      return set_err(HIRE_ERR_RUNTIME, std::string(#call) + ": " + ncclGetErrorString(r_)); \
+  } while (0)
+
+#define RET(call)             \
+  do {                        \
+    int rc_ = (call);         \
+    if (rc_ != HIRE_OK) return rc_; \
+  } while (0)
+
+constexpr size_t kAlign = 256;
+size_t align_up(size_t v, size_t a = kAlign) { return (v + a - 1) / a * a; }
+int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+}  // namespace
+
+struct hire_ctx_s {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  int num_sms = 148;
+  void* ws = nullptr;
+  size_t ws_cap = 0;
+  void* io_dev = nullptr;
+  size_t io_dev_cap = 0;
+  void* io_host = nullptr;
+  size_t io_host_cap = 0;
+  int64_t launches = 0;
+};
+
+struct hire_matrix_s {
+  void* ptr = nullptr;
+  int64_t rows = 0, d = 0;
+  int dtype = HIRE_F32;
+  bool owned = false;
+};
+
+struct hire_scorer_s {
+  int kind = HIRE_SCORER_Q4;
+  int64_t rows = 0, d = 0, r = 0;
+  // int4
+  uint8_t* codes = nullptr;
+  int64_t pitch = 0;
+  float* scales = nullptr;
+  // low-rank
+  void* z1 = nullptr;
+  void* z2 = nullptr;
+  int dtype = HIRE_F32;
+  bool owned = false;
+};
+
+struct hire_comm_s {
+  ncclComm_t comm = nullptr;
+  int world = 1, rank = 0;
+};
+
+namespace {
+
+size_t dtype_size(int dt) { return dt == HIRE_BF16 ? 2 : 4; }
+
+int ensure(void** buf, size_t* cap, size_t need, cudaStream_t s) {
+  if (need <= *cap) return HIRE_OK;
+  if (*buf) {
+    CK(cudaStreamSynchronize(s));
+    CK(cudaFree(*buf));
+    *buf = nullptr;
+  }
+  size_t n = std::max(need, *cap * 2);
+  CK(cudaMalloc(buf, n));
+  *cap = n;
+  return HIRE_OK;
+}
+
+int ensure_host(void** buf, size_t* cap, size_t need, cudaStream_t s) {
+  if (need <= *cap) return HIRE_OK;
+  if (*buf) {
+    CK(cudaStreamSynchronize(s));
+    CK(cudaFreeHost(*buf));
+    *buf = nullptr;
+  }
+  size_t n = std::max(need, *cap * 2);
+  CK(cudaMallocHost(buf, n));
+  *cap = n;
+  return HIRE_OK;
+}
+
+// Bump allocator over the context workspace. Offsets first, then one
+// ensure(); pointers are only valid for the current call.
+struct Arena {
+  size_t off = 0;
+  std::vector<std::pair<void**, size_t>> reqs;
+  template <typename T>
+  void take(T** p, size_t count) {
+    reqs.push_back({reinterpret_cast<void**>(p), off});
+    off += align_up(std::max<size_t>(count, 1) * sizeof(T));
+  }
+  int commit(hire_ctx ctx) {
+    RET(ensure(&ctx->ws, &ctx->ws_cap, off, ctx->stream));
+    for (auto& r : reqs) *r.first = static_cast<char*>(ctx->ws) + r.second;
+    return HIRE_OK;
+  }
+};
+
+template <typename K>
+int max_blocks(K kernel, int threads, size_t smem) {
+  int n = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kernel, threads, smem) != cudaSuccess) n = 1;
+  return std::max(n, 1);
+}
+
+// ----------------------------------------------------- selection policy --
+struct SelPlan {
+  int mode = 0;          // 0 direct, 1 bucket
+  int n_buckets = 0, t = 0;
+  int exact_fix = 1;
+  int64_t k_eff = 0;     // candidates produced
+  bool clamped = false;
+};
+
+int plan_select(int64_t n, int64_t k_prime, int sel_mode, int64_t nb_req, int64_t t_req,
+                SelPlan* sp) {
+  if (k_prime < 1) return invalid("topk_select: k must be >= 1");
+  if (n < 1) return invalid("selection over an empty score vector");
+  if (n > 0xFFFFFFFELL) return invalid("selection: more than 2^32-2 scores");
+  if (sel_mode == HIRE_SELECT_BUCKETED) {
+    if (nb_req < 1 || nb_req > n) return invalid("bucketed select: n_buckets must be in [1, rows]");
+    const int64_t t = t_req > 0 ? t_req : 1;
+    if (ceil_div(n, nb_req) > kBucketMaxWidth)
+      return invalid("bucketed select: bucket width exceeds " + std::to_string(kBucketMaxWidth));
+    // valid survivors = sum_b min(t, width_b)
+    const int64_t base = n / nb_req, extra = n % nb_req;
+    const int64_t valid = extra * std::min(t, base + 1) + (nb_req - extra) * std::min(t, base);
+    if (nb_req * t > kPoolKeys) return invalid("bucketed select: n_buckets * t exceeds the pool");
+    sp->mode = 1;
+    sp->n_buckets = static_cast<int>(nb_req);
+    sp->t = static_cast<int>(t);
+    sp->exact_fix = 0;
+    sp->k_eff = std::min(k_prime, valid);
+    sp->clamped = k_prime > valid;
+    return HIRE_OK;
+  }
+  sp->k_eff = std::min(k_prime, n);
+  sp->clamped = k_prime > n;
+  if (n <= kDirectMax && nb_req == 0) {
+    sp->mode = 0;
+    return HIRE_OK;
+  }
+  sp->mode = 1;
+  sp->exact_fix = 1;
+  int64_t width = 256;
+  for (;;) {
+    const int64_t nb = nb_req > 0 ? nb_req : std::max<int64_t>(1, ceil_div(n, width));
+    const int64_t w = ceil_div(n, nb);
+    const double mean = static_cast<double>(sp->k_eff) / static_cast<double>(nb);
+    int64_t t = t_req > 0 ? t_req : static_cast<int64_t>(std::ceil(mean + 4.0 * std::sqrt(mean) + 2.0));
+    t = std::min(t, w);
+    if (w > kBucketMaxWidth) return invalid("selection: bucket width exceeds " + std::to_string(kBucketMaxWidth));
+    if ((nb * t <= kPoolKeys / 2 && nb * t >= sp->k_eff) || nb_req > 0) {
+      if (nb * t > kPoolKeys) return invalid("selection: n_buckets * t exceeds the pool");
+      if (nb * t < sp->k_eff) return invalid("selection: n_buckets * t < k_prime");
+      sp->n_buckets = static_cast<int>(nb);
+      sp->t = static_cast<int>(t);
+      return HIRE_OK;
+    }
+    width *= 2;
+    if (width > kBucketMaxWidth) {
+      // very large k': fall back to the global-memory exact path via a
+      // single huge "overflow" (select kernel handles it)
+      sp->n_buckets = static_cast<int>(std::max<int64_t>(1, ceil_div(n, kBucketMaxWidth)));
+      sp->t = static_cast<int>(std::min<int64_t>(kBucketMaxWidth, kPoolKeys / 2 / sp->n_buckets));
+      if (static_cast<int64_t>(sp->n_buckets) * sp->t < sp->k_eff)
+        return invalid("selection: k_prime too large for the on-chip selector");
+      return HIRE_OK;
+    }
+  }
+}
+
+// Candidate selection over scores [B][n] -> cand [B][cand_stride] ascending.
+int run_select(hire_ctx ctx, const float* scores, int64_t score_stride, int64_t n, int64_t B,
+               const SelPlan& sp, uint64_t* surv, uint32_t* cand, int64_t cand_stride,
+               int* status) {
+  if (sp.mode == 1) {
+    bucket_topt_kernel<<<dim3(sp.n_buckets, static_cast<unsigned>(B)), 256, 0, ctx->stream>>>(
+        scores, score_stride, n, sp.n_buckets, sp.t, surv);
+    ctx->launches++;
+    CK(cudaGetLastError());
+  }
+  const size_t smem = sp.mode == 0 ? static_cast<size_t>(n) * 4 : static_cast<size_t>(kPoolKeys) * 8;
+  select_candidates_kernel<<<static_cast<unsigned>(B), kSelectThreads, smem, ctx->stream>>>(
+      sp.mode, scores, score_stride, n, surv, sp.n_buckets, sp.t, static_cast<int>(sp.k_eff),
+      sp.exact_fix, cand, cand_stride, status);
+  ctx->launches++;
+  CK(cudaGetLastError());
+  return HIRE_OK;
+}
+
+int check_phi(int phi) {
+  if (phi < 0 || phi > 2) return invalid("unknown activation");
+  return HIRE_OK;
+}
+
+// ---------------------------------------------------------- proxy scores --
+struct ScoreWs {
+  int8_t* xq = nullptr;
+  int8_t* xperm = nullptr;
+  float* sx = nullptr;
+  int* sumxq = nullptr;
+  float* t = nullptr;
+};
+
+void take_score_ws(Arena& ar, ScoreWs* w, const hire_scorer_s* a, int64_t B) {
+  ar.take(&w->xq, static_cast<size_t>(B * a->d));
+  ar.take(&w->xperm, static_cast<size_t>(B * a->d));
+  ar.take(&w->sx, static_cast<size_t>(B));
+  ar.take(&w->sumxq, static_cast<size_t>(B));
+  ar.take(&w->t, static_cast<size_t>(B * std::max<int64_t>(a->r, 1)));
+}
+
+template <int QB, int CPL>
+int launch_q4_int8(hire_ctx ctx, const hire_scorer_s* a, const ScoreWs& w, int64_t b0, int phi,
+                   float* out, int64_t stride) {
+  auto k = q4_score_fast_int8<QB, CPL>;
+  static int bps = 0;
+  if (!bps) bps = max_blocks(k, 256, 0);
+  const int64_t want = ceil_div(a->rows, 16);
+  const int grid = static_cast<int>(std::min<int64_t>(want, static_cast<int64_t>(bps) * ctx->num_sms));
+  k<<<grid, 256, 0, ctx->stream>>>(a->codes, a->pitch, a->scales, a->rows, static_cast<int>(a->d),
+                                    w.xperm + b0 * a->d, w.sx + b0, w.sumxq + b0, phi,
+                                    out + b0 * stride, stride);
+  ctx->launches++;
+  CK(cudaGetLastError());
+  return HIRE_OK;
+}
+
+template <int CPL>
+int launch_q4_int8_cpl(hire_ctx ctx, const hire_scorer_s* a, const ScoreWs& w, int64_t B, int phi,
+                       float* out, int64_t stride) {
+  constexpr int QBMAX = CPL <= 2 ? 4 : (CPL == 4 ? 2 : 1);
+  int64_t b0 = 0;
+  while (b0 < B) {
+    const int64_t left = B - b0;
+    if (QBMAX >= 4 && left >= 4) { RET((launch_q4_int8<(QBMAX >= 4 ? 4 : 1), CPL>(ctx, a, w, b0, phi, out, stride))); b0 += 4; }
+    else if (QBMAX >= 2 && left >= 2) { RET((launch_q4_int8<(QBMAX >= 2 ? 2 : 1), CPL>(ctx, a, w, b0, phi, out, stride))); b0 += 2; }
+    else { RET((launch_q4_int8<1, CPL>(ctx, a, w, b0, phi, out, stride))); b0 += 1; }
+  }
+  return HIRE_OK;
+}
+
+template <int CPL>
+int launch_q4_fpx(hire_ctx ctx, const hire_scorer_s* a, const float* x, int64_t B, int phi,
+                  float* out, int64_t stride) {
+  auto k = q4_score_fast_fpx<CPL>;
+  static int bps = 0;
+  if (!bps) bps = max_blocks(k, 256, 0);
+  const int64_t want = ceil_div(a->rows, 8);
+  const int grid = static_cast<int>(std::min<int64_t>(want, static_cast<int64_t>(bps) * ctx->num_sms));
+  for (int64_t b = 0; b < B; ++b) {
+    k<<<grid, 256, 0, ctx->stream>>>(a->codes, a->pitch, a->scales, a->rows, static_cast<int>(a->d),
+                                      x + b * a->d, phi, out + b * stride);
+    ctx->launches++;
+  }
+  CK(cudaGetLastError());
+  return HIRE_OK;
+}
+
+// phi(Z_approx^T x) for B queries into out [B][stride].
+int run_scores(hire_ctx ctx, const hire_scorer_s* a, const float* x, int64_t B, int phi,
+               int x_mode, int strict, const ScoreWs& w, float* out, int64_t stride) {
+  const int d = static_cast<int>(a->d);
+  if (a->kind == HIRE_SCORER_Q4) {
+    if (x_mode == HIRE_X_INT8) {
+      prep_x_int8_kernel<<<static_cast<unsigned>(B), 256, 0, ctx->stream>>>(x, d, w.xq, w.xperm, w.sx, w.sumxq);
+      ctx->launches++;
+      CK(cudaGetLastError());
+    }
+    const bool fast_shape = (d % 1024 == 0) && a->pitch == d / 2 && d <= 8192;
+    if (fast_shape && x_mode == HIRE_X_INT8) {
+      switch (d / 1024) {
+        case 1: return launch_q4_int8_cpl<1>(ctx, a, w, B, phi, out, stride);
+        case 2: return launch_q4_int8_cpl<2>(ctx, a, w, B, phi, out, stride);
+        case 4: return launch_q4_int8_cpl<4>(ctx, a, w, B, phi, out, stride);
+        case 8: return launch_q4_int8_cpl<8>(ctx, a, w, B, phi, out, stride);
+        default: break;
+      }
+    }
+    if (fast_shape && x_mode == HIRE_X_FP32 && !strict) {
+      switch (d / 1024) {
+        case 1: return launch_q4_fpx<1>(ctx, a, x, B, phi, out, stride);
+        case 2: return launch_q4_fpx<2>(ctx, a, x, B, phi, out, stride);
+        case 4: return launch_q4_fpx<4>(ctx, a, x, B, phi, out, stride);
+        default: break;
+      }
+    }
+    const size_t smem = static_cast<size_t>(d) * 5 + 16;
+    if (smem > 48 * 1024) CK(cudaFuncSetAttribute(q4_score_seq, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    q4_score_seq<<<dim3(static_cast<unsigned>(ceil_div(a->rows, 128)), static_cast<unsigned>(B)), 128, smem, ctx->stream>>>(
+        a->codes, a->pitch, a->scales, a->rows, d, x, w.xq, w.sx, x_mode == HIRE_X_INT8, phi, out, stride);
+    ctx->launches++;
+    CK(cudaGetLastError());
+    return HIRE_OK;
+  }
+  // low-rank
+  const int r = static_cast<int>(a->r);
+  const bool bf = a->dtype == HIRE_BF16;
+  {
+    const int64_t items = static_cast<int64_t>(r) * B;
+    const unsigned grid = static_cast<unsigned>(strict ? ceil_div(items, 256) : ceil_div(items * 32, 256));
+    if (bf) lr_t_kernel<__nv_bfloat16><<<grid, 256, 0, ctx->stream>>>(static_cast<const __nv_bfloat16*>(a->z1), r, d, x, static_cast<int>(B), strict, w.t);
+    else lr_t_kernel<float><<<grid, 256, 0, ctx->stream>>>(static_cast<const float*>(a->z1), r, d, x, static_cast<int>(B), strict, w.t);
+    ctx->launches++;
+    CK(cudaGetLastError());
+  }
+  const size_t smem = static_cast<size_t>(r) * B * 4;
+  const unsigned grid = static_cast<unsigned>(ceil_div(a->rows, 128));
+  auto setsm = [&](const void* f) -> int {
+    if (smem > 48 * 1024) CK(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    return HIRE_OK;
+  };
+  if (smem > 200 * 1024) return invalid("low-rank scores: rank * batch too large");
+  if (r == 64 && B * r * 4 <= 200 * 1024) {
+    if (bf && strict) { RET(setsm((const void*)lr_score_kernel<__nv_bfloat16, 64, true>)); lr_score_kernel<__nv_bfloat16, 64, true><<<grid, 128, smem, ctx->stream>>>(static_cast<const __nv_bfloat16*>(a->z2), a->rows, w.t, static_cast<int>(B), phi, out, stride); }
+    else if (bf) { RET(setsm((const void*)lr_score_kernel<__nv_bfloat16, 64, false>)); lr_score_kernel<__nv_bfloat16, 64, false><<<grid, 128, smem, ctx->stream>>>(static_cast<const __nv_bfloat16*>(a->z2), a->rows, w.t, static_cast<int>(B), phi, out, stride); }
+    else if (strict) { RET(setsm((const void*)lr_score_kernel<float, 64, true>)); lr_score_kernel<float, 64, true><<<grid, 128, smem, ctx->stream>>>(static_cast<const float*>(a->z2), a->rows, w.t, static_cast<int>(B), phi, out, stride); }
+    else { RET(setsm((const void*)lr_score_kernel<float, 64, false>)); lr_score_kernel<float, 64, false><<<grid, 128, smem, ctx->stream>>>(static_cast<const float*>(a->z2), a->rows, w.t, static_cast<int>(B), phi, out, stride); }
+  } else {
+    if (bf && strict) { RET(setsm((const void*)lr_score_generic<__nv_bfloat16, true>)); lr_score_generic<__nv_bfloat16, true><<<grid, 128, smem, ctx->stream>>>(static_cast<const __nv_bfloat16*>(a->z2), a->rows, r, w.t, static_cast<int>(B), phi, out, stride); }
+    else if (bf) { RET(setsm((const void*)lr_score_generic<__nv_bfloat16, false>)); lr_score_generic<__nv_bfloat16, false><<<grid, 128, smem, ctx->stream>>>(static_cast<const __nv_bfloat16*>(a->z2), a->rows, r, w.t, static_cast<int>(B), phi, out, stride); }
+    else if (strict) { RET(setsm((const void*)lr_score_generic<float, true>)); lr_score_generic<float, true><<<grid, 128, smem, ctx->stream>>>(static_cast<const float*>(a->z2), a->rows, r, w.t, static_cast<int>(B), phi, out, stride); }
+    else { RET(setsm((const void*)lr_score_generic<float, false>)); lr_score_generic<float, false><<<grid, 128, smem, ctx->stream>>>(static_cast<const float*>(a->z2), a->rows, r, w.t, static_cast<int>(B), phi, out, stride); }
+  }
+  ctx->launches++;
+  CK(cudaGetLastError());
+  return HIRE_OK;
+}
+
+// ------------------------------------------------------------- recompute --
+template <typename T, int CPL>
+int launch_recompute_fast(hire_ctx ctx, const void* w, int d, const uint32_t* cand,
+                          int64_t cand_stride, int64_t n_cand, const float* x, int64_t B, int phi,
+                          float* out, int64_t out_stride) {
+  const size_t smem = static_cast<size_t>(d) * 4;
+  auto k = recompute_fast<T, CPL>;
+  if (smem > 48 * 1024) CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+  const int64_t tiles = std::max<int64_t>(1, std::min<int64_t>(ceil_div(n_cand, 8), std::max<int64_t>(1, 4 * ctx->num_sms / B)));
+  k<<<dim3(static_cast<unsigned>(tiles), static_cast<unsigned>(B)), 256, smem, ctx->stream>>>(
+      static_cast<const T*>(w), d, cand, cand_stride, static_cast<int>(n_cand), x, phi, out, out_stride);
+  ctx->launches++;
+  CK(cudaGetLastError());
+  return HIRE_OK;
+}
+
+// phi(<W_row, x_b>) for rows cand[b][i] (or i when cand == nullptr).
+int run_recompute(hire_ctx ctx, const hire_matrix_s* m, const uint32_t* cand, int64_t cand_stride,
+                  int64_t n_cand, const float* x, int64_t B, int phi, int strict, float* out,
+                  int64_t out_stride) {
+  if (n_cand <= 0) return HIRE_OK;
+  const int d = static_cast<int>(m->d);
+  const size_t es = dtype_size(m->dtype);
+  const int64_t bytes = static_cast<int64_t>(d) * static_cast<int64_t>(es);
+  if (!strict && bytes % 512 == 0) {
+    const int cpl = static_cast<int>(bytes / 512);
+    const bool bf = m->dtype == HIRE_BF16;
+#define RC(C)                                                                                              \
+  case C:                                                                                                 \
+    return bf ? launch_recompute_fast<__nv_bfloat16, C>(ctx, m->ptr, d, cand, cand_stride, n_cand, x, B, phi, out, out_stride) \
+              : launch_recompute_fast<float, C>(ctx, m->ptr, d, cand, cand_stride, n_cand, x, B, phi, out, out_stride);
+    switch (cpl) {
+      RC(1) RC(2) RC(4) RC(8) RC(16)
+      default: break;
+    }
+#undef RC
+  }
+  const size_t smem = static_cast<size_t>(d) * 4;
+  const dim3 grid(static_cast<unsigned>(ceil_div(n_cand, 128)), static_cast<unsigned>(B));
+  if (m->dtype == HIRE_BF16) {
+    if (smem > 48 * 1024) CK(cudaFuncSetAttribute(recompute_seq<__nv_bfloat16>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    recompute_seq<__nv_bfloat16><<<grid, 128, smem, ctx->stream>>>(static_cast<const __nv_bfloat16*>(m->ptr), d, cand, cand_stride, static_cast<int>(n_cand), x, phi, out, out_stride);
+  } else {
+    if (smem > 48 * 1024) CK(cudaFuncSetAttribute(recompute_seq<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    recompute_seq<float><<<grid, 128, smem, ctx->stream>>>(static_cast<const float*>(m->ptr), d, cand, cand_stride, static_cast<int>(n_cand), x, phi, out, out_stride);
+  }
+  ctx->launches++;
+  CK(cudaGetLastError());
+  return HIRE_OK;
+}
+
+int run_final(hire_ctx ctx, const float* vals, int64_t vs, const uint32_t* idx, int64_t is,
+              const uint64_t* src_keys, int64_t n_per, int64_t part_stride, int64_t n, int64_t K,
+              int64_t B, int out_mode, uint32_t* out_idx, float* out_val, float* out_prob,
+              uint64_t* out_keys, int64_t out_stride) {
+  if (K < 1 || n < 1) return HIRE_OK;
+  if (out_mode == 0 && K > kFinalMax) return invalid("final top-k: k exceeds " + std::to_string(kFinalMax));
+  int64_t P = 1;
+  while (P < K) P <<= 1;
+  const size_t smem = out_mode == 0 ? static_cast<size_t>(P) * 8 : 0;
+  final_select_kernel<<<static_cast<unsigned>(B), kSelectThreads, smem, ctx->stream>>>(
+      vals, vs, idx, is, src_keys, static_cast<int>(std::max<int64_t>(n_per, 1)), part_stride,
+      static_cast<int>(n), static_cast<int>(K), out_mode, out_idx, out_val, out_prob, out_keys, out_stride);
+  ctx->launches++;
+  CK(cudaGetLastError());
+  return HIRE_OK;
+}
+
+__global__ void add_offset_kernel(uint32_t* idx, int64_t n, uint32_t off) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < n) idx[i] += off;
+}
+
+__global__ void add_offset_strided_kernel(uint32_t* s, int64_t stride, int64_t n, int64_t B, uint32_t off) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < n * B) s[(i / n) * stride + i % n] += off;
+}
+
+__global__ void iota_mod_kernel(uint32_t* u, int64_t m, int64_t n) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < n) u[i] = static_cast<uint32_t>(i % m);
+}
+
+__global__ void gather_values_kernel(const float* v, int64_t n, const uint32_t* c, int64_t kk, int64_t B, float* o) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < kk * B) o[i] = v[(i / kk) * n + c[i]];
+}
+
+// FFN helpers for g > 1 -------------------------------------------------------
+__global__ void group_proxy_kernel(const float* scores, int64_t ss, int64_t ngroups, int g, int B,
+                                   float* proxy) {
+  const int64_t id = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (id >= ngroups * B) return;
+  const int64_t b = id / ngroups, j = id % ngroups;
+  float acc = 0.0f;  // ffn.hpp:115-118, ascending t
+  for (int t = 0; t < g; ++t) acc = __fadd_rn(acc, fabsf(scores[b * ss + j * g + t]));
+  proxy[b * ngroups + j] = acc;
+}
+
+__global__ void expand_groups_kernel(const uint32_t* groups, int64_t gs, int64_t n, int g, int B,
+                                     uint32_t* units) {
+  const int64_t id = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (id >= n * g * B) return;
+  const int64_t b = id / (n * g), r = id % (n * g);
+  units[b * n * g + r] = groups[b * gs + r / g] * g + static_cast<uint32_t>(r % g);
+}
+
+__global__ void group_sum_kernel(const float* act, int64_t n, int g, int B, float* out) {
+  const int64_t id = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (id >= n * B) return;
+  const int64_t b = id / n, j = id % n;
+  float acc = 0.0f;  // ffn.hpp:127-129
+  for (int t = 0; t < g; ++t) acc = __fadd_rn(acc, fabsf(act[b * n * g + j * g + t]));
+  out[b * n + j] = acc;
+}
+
+int run_down(hire_ctx ctx, const hire_matrix_s* v, const uint32_t* units, const float* act,
+             int64_t stride, int64_t n_units, int64_t B, int strict, float* partial, float* out) {
+  const int d = static_cast<int>(v->d);
+  const bool bf = v->dtype == HIRE_BF16;
+  if (n_units == 0) {
+    CK(cudaMemsetAsync(out, 0, static_cast<size_t>(B) * d * 4, ctx->stream));
+    return HIRE_OK;
+  }
+  if (strict || (static_cast<int64_t>(d) * static_cast<int64_t>(dtype_size(v->dtype))) % 16 != 0) {
+    const dim3 grid(static_cast<unsigned>(ceil_div(d, 256)), static_cast<unsigned>(B));
+    if (bf) ffn_down_seq<__nv_bfloat16><<<grid, 256, 0, ctx->stream>>>(static_cast<const __nv_bfloat16*>(v->ptr), d, units, act, stride, static_cast<int>(n_units), out);
+    else ffn_down_seq<float><<<grid, 256, 0, ctx->stream>>>(static_cast<const float*>(v->ptr), d, units, act, stride, static_cast<int>(n_units), out);
+    ctx->launches++;
+    CK(cudaGetLastError());
+    return HIRE_OK;
+  }
+  const int ch = 8;
+  const int64_t nch = ceil_div(n_units, ch);
+  const dim3 grid(static_cast<unsigned>(nch), static_cast<unsigned>(B));
+  if (bf) ffn_down_partial<__nv_bfloat16><<<grid, 256, 0, ctx->stream>>>(static_cast<const __nv_bfloat16*>(v->ptr), d, units, act, stride, static_cast<int>(n_units), ch, partial);
+  else ffn_down_partial<float><<<grid, 256, 0, ctx->stream>>>(static_cast<const float*>(v->ptr), d, units, act, stride, static_cast<int>(n_units), ch, partial);
+  ctx->launches++;
+  CK(cudaGetLastError());
+  ffn_down_reduce<<<static_cast<unsigned>(ceil_div(B * d, 256)), 256, 0, ctx->stream>>>(partial, static_cast<int>(nch), d, static_cast<int>(B), out);
+  ctx->launches++;
+  CK(cudaGetLastError());
+  return HIRE_OK;
+}
+
+int validate_topk(const hire_matrix_s* w, const hire_scorer_s* a, int64_t B, const hire_topk_params* p) {
+  if (!w || !a || !p) return invalid("null handle");
+  if (p->k < 1) return invalid("HireConfig: k must be >= 1");
+  if (p->k > p->k_prime)
+    return invalid("HireConfig: k (" + std::to_string(p->k) + ") must be <= k_prime (" + std::to_string(p->k_prime) + ")");
+  RET(check_phi(p->phi));
+  if (a->d != w->d || a->rows != w->rows)
+    return invalid("hire_topk: scorer is " + std::to_string(a->d) + "x" + std::to_string(a->rows) +
+                   " but Z is " + std::to_string(w->d) + "x" + std::to_string(w->rows));
+  if (B < 1) return invalid("hire_topk: batch must be >= 1");
+  if (p->x_mode != HIRE_X_FP32 && p->x_mode != HIRE_X_INT8) return invalid("unknown x_mode");
+  if (p->x_mode == HIRE_X_INT8 && a->kind != HIRE_SCORER_Q4) return invalid("x_mode int8 needs an int4 proxy");
+  return HIRE_OK;
+}
+
+// The local stage of hire_topk: scores -> candidates -> exact values.
+struct TopkWs {
+  ScoreWs sw;
+  float* scores = nullptr;
+  uint64_t* surv = nullptr;
+  uint32_t* cand = nullptr;
+  float* vals = nullptr;
+  int* status = nullptr;
+};
+
+void take_topk_ws(Arena& ar, TopkWs* t, const hire_scorer_s* a, int64_t B, const SelPlan& sp,
+                  bool need_cand) {
+  take_score_ws(ar, &t->sw, a, B);
+  ar.take(&t->scores, static_cast<size_t>(B * a->rows));
+  ar.take(&t->surv, static_cast<size_t>(B) * std::max(sp.n_buckets * sp.t, 1));
+  if (need_cand) ar.take(&t->cand, static_cast<size_t>(B * sp.k_eff));
+  ar.take(&t->vals, static_cast<size_t>(B * sp.k_eff));
+  ar.take(&t->status, 1);
+}
+
+int local_candidates(hire_ctx ctx, const hire_matrix_s* w, const hire_scorer_s* a, const float* x,
+                     int64_t B, const hire_topk_params* p, const SelPlan& sp, const TopkWs& t,
+                     uint32_t* cand) {
+  RET(run_scores(ctx, a, x, B, p->phi, p->x_mode, p->strict, t.sw, t.scores, a->rows));
+  RET(run_select(ctx, t.scores, a->rows, a->rows, B, sp, t.surv, cand, sp.k_eff, t.status));
+  RET(run_recompute(ctx, w, cand, sp.k_eff, sp.k_eff, x, B, p->phi, p->strict, t.vals, sp.k_eff));
+  return HIRE_OK;
+}
+
+}  // namespace
+
+// ====================================================================== ABI
+extern "C" {
+
+const char* hire_last_error(void) { return g_err.c_str(); }
+int hire_abi_version(void) { return HIRE_ABI_VERSION; }
+
+int hire_ctx_create(int device, void* stream, int own_stream, hire_ctx* out) {
+  if (!out) return invalid("null out");
+  CK(cudaSetDevice(device));
+  auto* c = new hire_ctx_s();
+  c->device = device;
+  if (!own_stream) {
+    c->stream = static_cast<cudaStream_t>(stream);
+  } else {
+    cudaError_t e = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
+    if (e != cudaSuccess) {
+      delete c;
+      return set_err(HIRE_ERR_RUNTIME, std::string("cudaStreamCreate: ") + cudaGetErrorString(e));
+    }
+    c->own_stream = true;
+  }
+  cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device);
+  // opt-in shared memory for the selectors
+  CK(cudaFuncSetAttribute(select_candidates_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                          kPoolKeys * 8));
+  CK(cudaFuncSetAttribute(final_select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                          kFinalMax * 8));
+  *out = c;
+  return HIRE_OK;
+}
+
+int hire_ctx_destroy(hire_ctx c) {
+  if (!c) return HIRE_OK;
+  cudaStreamSynchronize(c->stream);
+  if (c->ws) cudaFree(c->ws);
+  if (c->io_dev) cudaFree(c->io_dev);
+  if (c->io_host) cudaFreeHost(c->io_host);
+  if (c->own_stream) cudaStreamDestroy(c->stream);
+  delete c;
+  return HIRE_OK;
+}
+
+int hire_ctx_stream(hire_ctx c, void** s) {
+  if (!c || !s) return invalid("null handle");
+  *s = c->stream;
+  return HIRE_OK;
+}
+
+int hire_ctx_synchronize(hire_ctx c) {
+  if (!c) return invalid("null handle");
+  CK(cudaStreamSynchronize(c->stream));
+  return HIRE_OK;
+}
+
+int64_t hire_ctx_launch_count(hire_ctx c) { return c ? c->launches : 0; }
+
+// ------------------------------------------------------------- matrices --
+int hire_matrix_create(const void* src, int64_t rows, int64_t d, int dtype, int src_on_device,
+                       hire_matrix* out) {
+  if (!out || !src) return invalid("null argument");
+  if (rows < 1 || d < 1) return invalid("ScoreMatrix: rows must be >= 1");
+  if (dtype != HIRE_F32 && dtype != HIRE_BF16) return invalid("unknown dtype");
+  auto* m = new hire_matrix_s();
+  m->rows = rows;
+  m->d = d;
+  m->dtype = dtype;
+  m->owned = true;
+  const size_t bytes = static_cast<size_t>(rows) * d * dtype_size(dtype);
+  cudaError_t e = cudaMalloc(&m->ptr, bytes);
+  if (e == cudaSuccess)
+    e = cudaMemcpy(m->ptr, src, bytes, src_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) {
+    if (m->ptr) cudaFree(m->ptr);
+    delete m;
+    return set_err(HIRE_ERR_RUNTIME, std::string("hire_matrix_create: ") + cudaGetErrorString(e));
+  }
+  *out = m;
+  return HIRE_OK;
+}
+
+int hire_matrix_view(void* ptr, int64_t rows, int64_t d, int dtype, hire_matrix* out) {
+  if (!out || !ptr) return invalid("null argument");
+  if (rows < 1 || d < 1) return invalid("ScoreMatrix: rows must be >= 1");
+  if (dtype != HIRE_F32 && dtype != HIRE_BF16) return invalid("unknown dtype");
+  auto* m = new hire_matrix_s();
+  m->ptr = ptr;
+  m->rows = rows;
+  m->d = d;
+  m->dtype = dtype;
+  m->owned = false;
+  *out = m;
+  return HIRE_OK;
+}
+
+int hire_matrix_slice(hire_matrix m, int64_t first, int64_t count, hire_matrix* out) {
+  if (!m || !out) return invalid("null argument");
+  if (first < 0 || count < 1 || first + count > m->rows) return invalid("ScoreMatrix::slice_cols: out of range");
+  return hire_matrix_view(static_cast<char*>(m->ptr) + first * m->d * dtype_size(m->dtype), count, m->d,
+                          m->dtype, out);
+}
+
+int hire_matrix_destroy(hire_matrix m) {
+  if (!m) return HIRE_OK;
+  if (m->owned && m->ptr) cudaFree(m->ptr);
+  delete m;
+  return HIRE_OK;
+}
+
+int hire_matrix_info(hire_matrix m, int64_t* rows, int64_t* d, int* dtype) {
+  if (!m) return invalid("null handle");
+  if (rows) *rows = m->rows;
+  if (d) *d = m->d;
+  if (dtype) *dtype = m->dtype;
+  return HIRE_OK;
+}
+
+// -------------------------------------------------------------- scorers --
+static int64_t q4_pitch(int64_t d) { return (((d + 1) / 2) + 15) / 16 * 16; }
+
+static int make_q4(const std::vector<uint8_t>& packed_rows, const float* scales, int64_t rows,
+                   int64_t d, hire_scorer* out) {
+  auto* a = new hire_scorer_s();
+  a->kind = HIRE_SCORER_Q4;
+  a->rows = rows;
+  a->d = d;
+  a->pitch = q4_pitch(d);
+  a->owned = true;
+  cudaError_t e = cudaMalloc(&a->codes, static_cast<size_t>(rows) * a->pitch);
+  if (e == cudaSuccess) e = cudaMalloc(&a->scales, static_cast<size_t>(rows) * 4);
+  if (e == cudaSuccess) e = cudaMemcpy(a->codes, packed_rows.data(), packed_rows.size(), cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMemcpy(a->scales, scales, static_cast<size_t>(rows) * 4, cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) {
+    cudaFree(a->codes);
+    cudaFree(a->scales);
+    delete a;
+    return set_err(HIRE_ERR_RUNTIME, std::string("q4 upload: ") + cudaGetErrorString(e));
+  }
+  *out = a;
+  return HIRE_OK;
+}
+
+int hire_scorer_create_q4_codes(const int8_t* codes, const float* scales, int64_t rows, int64_t d,
+                                hire_scorer* out) {
+  if (!codes || !scales || !out) return invalid("null argument");
+  if (rows < 1 || d < 1) return invalid("quantized matrix: dims must be positive");
+  const int64_t pitch = q4_pitch(d);
+  std::vector<uint8_t> buf(static_cast<size_t>(rows * pitch), 0);
+  for (int64_t j = 0; j < rows; ++j)
+    for (int64_t i = 0; i < d; ++i) {
+      const int8_t c = codes[j * d + i];
+      if (c < -7 || c > 7) return invalid("quantized matrix: code outside [-7, 7]");
+      const uint8_t nib = static_cast<uint8_t>(c) & 0x0F;
+      buf[j * pitch + i / 2] |= (i & 1) ? static_cast<uint8_t>(nib << 4) : nib;
+    }
+  return make_q4(buf, scales, rows, d, out);
+}
+
+int hire_scorer_create_q4_hirq(const uint8_t* payload, const float* scales, int64_t rows, int64_t d,
+                               hire_scorer* out) {
+  if (!payload || !scales || !out) return invalid("null argument");
+  if (rows < 1 || d < 1) return invalid("quantized matrix: dims must be positive");
+  const int64_t pitch = q4_pitch(d);
+  std::vector<uint8_t> buf(static_cast<size_t>(rows * pitch), 0);
+  if (d % 2 == 0) {
+    for (int64_t j = 0; j < rows; ++j) std::memcpy(&buf[j * pitch], payload + j * (d / 2), d / 2);
+  } else {
+    for (int64_t j = 0; j < rows; ++j)
+      for (int64_t i = 0; i < d; ++i) {
+        const int64_t s = j * d + i;  // continuous HIRQ stream position
+        const uint8_t nib = (s & 1) ? (payload[s / 2] >> 4) : (payload[s / 2] & 0x0F);
+        buf[j * pitch + i / 2] |= (i & 1) ? static_cast<uint8_t>(nib << 4) : nib;
+      }
+  }
+  return make_q4(buf, scales, rows, d, out);
+}
+
+int hire_scorer_quantize(hire_ctx ctx, hire_matrix w, hire_scorer* out) {
+  if (!ctx || !w || !out) return invalid("null argument");
+  auto* a = new hire_scorer_s();
+  a->kind = HIRE_SCORER_Q4;
+  a->rows = w->rows;
+  a->d = w->d;
+  a->pitch = q4_pitch(w->d);
+  a->owned = true;
+  cudaError_t e = cudaMalloc(&a->codes, static_cast<size_t>(a->rows) * a->pitch);
+  if (e == cudaSuccess) e = cudaMalloc(&a->scales, static_cast<size_t>(a->rows) * 4);
+  if (e != cudaSuccess) {
+    cudaFree(a->codes);
+    delete a;
+    return set_err(HIRE_ERR_RUNTIME, std::string("hire_scorer_quantize: ") + cudaGetErrorString(e));
+  }
+  const unsigned grid = static_cast<unsigned>(ceil_div(w->rows * 32, 256));
+  if (w->dtype == HIRE_BF16)
+    quantize_q4_kernel<__nv_bfloat16><<<grid, 256, 0, ctx->stream>>>(static_cast<const __nv_bfloat16*>(w->ptr), w->rows, static_cast<int>(w->d), a->codes, a->pitch, a->scales);
+  else
+    quantize_q4_kernel<float><<<grid, 256, 0, ctx->stream>>>(static_cast<const float*>(w->ptr), w->rows, static_cast<int>(w->d), a->codes, a->pitch, a->scales);
+  ctx->launches++;
+  e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    cudaFree(a->codes);
+    cudaFree(a->scales);
+    delete a;
+    return set_err(HIRE_ERR_RUNTIME, std::string("quantize_q4_kernel: ") + cudaGetErrorString(e));
+  }
+  *out = a;
+  return HIRE_OK;
+}
+
+int hire_scorer_create_lowrank(const void* z1, const void* z2, int64_t d, int64_t rows, int64_t r,
+                               int dtype, int src_on_device, hire_scorer* out) {
+  if (!z1 || !z2 || !out) return invalid("null argument");
+  if (d < 1 || rows < 1 || r < 1) return invalid("ApproxScorer: low-rank factors do not match rank " + std::to_string(r));
+  if (dtype != HIRE_F32 && dtype != HIRE_BF16) return invalid("unknown dtype");
+  auto* a = new hire_scorer_s();
+  a->kind = HIRE_SCORER_LOWRANK;
+  a->rows = rows;
+  a->d = d;
+  a->r = r;
+  a->dtype = dtype;
+  a->owned = true;
+  const size_t es = dtype_size(dtype);
+  const auto kind = src_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+  cudaError_t e = cudaMalloc(&a->z1, static_cast<size_t>(r) * d * es);
+  if (e == cudaSuccess) e = cudaMalloc(&a->z2, static_cast<size_t>(rows) * r * es);
+  if (e == cudaSuccess) e = cudaMemcpy(a->z1, z1, static_cast<size_t>(r) * d * es, kind);
+  if (e == cudaSuccess) e = cudaMemcpy(a->z2, z2, static_cast<size_t>(rows) * r * es, kind);
+  if (e != cudaSuccess) {
+    cudaFree(a->z1);
+    cudaFree(a->z2);
+    delete a;
+    return set_err(HIRE_ERR_RUNTIME, std::string("low-rank upload: ") + cudaGetErrorString(e));
+  }
+  *out = a;
+  return HIRE_OK;
+}
+
+int hire_scorer_slice(hire_scorer a, int64_t first, int64_t count, hire_scorer* out) {
+  if (!a || !out) return invalid("null argument");
+  if (first < 0 || count < 1 || first + count > a->rows) return invalid("ApproxScorer::slice_cols: out of range");
+  auto* s = new hire_scorer_s(*a);
+  s->owned = false;
+  s->rows = count;
+  if (a->kind == HIRE_SCORER_Q4) {
+    s->codes = a->codes + first * a->pitch;
+    s->scales = a->scales + first;
+  } else {
+    s->z2 = static_cast<char*>(a->z2) + first * a->r * dtype_size(a->dtype);
+  }
+  *out = s;
+  return HIRE_OK;
+}
+
+int hire_scorer_export_q4(hire_scorer a, int8_t* codes, float* scales) {
+  if (!a || !codes || !scales) return invalid("null argument");
+  if (a->kind != HIRE_SCORER_Q4) return invalid("not an int4 scorer");
+  std::vector<uint8_t> buf(static_cast<size_t>(a->rows * a->pitch));
+  CK(cudaDeviceSynchronize());
+  CK(cudaMemcpy(buf.data(), a->codes, buf.size(), cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(scales, a->scales, static_cast<size_t>(a->rows) * 4, cudaMemcpyDeviceToHost));
+  for (int64_t j = 0; j < a->rows; ++j)
+    for (int64_t i = 0; i < a->d; ++i) {
+      const uint8_t b = buf[j * a->pitch + i / 2];
+      const uint8_t nib = (i & 1) ? (b >> 4) : (b & 0x0F);
+      codes[j * a->d + i] = static_cast<int8_t>((nib & 0x08) ? (nib | 0xF0) : nib);
+    }
+  return HIRE_OK;
+}
+
+int hire_scorer_info(hire_scorer a, int* kind, int64_t* rows, int64_t* d, int64_t* rank) {
+  if (!a) return invalid("null handle");
+  if (kind) *kind = a->kind;
+  if (rows) *rows = a->rows;
+  if (d) *d = a->d;
+  if (rank) *rank = a->r;
+  return HIRE_OK;
+}
+
+int hire_scorer_destroy(hire_scorer a) {
+  if (!a) return HIRE_OK;
+  if (a->owned) {
+    cudaFree(a->codes);
+    cudaFree(a->scales);
+    cudaFree(a->z1);
+    cudaFree(a->z2);
+  }
+  delete a;
+  return HIRE_OK;
+}
+
+// ----------------------------------------------------------- primitives --
+int hire_scores(hire_ctx ctx, hire_scorer a, const float* x, int64_t B, int phi, int x_mode,
+                int strict, float* out) {
+  if (!ctx || !a || !x || !out) return invalid("null argument");
+  if (B < 1) return invalid("batch must be >= 1");
+  RET(check_phi(phi));
+  if (x_mode == HIRE_X_INT8 && a->kind != HIRE_SCORER_Q4) return invalid("x_mode int8 needs an int4 proxy");
+  Arena ar;
+  ScoreWs w;
+  take_score_ws(ar, &w, a, B);
+  RET(ar.commit(ctx));
+  return run_scores(ctx, a, x, B, phi, x_mode, strict, w, out, a->rows);
+}
+
+int hire_matvec(hire_ctx ctx, hire_matrix w, const float* x, int64_t B, int phi, int strict, float* out) {
+  if (!ctx || !w || !x || !out) return invalid("null argument");
+  RET(check_phi(phi));
+  return run_recompute(ctx, w, nullptr, 0, w->rows, x, B, phi, strict, out, w->rows);
+}
+
+int hire_topk_select(hire_ctx ctx, const float* v, int64_t B, int64_t n, int64_t k, uint32_t* idx,
+                     float* val, int* clamped) {
+  if (!ctx || !v || !idx || !val) return invalid("null argument");
+  if (k < 1) return invalid("topk_select: k must be >= 1");
+  SelPlan sp;
+  RET(plan_select(n, k, HIRE_SELECT_EXACT, 0, 0, &sp));
+  Arena ar;
+  uint64_t* surv;
+  uint32_t* cand;
+  int* status;
+  float* cv;
+  ar.take(&surv, static_cast<size_t>(B) * std::max(sp.n_buckets * sp.t, 1));
+  ar.take(&cand, static_cast<size_t>(B * sp.k_eff));
+  ar.take(&status, 1);
+  ar.take(&cv, static_cast<size_t>(B * sp.k_eff));
+  RET(ar.commit(ctx));
+  RET(run_select(ctx, v, n, n, B, sp, surv, cand, sp.k_eff, status));
+  gather_values_kernel<<<static_cast<unsigned>(ceil_div(B * sp.k_eff, 256)), 256, 0, ctx->stream>>>(v, n, cand, sp.k_eff, B, cv);
+  ctx->launches++;
+  CK(cudaGetLastError());
+  RET(run_final(ctx, cv, sp.k_eff, cand, sp.k_eff, nullptr, 0, 0, sp.k_eff, sp.k_eff, B, 0, idx, val,
+                nullptr, nullptr, sp.k_eff));
+  if (clamped) *clamped = sp.clamped;
+  return HIRE_OK;
+}
+
+// ------------------------------------------------------------ hire_topk --
+int hire_topk_run(hire_ctx ctx, hire_matrix w, hire_scorer a, const float* x, int64_t B,
+                  const hire_topk_params* p, uint32_t* cand, uint32_t* top_idx, float* top_val,
+                  float* top_prob, int64_t* n_cand, int64_t* n_top, int* clamped) {
+  if (!ctx || !x || !top_idx || !top_val) return invalid("null argument");
+  RET(validate_topk(w, a, B, p));
+  if (top_prob && p->phi != HIRE_PHI_IDENTITY) return invalid("softmax_topk: phi must be identity");
+  SelPlan sp;
+  RET(plan_select(w->rows, p->k_prime, p->select, p->n_buckets, p->bucket_t, &sp));
+  Arena ar;
+  TopkWs t;
+  take_topk_ws(ar, &t, a, B, sp, true);
+  RET(ar.commit(ctx));
+  RET(local_candidates(ctx, w, a, x, B, p, sp, t, t.cand));
+  const int64_t take = std::min<int64_t>(p->k, sp.k_eff);
+  RET(run_final(ctx, t.vals, sp.k_eff, t.cand, sp.k_eff, nullptr, 0, 0, sp.k_eff, take, B, 0, top_idx,
+                top_val, top_prob, nullptr, p->k));
+  if (cand) CK(cudaMemcpy2DAsync(cand, p->k_prime * 4, t.cand, sp.k_eff * 4, sp.k_eff * 4, B,
+                                 cudaMemcpyDeviceToDevice, ctx->stream));
+  if (n_cand) *n_cand = sp.k_eff;
+  if (n_top) *n_top = take;
+  if (clamped) *clamped = sp.clamped || take < p->k;
+  return HIRE_OK;
+}
+
+int hire_topk_host(hire_ctx ctx, hire_matrix w, hire_scorer a, const float* x_host, int64_t B,
+                   const hire_topk_params* p, uint32_t* cand_host, uint32_t* top_idx_host,
+                   float* top_val_host, float* top_prob_host, int64_t* n_cand, int64_t* n_top,
+                   int* clamped) {
+  if (!ctx || !x_host || !top_idx_host || !top_val_host) return invalid("null argument");
+  RET(validate_topk(w, a, B, p));
+  SelPlan sp;
+  RET(plan_select(w->rows, p->k_prime, p->select, p->n_buckets, p->bucket_t, &sp));
+  const int64_t take = std::min<int64_t>(p->k, sp.k_eff);
+  const size_t xb = static_cast<size_t>(B * w->d) * 4;
+  const size_t cb = cand_host ? static_cast<size_t>(B * p->k_prime) * 4 : 0;
+  const size_t tb = static_cast<size_t>(B * p->k) * 4;
+  const size_t pb = top_prob_host ? tb : 0;
+  const size_t in_bytes = align_up(xb);
+  const size_t out_bytes = align_up(cb) + align_up(tb) * 2 + align_up(pb);
+  RET(ensure(&ctx->io_dev, &ctx->io_dev_cap, in_bytes + out_bytes, ctx->stream));
+  RET(ensure_host(&ctx->io_host, &ctx->io_host_cap, in_bytes + out_bytes, ctx->stream));
+  char* dv = static_cast<char*>(ctx->io_dev);
+  char* hs = static_cast<char*>(ctx->io_host);
+  std::memcpy(hs, x_host, xb);
+  CK(cudaMemcpyAsync(dv, hs, xb, cudaMemcpyHostToDevice, ctx->stream));
+  char* o = dv + in_bytes;
+  uint32_t* dcand = cb ? reinterpret_cast<uint32_t*>(o) : nullptr;
+  o += align_up(cb);
+  uint32_t* didx = reinterpret_cast<uint32_t*>(o);
+  o += align_up(tb);
+  float* dval = reinterpret_cast<float*>(o);
+  o += align_up(tb);
+  float* dprob = pb ? reinterpret_cast<float*>(o) : nullptr;
+  RET(hire_topk_run(ctx, w, a, reinterpret_cast<const float*>(dv), B, p, dcand, didx, dval, dprob,
+                    n_cand, n_top, clamped));
+  CK(cudaMemcpyAsync(hs + in_bytes, dv + in_bytes, out_bytes, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  const char* ho = hs + in_bytes;
+  (void)take;
+  if (cb) std::memcpy(cand_host, ho, cb);
+  ho += align_up(cb);
+  std::memcpy(top_idx_host, ho, tb);
+  ho += align_up(tb);
+  std::memcpy(top_val_host, ho, tb);
+  ho += align_up(tb);
+  if (pb) std::memcpy(top_prob_host, ho, pb);
+  return HIRE_OK;
+}
+
+// ------------------------------------------------------------------ FFN --
+namespace {
+int validate_ffn(const hire_matrix_s* u, const hire_matrix_s* v, const hire_scorer_s* a, int64_t B,
+                 const hire_ffn_params* p) {
+  if (!u || !v || !a || !p) return invalid("null handle");
+  if (u->rows != v->rows || u->d != v->d) return invalid("GroupedFFN: U and V must both be d x m");
+  const int64_t g = p->group_size, m = u->rows;
+  if (g < 1) return invalid("GroupedFFN: group size must be >= 1");
+  if (m % g != 0) return invalid("GroupedFFN: g = " + std::to_string(g) + " must divide m = " + std::to_string(m));
+  if (p->k < 1 || p->k % g != 0) return invalid("ffn_group_sparse: g = " + std::to_string(g) + " must divide k = " + std::to_string(p->k));
+  if (p->k_prime % g != 0) return invalid("ffn_group_sparse: g = " + std::to_string(g) + " must divide k_prime = " + std::to_string(p->k_prime));
+  if (p->k > p->k_prime || p->k_prime > m)
+    return invalid("ffn_group_sparse: need k <= k_prime <= m, got k = " + std::to_string(p->k) +
+                   ", k_prime = " + std::to_string(p->k_prime) + ", m = " + std::to_string(m));
+  if (a->rows != m || a->d != u->d)
+    return invalid("group_proxy: scorer covers " + std::to_string(a->rows) + " units but FFN has " + std::to_string(m));
+  RET(check_phi(p->phi));
+  if (B < 1) return invalid("batch must be >= 1");
+  if (p->x_mode == HIRE_X_INT8 && a->kind != HIRE_SCORER_Q4) return invalid("x_mode int8 needs an int4 proxy");
+  return HIRE_OK;
+}
+
+struct FfnWs {
+  TopkWs t;
+  float* proxy = nullptr;
+  uint32_t* cand = nullptr;
+  uint32_t* units = nullptr;
+  float* act = nullptr;
+  float* gval = nullptr;
+  uint32_t* selg = nullptr;
+  float* selv = nullptr;
+  uint32_t* selu = nullptr;
+  float* selact = nullptr;
+  float* partial = nullptr;
+};
+
+// Local select_groups + the exact activations of the selected units. Writes
+// selected group ids (ascending) into `sel` [B][kg] (stride kg) and returns
+// units/activations for the down-projection in fw.selu/fw.selact [B][kg*g].
+int ffn_select(hire_ctx ctx, const hire_matrix_s* u, const hire_scorer_s* a, const float* x,
+               int64_t B, int64_t g, int64_t kg, int64_t kpg, int phi, int x_mode, int strict,
+               const SelPlan& sp, FfnWs& fw, uint32_t* sel, int64_t sel_stride) {
+  const int64_t m = u->rows, ng = m / g;
+  RET(run_scores(ctx, a, x, B, phi, x_mode, strict, fw.t.sw, fw.t.scores, m));
+  const float* proxy = fw.t.scores;
+  if (g > 1) {
+    group_proxy_kernel<<<static_cast<unsigned>(ceil_div(ng * B, 256)), 256, 0, ctx->stream>>>(fw.t.scores, m, ng, static_cast<int>(g), static_cast<int>(B), fw.proxy);
+    ctx->launches++;
+    CK(cudaGetLastError());
+    proxy = fw.proxy;
+  }
+  RET(run_select(ctx, proxy, g > 1 ? ng : m, ng, B, sp, fw.t.surv, fw.cand, kpg, fw.t.status));
+  if (g == 1) {
+    RET(run_recompute(ctx, u, fw.cand, kpg, kpg, x, B, phi, strict, fw.act, kpg));
+    // top-k by exact activation, emitted in ascending unit order with values
+    RET(run_final(ctx, fw.act, kpg, fw.cand, kpg, nullptr, 0, 0, kpg, kg, B, 1, sel, fw.selact,
+                  nullptr, nullptr, sel_stride));
+    return HIRE_OK;
+  }
+  expand_groups_kernel<<<static_cast<unsigned>(ceil_div(kpg * g * B, 256)), 256, 0, ctx->stream>>>(fw.cand, kpg, kpg, static_cast<int>(g), static_cast<int>(B), fw.units);
+  ctx->launches++;
+  CK(cudaGetLastError());
+  RET(run_recompute(ctx, u, fw.units, kpg * g, kpg * g, x, B, phi, strict, fw.act, kpg * g));
+  group_sum_kernel<<<static_cast<unsigned>(ceil_div(kpg * B, 256)), 256, 0, ctx->stream>>>(fw.act, kpg, static_cast<int>(g), static_cast<int>(B), fw.gval);
+  ctx->launches++;
+  CK(cudaGetLastError());
+  RET(run_final(ctx, fw.gval, kpg, fw.cand, kpg, nullptr, 0, 0, kpg, kg, B, 1, sel, fw.selv, nullptr,
+                nullptr, sel_stride));
+  expand_groups_kernel<<<static_cast<unsigned>(ceil_div(kg * g * B, 256)), 256, 0, ctx->stream>>>(sel, sel_stride, kg, static_cast<int>(g), static_cast<int>(B), fw.selu);
+  ctx->launches++;
+  CK(cudaGetLastError());
+  RET(run_recompute(ctx, u, fw.selu, kg * g, kg * g, x, B, phi, strict, fw.selact, kg * g));
+  return HIRE_OK;
+}
+
+void take_ffn_ws(Arena& ar, FfnWs* fw, const hire_scorer_s* a, int64_t B, int64_t m, int64_t d,
+                 int64_t g, int64_t kg, int64_t kpg, const SelPlan& sp, int64_t max_chunks) {
+  take_score_ws(ar, &fw->t.sw, a, B);
+  ar.take(&fw->t.scores, static_cast<size_t>(B * m));
+  ar.take(&fw->t.surv, static_cast<size_t>(B) * std::max(sp.n_buckets * sp.t, 1));
+  ar.take(&fw->t.status, 1);
+  ar.take(&fw->proxy, static_cast<size_t>(B * (m / g)));
+  ar.take(&fw->cand, static_cast<size_t>(B * kpg));
+  ar.take(&fw->units, static_cast<size_t>(B * kpg * g));
+  ar.take(&fw->act, static_cast<size_t>(B * kpg * g));
+  ar.take(&fw->gval, static_cast<size_t>(B * kpg));
+  ar.take(&fw->selv, static_cast<size_t>(B * kg));
+  ar.take(&fw->selu, static_cast<size_t>(B * kg * g));
+  ar.take(&fw->selact, static_cast<size_t>(B * kg * g));
+  ar.take(&fw->partial, static_cast<size_t>(B * std::max<int64_t>(max_chunks, 1) * d));
+}
+}  // namespace
+
+int hire_ffn_run(hire_ctx ctx, hire_matrix u, hire_matrix v, hire_scorer a, const float* x, int64_t B,
+                 const hire_ffn_params* p, uint32_t* sel, float* out) {
+  if (!ctx || !x || !sel || !out) return invalid("null argument");
+  RET(validate_ffn(u, v, a, B, p));
+  const int64_t g = p->group_size, m = u->rows, kg = p->k / g, kpg = p->k_prime / g;
+  SelPlan sp;
+  RET(plan_select(m / g, kpg, HIRE_SELECT_EXACT, 0, 0, &sp));
+  Arena ar;
+  FfnWs fw;
+  take_ffn_ws(ar, &fw, a, B, m, u->d, g, kg, kpg, sp, ceil_div(kg * g, 8));
+  RET(ar.commit(ctx));
+  RET(ffn_select(ctx, u, a, x, B, g, kg, kpg, p->phi, p->x_mode, p->strict, sp, fw, sel, kg));
+  const uint32_t* units = g == 1 ? sel : fw.selu;
+  RET(run_down(ctx, v, units, fw.selact, kg * g, kg * g, B, p->strict, fw.partial, out));
+  return HIRE_OK;
+}
+
+int hire_ffn_host(hire_ctx ctx, hire_matrix u, hire_matrix v, hire_scorer a, const float* x_host,
+                  int64_t B, const hire_ffn_params* p, uint32_t* sel_host, float* out_host) {
+  if (!ctx || !x_host || !out_host) return invalid("null argument");
+  RET(validate_ffn(u, v, a, B, p));
+  const int64_t kg = p->k / p->group_size;
+  const size_t xb = static_cast<size_t>(B * u->d) * 4;
+  const size_t sb = static_cast<size_t>(B * kg) * 4;
+  const size_t ob = static_cast<size_t>(B * u->d) * 4;
+  const size_t in_bytes = align_up(xb), out_bytes = align_up(sb) + align_up(ob);
+  RET(ensure(&ctx->io_dev, &ctx->io_dev_cap, in_bytes + out_bytes, ctx->stream));
+  RET(ensure_host(&ctx->io_host, &ctx->io_host_cap, in_bytes + out_bytes, ctx->stream));
+  char* dv = static_cast<char*>(ctx->io_dev);
+  char* hs = static_cast<char*>(ctx->io_host);
+  std::memcpy(hs, x_host, xb);
+  CK(cudaMemcpyAsync(dv, hs, xb, cudaMemcpyHostToDevice, ctx->stream));
+  uint32_t* dsel = reinterpret_cast<uint32_t*>(dv + in_bytes);
+  float* dout = reinterpret_cast<float*>(dv + in_bytes + align_up(sb));
+  RET(hire_ffn_run(ctx, u, v, a, reinterpret_cast<const float*>(dv), B, p, dsel, dout));
+  CK(cudaMemcpyAsync(hs + in_bytes, dv + in_bytes, out_bytes, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  if (sel_host) std::memcpy(sel_host, hs + in_bytes, sb);
+  std::memcpy(out_host, hs + in_bytes + align_up(sb), ob);
+  return HIRE_OK;
+}
+
+int hire_ffn_dense_run(hire_ctx ctx, hire_matrix u, hire_matrix v, const float* x, int64_t B, int phi,
+                       int strict, float* out) {
+  if (!ctx || !u || !v || !x || !out) return invalid("null argument");
+  if (u->rows != v->rows || u->d != v->d) return invalid("GroupedFFN: U and V must both be d x m");
+  RET(check_phi(phi));
+  const int64_t m = u->rows;
+  Arena ar;
+  float* act;
+  uint32_t* units;
+  float* partial;
+  ar.take(&act, static_cast<size_t>(B * m));
+  ar.take(&units, static_cast<size_t>(B * m));
+  ar.take(&partial, static_cast<size_t>(B * ceil_div(m, 8) * u->d));
+  RET(ar.commit(ctx));
+  RET(run_recompute(ctx, u, nullptr, 0, m, x, B, phi, strict, act, m));
+  iota_mod_kernel<<<static_cast<unsigned>(ceil_div(B * m, 256)), 256, 0, ctx->stream>>>(units, m, B * m);
+  ctx->launches++;
+  CK(cudaGetLastError());
+  return run_down(ctx, v, units, act, m, m, B, strict, partial, out);
+}
+
+// ------------------------------------------------------------------- DA --
+int hire_comm_unique_id(uint8_t id[128]) {
+  ncclUniqueId u;
+  CKN(ncclGetUniqueId(&u));
+  std::memcpy(id, u.internal, 128);
+  return HIRE_OK;
+}
+
+int hire_comm_create(const uint8_t id[128], int world, int rank, hire_comm* out) {
+  if (!out || world < 1 || rank < 0 || rank >= world) return invalid("bad communicator arguments");
+  ncclUniqueId u;
+  std::memcpy(u.internal, id, 128);
+  auto* c = new hire_comm_s();
+  c->world = world;
+  c->rank = rank;
+  ncclResult_t r = ncclCommInitRank(&c->comm, world, u, rank);
+  if (r != ncclSuccess) {
+    delete c;
+    return set_err(HIRE_ERR_RUNTIME, std::string("ncclCommInitRank: ") + ncclGetErrorString(r));
+  }
+  *out = c;
+  return HIRE_OK;
+}
+
+int hire_comm_destroy(hire_comm c) {
+  if (!c) return HIRE_OK;
+  ncclCommDestroy(c->comm);
+  delete c;
+  return HIRE_OK;
+}
+
+namespace {
+int64_t quota(int64_t k, int64_t s, int64_t i) { return k / s + (i < k % s ? 1 : 0); }
+
+struct DaPlan {
+  int64_t kl = 0, kpl = 0;     // this shard's quotas
+  int64_t kq_max = 0;          // per-rank send slots
+  SelPlan sp;
+};
+
+int plan_da(const hire_topk_params* p, int64_t width, int world, int rank, int merge, int uneven,
+            DaPlan* dp) {
+  if (world < 1) return invalid("da_topk: no shards");
+  if (!uneven && p->k % world != 0)
+    return invalid("da_topk: s = " + std::to_string(world) + " must divide k = " + std::to_string(p->k));
+  if (!uneven && p->k_prime % world != 0)
+    return invalid("da_topk: s = " + std::to_string(world) + " must divide k_prime = " + std::to_string(p->k_prime));
+  dp->kl = quota(p->k, world, rank);
+  dp->kpl = quota(p->k_prime, world, rank);
+  if (dp->kl > width)
+    return invalid("da_topk: per-shard quota k/s = " + std::to_string(dp->kl) + " exceeds shard width " + std::to_string(width));
+  RET(plan_select(width, dp->kpl, p->select, p->n_buckets, p->bucket_t, &dp->sp));
+  dp->kq_max = merge == HIRE_MERGE_PER_SHARD ? ceil_div(p->k, world) : ceil_div(p->k_prime, world);
+  return HIRE_OK;
+}
+
+// One shard's local stage; writes keys (global indices) into send [B][kq_max].
+int da_local(hire_ctx ctx, const hire_matrix_s* w, const hire_scorer_s* a, int64_t offset,
+             const float* x, int64_t B, const hire_topk_params* p, const DaPlan& dp, int merge,
+             uint64_t* send) {
+  Arena ar;
+  TopkWs t;
+  take_topk_ws(ar, &t, a, B, dp.sp, true);
+  RET(ar.commit(ctx));
+  RET(local_candidates(ctx, w, a, x, B, p, dp.sp, t, t.cand));
+  if (offset) {
+    add_offset_kernel<<<static_cast<unsigned>(ceil_div(B * dp.sp.k_eff, 256)), 256, 0, ctx->stream>>>(t.cand, B * dp.sp.k_eff, static_cast<uint32_t>(offset));
+    ctx->launches++;
+    CK(cudaGetLastError());
+  }
+  const int64_t K = merge == HIRE_MERGE_PER_SHARD ? std::min(dp.kl, dp.sp.k_eff) : dp.sp.k_eff;
+  if (K < 1) {
+    CK(cudaMemsetAsync(send, 0, static_cast<size_t>(B * dp.kq_max) * 8, ctx->stream));
+    return HIRE_OK;
+  }
+  return run_final(ctx, t.vals, dp.sp.k_eff, t.cand, dp.sp.k_eff, nullptr, 0, 0, dp.sp.k_eff, K, B, 2,
+                   nullptr, nullptr, nullptr, send, dp.kq_max);
+}
+
+int64_t da_total_k(const hire_topk_params* p, int64_t total_rows, int world, int merge, int uneven,
+                   bool* clamped) {
+  int64_t tot = 0, kp_tot = 0;
+  *clamped = false;
+  for (int r = 0; r < world; ++r) {
+    int64_t f, wdt;
+    part_range(total_rows, world, r, &f, &wdt);
+    const int64_t kpl = quota(p->k_prime, world, r), kl = quota(p->k, world, r);
+    const int64_t keff = std::min(kpl, wdt);
+    if (kpl > wdt) *clamped = true;
+    kp_tot += keff;
+    tot += std::min(kl, keff);
+  }
+  (void)uneven;
+  if (merge == HIRE_MERGE_GLOBAL) {
+    if (kp_tot < p->k) *clamped = true;
+    return std::min(p->k, kp_tot);
+  }
+  return tot;
+}
+}  // namespace
+
+int hire_da_topk_run(hire_ctx ctx, hire_comm comm, hire_matrix w, hire_scorer a, int64_t total_rows,
+                     int world, int rank, const float* x, int64_t B, const hire_topk_params* p,
+                     int merge, int uneven, uint32_t* top_idx, float* top_val, int64_t* n_top,
+                     int* clamped) {
+  if (!ctx || !x || !top_idx || !top_val) return invalid("null argument");
+  if (comm && (comm->world != world || comm->rank != rank)) return invalid("communicator does not match world/rank");
+  if (!comm && world != 1) return invalid("da_topk: world > 1 needs a communicator");
+  hire_topk_params lp = *p;
+  lp.k = std::max<int64_t>(1, quota(p->k, world, rank));
+  lp.k_prime = std::max(lp.k, quota(p->k_prime, world, rank));
+  RET(validate_topk(w, a, B, &lp));
+  int64_t first, width;
+  part_range(total_rows, world, rank, &first, &width);
+  if (w->rows != width) return invalid("da_topk: shard has " + std::to_string(w->rows) + " rows, width rule says " + std::to_string(width));
+  DaPlan dp;
+  RET(plan_da(p, width, world, rank, merge, uneven, &dp));
+  // send/recv keys live in io_dev (separate from the per-stage workspace)
+  const size_t sendb = align_up(static_cast<size_t>(B * dp.kq_max) * 8);
+  const size_t recvb = align_up(static_cast<size_t>(world * B * dp.kq_max) * 8);
+  RET(ensure(&ctx->io_dev, &ctx->io_dev_cap, sendb + recvb, ctx->stream));
+  uint64_t* send = static_cast<uint64_t*>(ctx->io_dev);
+  uint64_t* recv = reinterpret_cast<uint64_t*>(static_cast<char*>(ctx->io_dev) + sendb);
+  RET(da_local(ctx, w, a, first, x, B, p, dp, merge, world == 1 ? recv : send));
+  if (world > 1) {
+    CKN(ncclAllGather(send, recv, static_cast<size_t>(B * dp.kq_max), ncclUint64, comm->comm, ctx->stream));
+  }
+  bool cl = false;
+  const int64_t K = da_total_k(p, total_rows, world, merge, uneven, &cl);
+  RET(run_final(ctx, nullptr, 0, nullptr, 0, recv, dp.kq_max, B * dp.kq_max, world * dp.kq_max, K, B,
+                0, top_idx, top_val, nullptr, nullptr, p->k));
+  if (n_top) *n_top = K;
+  if (clamped) *clamped = cl;
+  return HIRE_OK;
+}
+
+int hire_da_topk_emulated(hire_ctx ctx, hire_matrix w, hire_scorer a, int world, const float* x,
+                          int64_t B, const hire_topk_params* p, int merge, int uneven,
+                          uint32_t* top_idx, float* top_val, int64_t* n_top, int* clamped) {
+  if (!ctx || !x || !top_idx || !top_val) return invalid("null argument");
+  RET(validate_topk(w, a, B, p));
+  if (world < 1 || world > w->rows) return invalid("shard: s = " + std::to_string(world) + " exceeds l = " + std::to_string(w->rows));
+  int64_t kq_max = 0;
+  std::vector<DaPlan> plans(world);
+  for (int r = 0; r < world; ++r) {
+    int64_t f, wd;
+    part_range(w->rows, world, r, &f, &wd);
+    RET(plan_da(p, wd, world, r, merge, uneven, &plans[r]));
+    kq_max = plans[r].kq_max;
+  }
+  const size_t recvb = align_up(static_cast<size_t>(world * B * kq_max) * 8);
+  RET(ensure(&ctx->io_dev, &ctx->io_dev_cap, recvb, ctx->stream));
+  uint64_t* recv = static_cast<uint64_t*>(ctx->io_dev);
+  for (int r = 0; r < world; ++r) {
+    int64_t f, wd;
+    part_range(w->rows, world, r, &f, &wd);
+    hire_matrix ws;
+    hire_scorer as;
+    RET(hire_matrix_slice(w, f, wd, &ws));
+    RET(hire_scorer_slice(a, f, wd, &as));
+    const int rc = da_local(ctx, ws, as, f, x, B, p, plans[r], merge, recv + static_cast<int64_t>(r) * B * kq_max);
+    hire_matrix_destroy(ws);
+    hire_scorer_destroy(as);
+    RET(rc);
+  }
+  bool cl = false;
+  const int64_t K = da_total_k(p, w->rows, world, merge, uneven, &cl);
+  RET(run_final(ctx, nullptr, 0, nullptr, 0, recv, kq_max, B * kq_max, world * kq_max, K, B, 0, top_idx,
+                top_val, nullptr, nullptr, p->k));
+  if (n_top) *n_top = K;
+  if (clamped) *clamped = cl;
+  return HIRE_OK;
+}
+
+// DA FFN ------------------------------------------------------------------
+namespace {
+struct DaFfnPlan {
+  int64_t kgl = 0, kpl = 0, kg_max = 0;
+  SelPlan sp;
+};
+
+int plan_da_ffn(const hire_ffn_params* p, int64_t total_units, int64_t width_groups, int world, int rank,
+                int uneven, DaFfnPlan* fp) {
+  const int64_t g = p->group_size;
+  const int64_t kg = p->k / g, kpg = p->k_prime / g;
+  if (world < 1) return invalid("da_group_sparse: s must be >= 1");
+  if (world > total_units / g)
+    return invalid("da_group_sparse: s = " + std::to_string(world) + " exceeds group count " + std::to_string(total_units / g));
+  if (!uneven && kg % world != 0)
+    return invalid("da_group_sparse: s = " + std::to_string(world) + " must divide the group quota k/g = " + std::to_string(kg));
+  if (!uneven && kpg % world != 0)
+    return invalid("da_group_sparse: s = " + std::to_string(world) + " must divide the candidate quota k_prime/g = " + std::to_string(kpg));
+  fp->kgl = quota(kg, world, rank);
+  fp->kpl = std::min(quota(kpg, world, rank), width_groups);  // distributed.hpp:192
+  if (fp->kgl > width_groups)
+    return invalid("da_group_sparse: per-shard quota " + std::to_string(fp->kgl) + " exceeds shard group count " + std::to_string(width_groups));
+  fp->kg_max = ceil_div(kg, world);
+  return plan_select(width_groups, fp->kpl, HIRE_SELECT_EXACT, 0, 0, &fp->sp);
+}
+
+__global__ void concat_sel_kernel(const uint32_t* recv, int world, int64_t B, int64_t kg_max,
+                                  const int64_t* counts, int64_t kg, uint32_t* sel) {
+  // counts[r] valid entries per rank (same for every query); rank-major
+  // concatenation of ascending shard-local lists is globally ascending.
+  const int64_t b = blockIdx.x;
+  int64_t pos = 0;
+  for (int r = 0; r < world; ++r) {
+    const int64_t c = counts[r];
+    for (int64_t i = threadIdx.x; i < c; i += blockDim.x)
+      sel[b * kg + pos + i] = recv[(r * B + b) * kg_max + i];
+    pos += c;
+  }
+}
+
+// local stage of da_group_sparse: selection with local quotas on this
+// shard, global group ids, partial down-projection into out_partial.
+int da_ffn_local(hire_ctx ctx, const hire_matrix_s* u, const hire_matrix_s* v, const hire_scorer_s* a,
+                 int64_t first_group, const float* x, int64_t B, const hire_ffn_params* p,
+                 const DaFfnPlan& fp, uint32_t* sel_out, int64_t sel_stride, float* out_partial) {
+  const int64_t g = p->group_size, m = u->rows;
+  Arena ar;
+  FfnWs fw;
+  take_ffn_ws(ar, &fw, a, B, m, u->d, g, fp.kgl, fp.kpl, fp.sp, ceil_div(fp.kgl * g, 8));
+  uint32_t* sel_local;
+  ar.take(&sel_local, static_cast<size_t>(B * std::max<int64_t>(fp.kgl, 1)));
+  RET(ar.commit(ctx));
+  if (fp.kgl == 0 || fp.kpl == 0) {
+    CK(cudaMemsetAsync(out_partial, 0, static_cast<size_t>(B * u->d) * 4, ctx->stream));
+    return HIRE_OK;
+  }
+  RET(ffn_select(ctx, u, a, x, B, g, fp.kgl, fp.kpl, p->phi, p->x_mode, p->strict, fp.sp, fw, sel_local, fp.kgl));
+  const uint32_t* units = g == 1 ? sel_local : fw.selu;
+  RET(run_down(ctx, v, units, fw.selact, fp.kgl * g, fp.kgl * g, B, p->strict, fw.partial, out_partial));
+  // global group ids into the send slots (padded rows untouched)
+  CK(cudaMemcpy2DAsync(sel_out, sel_stride * 4, sel_local, fp.kgl * 4, fp.kgl * 4, B, cudaMemcpyDeviceToDevice, ctx->stream));
+  if (first_group) {
+    add_offset_strided_kernel<<<static_cast<unsigned>(ceil_div(fp.kgl * B, 256)), 256, 0, ctx->stream>>>(sel_out, sel_stride, fp.kgl, B, static_cast<uint32_t>(first_group));
+    ctx->launches++;
+    CK(cudaGetLastError());
+  }
+  return HIRE_OK;
+}
+
+__global__ void sum_parts_kernel(const float* parts, int world, int64_t n, float* out) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  float s = 0.0f;
+  for (int r = 0; r < world; ++r) s = __fadd_rn(s, parts[r * n + i]);
+  out[i] = s;
+}
+}  // namespace
+
+int hire_da_ffn_run(hire_ctx ctx, hire_comm comm, hire_matrix u, hire_matrix v, hire_scorer a,
+                    int64_t total_units, int world, int rank, const float* x, int64_t B,
+                    const hire_ffn_params* p, int uneven, uint32_t* sel, float* out) {
+  if (!ctx || !u || !v || !a || !p || !x || !sel || !out) return invalid("null argument");
+  if (comm && (comm->world != world || comm->rank != rank)) return invalid("communicator does not match world/rank");
+  if (!comm && world != 1) return invalid("da_group_sparse: world > 1 needs a communicator");
+  const int64_t g = p->group_size;
+  if (g < 1 || total_units % g != 0) return invalid("GroupedFFN: g must divide m");
+  const int64_t ng = total_units / g;
+  int64_t fg, wg;
+  part_range(ng, world, rank, &fg, &wg);
+  if (u->rows != wg * g) return invalid("da_group_sparse: shard unit count does not match the width rule");
+  DaFfnPlan fp;
+  RET(plan_da_ffn(p, total_units, wg, world, rank, uneven, &fp));
+  hire_ffn_params lp = *p;
+  lp.k = std::max<int64_t>(1, fp.kgl) * g;
+  lp.k_prime = std::max<int64_t>(lp.k, fp.kpl * g);
+  if (fp.kgl > 0) RET(validate_ffn(u, v, a, B, &lp));
+  const int64_t kg = p->k / g;
+  const size_t sendb = align_up(static_cast<size_t>(B * fp.kg_max) * 4);
+  const size_t recvb = align_up(static_cast<size_t>(world * B * fp.kg_max) * 4);
+  const size_t cntb = align_up(static_cast<size_t>(world) * 8);
+  RET(ensure(&ctx->io_dev, &ctx->io_dev_cap, sendb + recvb + cntb, ctx->stream));
+  uint32_t* send = static_cast<uint32_t*>(ctx->io_dev);
+  uint32_t* recv = reinterpret_cast<uint32_t*>(static_cast<char*>(ctx->io_dev) + sendb);
+  int64_t* cnt = reinterpret_cast<int64_t*>(static_cast<char*>(ctx->io_dev) + sendb + recvb);
+  RET(da_ffn_local(ctx, u, v, a, fg, x, B, p, fp, world == 1 ? recv : send, fp.kg_max, out));
+  if (world > 1) {
+    CKN(ncclGroupStart());
+    CKN(ncclAllGather(send, recv, static_cast<size_t>(B * fp.kg_max), ncclUint32, comm->comm, ctx->stream));
+    CKN(ncclAllReduce(out, out, static_cast<size_t>(B * u->d), ncclFloat32, ncclSum, comm->comm, ctx->stream));
+    CKN(ncclGroupEnd());
+  }
+  std::vector<int64_t> counts(world);
+  int64_t total = 0;
+  for (int r = 0; r < world; ++r) {
+    int64_t f2, w2;
+    part_range(ng, world, r, &f2, &w2);
+    counts[r] = std::min(quota(kg, world, r), w2);
+    total += counts[r];
+  }
+  CK(cudaMemcpyAsync(cnt, counts.data(), world * 8, cudaMemcpyHostToDevice, ctx->stream));
+  concat_sel_kernel<<<static_cast<unsigned>(B), 128, 0, ctx->stream>>>(recv, world, B, fp.kg_max, cnt, total, sel);
+  ctx->launches++;
+  CK(cudaGetLastError());
+  CK(cudaStreamSynchronize(ctx->stream));  // counts is a pageable host vector
+  return HIRE_OK;
+}
+
+int hire_da_ffn_emulated(hire_ctx ctx, hire_matrix u, hire_matrix v, hire_scorer a, int world,
+                         const float* x, int64_t B, const hire_ffn_params* p, int uneven, uint32_t* sel,
+                         float* out) {
+  if (!ctx || !u || !v || !a || !p || !x || !sel || !out) return invalid("null argument");
+  RET(validate_ffn(u, v, a, B, p));
+  const int64_t g = p->group_size, ng = u->rows / g, kg = p->k / g;
+  std::vector<DaFfnPlan> plans(world);
+  for (int r = 0; r < world; ++r) {
+    int64_t f, w;
+    part_range(ng, world, r, &f, &w);
+    RET(plan_da_ffn(p, u->rows, w, world, r, uneven, &plans[r]));
+  }
+  const int64_t kg_max = plans[0].kg_max;
+  const size_t recvb = align_up(static_cast<size_t>(world * B * kg_max) * 4);
+  const size_t partb = align_up(static_cast<size_t>(world * B * u->d) * 4);
+  const size_t cntb = align_up(static_cast<size_t>(world) * 8);
+  RET(ensure(&ctx->io_dev, &ctx->io_dev_cap, recvb + partb + cntb, ctx->stream));
+  uint32_t* recv = static_cast<uint32_t*>(ctx->io_dev);
+  float* parts = reinterpret_cast<float*>(static_cast<char*>(ctx->io_dev) + recvb);
+  int64_t* cnt = reinterpret_cast<int64_t*>(static_cast<char*>(ctx->io_dev) + recvb + partb);
+  std::vector<int64_t> counts(world);
+  int64_t total = 0;
+  for (int r = 0; r < world; ++r) {
+    int64_t fgr, wg;
+    part_range(ng, world, r, &fgr, &wg);
+    hire_matrix us, vs;
+    hire_scorer as;
+    RET(hire_matrix_slice(u, fgr * g, wg * g, &us));
+    RET(hire_matrix_slice(v, fgr * g, wg * g, &vs));
+    RET(hire_scorer_slice(a, fgr * g, wg * g, &as));
+    const int rc = da_ffn_local(ctx, us, vs, as, fgr, x, B, p, plans[r],
+                                recv + static_cast<int64_t>(r) * B * kg_max, kg_max,
+                                parts + static_cast<int64_t>(r) * B * u->d);
+    hire_matrix_destroy(us);
+    hire_matrix_destroy(vs);
+    hire_scorer_destroy(as);
+    RET(rc);
+    counts[r] = std::min(quota(kg, world, r), wg);
+    total += counts[r];
+  }
+  CK(cudaMemcpyAsync(cnt, counts.data(), world * 8, cudaMemcpyHostToDevice, ctx->stream));
+  concat_sel_kernel<<<static_cast<unsigned>(B), 128, 0, ctx->stream>>>(recv, world, B, kg_max, cnt, total, sel);
+  ctx->launches++;
+  CK(cudaGetLastError());
+  if (p->strict) {
+    // the reference's own order: one ascending sum over the union
+    Arena ar;
+    uint32_t* units;
+    float* act;
+    ar.take(&units, static_cast<size_t>(B * total * g));
+    ar.take(&act, static_cast<size_t>(B * total * g));
+    RET(ar.commit(ctx));
+    expand_groups_kernel<<<static_cast<unsigned>(ceil_div(total * g * B, 256)), 256, 0, ctx->stream>>>(sel, total, total, static_cast<int>(g), static_cast<int>(B), units);
+    ctx->launches++;
+    RET(run_recompute(ctx, u, units, total * g, total * g, x, B, p->phi, 1, act, total * g));
+    RET(run_down(ctx, v, units, act, total * g, total * g, B, 1, nullptr, out));
+  } else {
+    sum_parts_kernel<<<static_cast<unsigned>(ceil_div(B * u->d, 256)), 256, 0, ctx->stream>>>(parts, world, B * u->d, out);
+    ctx->launches++;
+    CK(cudaGetLastError());
+  }
+  CK(cudaStreamSynchronize(ctx->stream));
+  return HIRE_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,397 @@
+// score.cuh — compressed-proxy scorers (K1 int4, K2 low-rank), the x
+// quantiser for the integer mode and the on-device int4 proxy build (K9).
+//
+// Reference semantics being replaced:
+//   ApproxScorer::scores  /root/reference/proj/include/hire/approx.hpp:382-411
+//     quantized branch :395-403  s_j = phi(sum_i (code_ji*scale_j)*x_i)
+//     low-rank branch  :477-496  t = Z1^T x ; s_j = phi(sum_q Z2[j,q] t_q)
+//   quantize_int4       approx.hpp:49-65
+//
+// Device layouts:
+//   int4 proxy  : uint8 [rows][pitch], pitch = round_up(ceil(d/2), 16);
+//                 two codes per byte, low nibble = even column (the HIRQ
+//                 packing of approx.hpp:551-564, one row per reference column)
+//   scales      : fp32 [rows]
+//   low-rank Z1 : T [r][d]   (reference z1 columns, byte-identical)
+//   low-rank Z2 : T [rows][r] (row j = the r coefficients of output j)
+#pragma once
+#include "common.cuh"
+
+namespace hire_dev {
+
+// ---------------------------------------------------------------------
+// Integer mode, step 0: quantise each query x[b] to int8 with the
+// quantize_int4 rule widened to [-127,127] (approx.hpp:41-65):
+//   sx = max|x| / 127 (1 if x == 0), xq_i = RHAZ(x_i / sx).
+// Writes xq (natural order), xperm (dp4a order, see q4_score_fast_int8),
+// sx and sum(xq). One CTA per query.
+// ---------------------------------------------------------------------
+__global__ void __launch_bounds__(256) prep_x_int8_kernel(
+    const float* __restrict__ x, int d, int8_t* __restrict__ xq,
+    int8_t* __restrict__ xperm, float* __restrict__ sx_out,
+    int* __restrict__ sumxq_out) {
+  const int b = blockIdx.x;
+  const float* xb = x + static_cast<int64_t>(b) * d;
+  __shared__ float s_red[8];
+  __shared__ int s_sum[8];
+  float m = 0.0f;
+  for (int i = threadIdx.x; i < d; i += blockDim.x) m = fmaxf(m, fabsf(xb[i]));
+  m = warp_max_f32(m);
+  if ((threadIdx.x & 31) == 0) s_red[threadIdx.x >> 5] = m;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    float v = threadIdx.x < (blockDim.x >> 5) ? s_red[threadIdx.x] : 0.0f;
+    v = warp_max_f32(v);
+    if (threadIdx.x == 0) s_red[0] = v;
+  }
+  __syncthreads();
+  const float maxabs = s_red[0];
+  const float sx = maxabs > 0.0f ? __fdiv_rn(maxabs, 127.0f) : 1.0f;
+  int local = 0;
+  for (int i = threadIdx.x; i < d; i += blockDim.x) {
+    const int q = rhaz_clamp(__fdiv_rn(xb[i], sx), 127);
+    local += q;
+    xq[static_cast<int64_t>(b) * d + i] = static_cast<int8_t>(q);
+    // dp4a order: within each 8-element word group, the 4 even elements
+    // then the 4 odd elements (matches the lo/hi nibble extraction).
+    const int g = i & ~7, j = i & 7;
+    const int pos = g + ((j & 1) ? 4 : 0) + (j >> 1);
+    xperm[static_cast<int64_t>(b) * d + pos] = static_cast<int8_t>(q);
+  }
+  local = warp_sum_i32(local);
+  if ((threadIdx.x & 31) == 0) s_sum[threadIdx.x >> 5] = local;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int s = 0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s += s_sum[w];
+    sumxq_out[b] = s;
+    sx_out[b] = sx;
+  }
+}
+
+// ---------------------------------------------------------------------
+// K1, integer mode, fast path (d % 1024 == 0). One warp per row, two rows
+// in flight per warp; each lane streams CPL 16-byte chunks (32 codes) of
+// each row with 128-bit non-allocating loads and keeps the matching int8 x
+// words of QB queries in registers for the whole kernel.
+//   Offset trick: code c in [-7,7] is the two's-complement nibble n;
+//   n ^ 8 == c + 8 in [1,15], so one XOR per word turns 8 nibbles into
+//   unsigned digits; lo/hi masks give 4 bytes each, fed to dp4a against the
+//   even/odd x bytes. sum((c+8)*xq) - 8*sum(xq) = sum(c*xq) exactly (int32).
+//   score = phi(float(acc) * (scale_j * sx)) — the oracle's multiply order.
+// ---------------------------------------------------------------------
+template <int QB, int CPL>
+__global__ void __launch_bounds__(256) q4_score_fast_int8(
+    const uint8_t* __restrict__ wq, int64_t pitch, const float* __restrict__ scales,
+    int64_t rows, int d, const int8_t* __restrict__ xperm,
+    const float* __restrict__ sx, const int* __restrict__ sumxq, int phi,
+    float* __restrict__ scores, int64_t score_stride) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+
+  int xw[QB][CPL][8];
+#pragma unroll
+  for (int q = 0; q < QB; ++q)
+#pragma unroll
+    for (int c = 0; c < CPL; ++c) {
+      const int4* p = reinterpret_cast<const int4*>(
+          xperm + static_cast<int64_t>(q) * d + (lane + 32 * c) * 32);
+      const int4 a = p[0], b = p[1];
+      xw[q][c][0] = a.x; xw[q][c][1] = a.y; xw[q][c][2] = a.z; xw[q][c][3] = a.w;
+      xw[q][c][4] = b.x; xw[q][c][5] = b.y; xw[q][c][6] = b.z; xw[q][c][7] = b.w;
+    }
+  float qsx[QB];
+  int qsum[QB];
+#pragma unroll
+  for (int q = 0; q < QB; ++q) { qsx[q] = sx[q]; qsum[q] = sumxq[q]; }
+
+  for (int64_t r0 = warp * 2; r0 < rows; r0 += nwarps * 2) {
+    const bool has1 = r0 + 1 < rows;
+    uint4 w[2][CPL];
+#pragma unroll
+    for (int c = 0; c < CPL; ++c) {
+      w[0][c] = ldg_stream(wq + r0 * pitch + (lane + 32 * c) * 16);
+      w[1][c] = has1 ? ldg_stream(wq + (r0 + 1) * pitch + (lane + 32 * c) * 16)
+                     : make_uint4(0x88888888u, 0x88888888u, 0x88888888u, 0x88888888u);
+    }
+    int acc[2][QB];
+#pragma unroll
+    for (int rr = 0; rr < 2; ++rr) {
+#pragma unroll
+      for (int q = 0; q < QB; ++q) acc[rr][q] = 0;
+#pragma unroll
+      for (int c = 0; c < CPL; ++c) {
+        const uint32_t words[4] = {w[rr][c].x, w[rr][c].y, w[rr][c].z, w[rr][c].w};
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const uint32_t u = words[k] ^ 0x88888888u;
+          const int lo = static_cast<int>(u & 0x0F0F0F0Fu);
+          const int hi = static_cast<int>((u >> 4) & 0x0F0F0F0Fu);
+#pragma unroll
+          for (int q = 0; q < QB; ++q) {
+            acc[rr][q] = __dp4a(lo, xw[q][c][2 * k], acc[rr][q]);
+            acc[rr][q] = __dp4a(hi, xw[q][c][2 * k + 1], acc[rr][q]);
+          }
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < QB; ++q) acc[rr][q] = warp_sum_i32(acc[rr][q]);
+    }
+    // lanes 0..2*QB-1 write one (row, query) each
+#pragma unroll
+    for (int rr = 0; rr < 2; ++rr)
+#pragma unroll
+      for (int q = 0; q < QB; ++q)
+        if (lane == rr * QB + q && (rr == 0 || has1)) {
+          const int a = acc[rr][q] - 8 * qsum[q];
+          const float cs = __fmul_rn(scales[r0 + rr], qsx[q]);
+          scores[static_cast<int64_t>(q) * score_stride + r0 + rr] =
+              apply_phi(phi, __fmul_rn(static_cast<float>(a), cs));
+        }
+  }
+}
+
+// ---------------------------------------------------------------------
+// K1, fp32-x mode (the reference's own scorer, approx.hpp:395-403), fast
+// path: one query per pass, x in registers, nibble -> fp32 through the
+// 2^23 magic constant (exact), fp32 FMA per code, x-chunk partial sums
+// reduced by the fixed warp tree, then one multiply by scale_j. Values
+// differ from the reference's sequential sum by rounding only (near-tie
+// tolerance); the strict kernel below is bit-exact.
+// ---------------------------------------------------------------------
+template <int CPL>
+__global__ void __launch_bounds__(256) q4_score_fast_fpx(
+    const uint8_t* __restrict__ wq, int64_t pitch, const float* __restrict__ scales,
+    int64_t rows, int d, const float* __restrict__ x, int phi,
+    float* __restrict__ scores) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  float xr[CPL][32];
+#pragma unroll
+  for (int c = 0; c < CPL; ++c) {
+    const float4* p = reinterpret_cast<const float4*>(x + (lane + 32 * c) * 32);
+#pragma unroll
+    for (int v = 0; v < 8; ++v) {
+      const float4 f = p[v];
+      xr[c][4 * v] = f.x; xr[c][4 * v + 1] = f.y; xr[c][4 * v + 2] = f.z; xr[c][4 * v + 3] = f.w;
+    }
+  }
+  for (int64_t r = warp; r < rows; r += nwarps) {
+    uint4 w[CPL];
+#pragma unroll
+    for (int c = 0; c < CPL; ++c) w[c] = ldg_stream(wq + r * pitch + (lane + 32 * c) * 16);
+    float acc = 0.0f;
+#pragma unroll
+    for (int c = 0; c < CPL; ++c) {
+      const uint32_t words[4] = {w[c].x, w[c].y, w[c].z, w[c].w};
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const uint32_t u = words[k] ^ 0x88888888u;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const float cf = __fsub_rn(__uint_as_float(0x4B000000u | ((u >> (4 * j)) & 0xFu)), 8388616.0f);
+          acc = fmaf(cf, xr[c][8 * k + j], acc);
+        }
+      }
+    }
+    acc = warp_sum_f32(acc);
+    if (lane == 0) scores[r] = apply_phi(phi, __fmul_rn(acc, scales[r]));
+  }
+}
+
+// ---------------------------------------------------------------------
+// K1, generic / strict path: one thread per row, columns in ascending order.
+//   fp32-x : acc = acc + (code*scale)*x_i, no contraction — bit-identical to
+//            approx.hpp:398-402.
+//   int8   : exact int32 sum, then the integer-mode epilogue.
+// Any d; x (and xq) for the query staged in shared memory (broadcast reads).
+// ---------------------------------------------------------------------
+__global__ void __launch_bounds__(128) q4_score_seq(
+    const uint8_t* __restrict__ wq, int64_t pitch, const float* __restrict__ scales,
+    int64_t rows, int d, const float* __restrict__ x, const int8_t* __restrict__ xq,
+    const float* __restrict__ sx, int int8_mode, int phi, float* __restrict__ scores,
+    int64_t score_stride) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  float* s_x = reinterpret_cast<float*>(smem);
+  int8_t* s_xq = reinterpret_cast<int8_t*>(smem + static_cast<size_t>(d) * 4);
+  const int b = blockIdx.y;
+  for (int i = threadIdx.x; i < d; i += blockDim.x) {
+    if (int8_mode) s_xq[i] = xq[static_cast<int64_t>(b) * d + i];
+    else s_x[i] = x[static_cast<int64_t>(b) * d + i];
+  }
+  __syncthreads();
+  const int64_t r = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (r >= rows) return;
+  const uint8_t* row = wq + r * pitch;
+  const float scale = scales[r];
+  if (int8_mode) {
+    int acc = 0;
+    for (int i0 = 0; i0 < d; i0 += 32) {
+      const uint4 v = *reinterpret_cast<const uint4*>(row + i0 / 2);
+      const uint32_t words[4] = {v.x, v.y, v.z, v.w};
+      for (int j = 0; j < 32 && i0 + j < d; ++j) {
+        const uint32_t nib = (words[j >> 3] >> (4 * (j & 7))) & 0xFu;
+        const int c = static_cast<int>(nib ^ 8u) - 8;
+        acc += c * s_xq[i0 + j];
+      }
+    }
+    const float cs = __fmul_rn(scale, sx[b]);
+    scores[static_cast<int64_t>(b) * score_stride + r] =
+        apply_phi(phi, __fmul_rn(static_cast<float>(acc), cs));
+  } else {
+    float acc = 0.0f;
+    for (int i0 = 0; i0 < d; i0 += 32) {
+      const uint4 v = *reinterpret_cast<const uint4*>(row + i0 / 2);
+      const uint32_t words[4] = {v.x, v.y, v.z, v.w};
+      for (int j = 0; j < 32 && i0 + j < d; ++j) {
+        const uint32_t nib = (words[j >> 3] >> (4 * (j & 7))) & 0xFu;
+        const float c = static_cast<float>(static_cast<int>(nib ^ 8u) - 8);
+        acc = __fadd_rn(acc, __fmul_rn(__fmul_rn(c, scale), s_x[i0 + j]));
+      }
+    }
+    scores[static_cast<int64_t>(b) * score_stride + r] = apply_phi(phi, acc);
+  }
+}
+
+// ---------------------------------------------------------------------
+// K9 — int4 proxy build on the device (approx.hpp:49-65): per row absmax,
+// scale = absmax/7 (IEEE division, 1 for a zero row), code = RHAZ(w/scale)
+// clamped to [-7,7], packed low nibble first. One warp per row.
+// ---------------------------------------------------------------------
+template <typename T>
+__global__ void __launch_bounds__(256) quantize_q4_kernel(
+    const T* __restrict__ w, int64_t rows, int d, uint8_t* __restrict__ wq, int64_t pitch,
+    float* __restrict__ scales) {
+  const int lane = threadIdx.x & 31;
+  const int64_t r = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  if (r >= rows) return;
+  const T* row = w + r * d;
+  float m = 0.0f;
+  for (int i = lane; i < d; i += 32) m = fmaxf(m, fabsf(load_elem<T>(row, i)));
+  m = warp_max_f32(m);
+  const float scale = m > 0.0f ? __fdiv_rn(m, 7.0f) : 1.0f;
+  if (lane == 0) scales[r] = scale;
+  uint8_t* out = wq + r * pitch;
+  // each lane packs 8 consecutive codes into one 32-bit word
+  for (int g = lane * 8; g < static_cast<int>(pitch) * 2; g += 256) {
+    uint32_t word = 0;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int i = g + j;
+      if (i < d) {
+        const int c = rhaz_clamp(__fdiv_rn(load_elem<T>(row, i), scale), 7);
+        word |= (static_cast<uint32_t>(c) & 0xFu) << (4 * j);
+      }
+    }
+    if (g / 2 + 3 < pitch) *reinterpret_cast<uint32_t*>(out + g / 2) = word;
+    else
+      for (int j = 0; j < 4 && g / 2 + j < pitch; ++j) out[g / 2 + j] = (word >> (8 * j)) & 0xFF;
+  }
+}
+
+// ---------------------------------------------------------------------
+// K2 — low-rank proxy, step 1: t[b][q] = sum_i Z1[q][i] * x[b][i].
+//   fast  : one warp per (q, b), fixed butterfly tree.
+//   strict: one thread per (q, b), ascending i, no contraction (bit-exact
+//           with approx.hpp:483-488).
+// ---------------------------------------------------------------------
+template <typename T>
+__global__ void __launch_bounds__(256) lr_t_kernel(const T* __restrict__ z1, int r, int d,
+                                                   const float* __restrict__ x, int B,
+                                                   int strict, float* __restrict__ t) {
+  if (strict) {
+    const int id = blockIdx.x * blockDim.x + threadIdx.x;
+    if (id >= r * B) return;
+    const int q = id % r, b = id / r;
+    const T* zr = z1 + static_cast<int64_t>(q) * d;
+    const float* xb = x + static_cast<int64_t>(b) * d;
+    float acc = 0.0f;
+    for (int i = 0; i < d; ++i) acc = __fadd_rn(acc, __fmul_rn(load_elem<T>(zr, i), xb[i]));
+    t[static_cast<int64_t>(b) * r + q] = acc;
+    return;
+  }
+  const int lane = threadIdx.x & 31;
+  const int id = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (id >= r * B) return;
+  const int q = id % r, b = id / r;
+  const T* zr = z1 + static_cast<int64_t>(q) * d;
+  const float* xb = x + static_cast<int64_t>(b) * d;
+  float acc = 0.0f;
+  for (int i = lane; i < d; i += 32) acc = fmaf(load_elem<T>(zr, i), xb[i], acc);
+  acc = warp_sum_f32(acc);
+  if (lane == 0) t[static_cast<int64_t>(b) * r + q] = acc;
+}
+
+// ---------------------------------------------------------------------
+// K2 step 2: s[b][j] = phi(sum_q Z2[j][q] * t[b][q]), q ascending — one
+// thread per row, the whole row in registers, all queries' t in shared
+// memory (broadcast). strict: __fmul_rn/__fadd_rn (bit-exact with
+// approx.hpp:489-494); fast: fmaf in the same order.
+// ---------------------------------------------------------------------
+template <typename T, int R, bool STRICT>
+__global__ void __launch_bounds__(128) lr_score_kernel(
+    const T* __restrict__ z2, int64_t rows, const float* __restrict__ t, int B, int phi,
+    float* __restrict__ scores, int64_t score_stride) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  float* s_t = reinterpret_cast<float*>(smem);
+  for (int i = threadIdx.x; i < R * B; i += blockDim.x) s_t[i] = t[i];
+  __syncthreads();
+  const int64_t j = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (j >= rows) return;
+  float z[R];
+  const T* row = z2 + j * R;
+  if constexpr (sizeof(T) == 2) {
+#pragma unroll
+    for (int v = 0; v < R / 8; ++v) {
+      const uint4 u = *reinterpret_cast<const uint4*>(row + 8 * v);
+      z[8 * v + 0] = bf16_lo(u.x); z[8 * v + 1] = bf16_hi(u.x);
+      z[8 * v + 2] = bf16_lo(u.y); z[8 * v + 3] = bf16_hi(u.y);
+      z[8 * v + 4] = bf16_lo(u.z); z[8 * v + 5] = bf16_hi(u.z);
+      z[8 * v + 6] = bf16_lo(u.w); z[8 * v + 7] = bf16_hi(u.w);
+    }
+  } else {
+#pragma unroll
+    for (int v = 0; v < R / 4; ++v) {
+      const float4 u = *reinterpret_cast<const float4*>(row + 4 * v);
+      z[4 * v] = u.x; z[4 * v + 1] = u.y; z[4 * v + 2] = u.z; z[4 * v + 3] = u.w;
+    }
+  }
+  for (int b = 0; b < B; ++b) {
+    const float* tb = s_t + b * R;
+    float acc = 0.0f;
+#pragma unroll
+    for (int q = 0; q < R; ++q) {
+      if constexpr (STRICT) acc = __fadd_rn(acc, __fmul_rn(z[q], tb[q]));
+      else acc = fmaf(z[q], tb[q], acc);
+    }
+    scores[static_cast<int64_t>(b) * score_stride + j] = apply_phi(phi, acc);
+  }
+}
+
+// Generic-rank fallback (any r): same arithmetic, row streamed from memory.
+template <typename T, bool STRICT>
+__global__ void __launch_bounds__(128) lr_score_generic(
+    const T* __restrict__ z2, int64_t rows, int r, const float* __restrict__ t, int B, int phi,
+    float* __restrict__ scores, int64_t score_stride) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  float* s_t = reinterpret_cast<float*>(smem);
+  for (int i = threadIdx.x; i < r * B; i += blockDim.x) s_t[i] = t[i];
+  __syncthreads();
+  const int64_t j = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (j >= rows) return;
+  const T* row = z2 + j * r;
+  for (int b = 0; b < B; ++b) {
+    const float* tb = s_t + b * r;
+    float acc = 0.0f;
+    for (int q = 0; q < r; ++q) {
+      const float zq = load_elem<T>(row, q);
+      if constexpr (STRICT) acc = __fadd_rn(acc, __fmul_rn(zq, tb[q]));
+      else acc = fmaf(zq, tb[q], acc);
+    }
+    scores[static_cast<int64_t>(b) * score_stride + j] = apply_phi(phi, acc);
+  }
+}
+
+}  // namespace hire_dev
