@@ -96,6 +96,14 @@ HIRE_API int hire_ctx_stream(hire_ctx ctx, void** cuda_stream);
 HIRE_API int hire_ctx_synchronize(hire_ctx ctx);
 /* number of kernels this context launched so far (bench accounting) */
 HIRE_API int64_t hire_ctx_launch_count(hire_ctx ctx);
+/* Stage profiling: when on, every stage of every run is bracketed by CUDA
+ * events on the context stream. profile_read synchronises, returns the
+ * summed milliseconds and the number of timed intervals per stage
+ * (0 proxy scores, 1 candidate select, 2 gather recompute, 3 final top-k,
+ * 4 FFN down-projection, 5 NCCL collective, 6 int8 x quantisation), and
+ * clears the record. */
+HIRE_API int hire_ctx_set_profiling(hire_ctx ctx, int on);
+HIRE_API int hire_ctx_profile_read(hire_ctx ctx, double* ms, int64_t* counts, int n_stages);
 
 /* ---- dense matrices (ScoreMatrix, linalg.hpp:44-90) --------------------- */
 /* Copies src (host or device) into an owned device buffer; dtype HIRE_F32 or

@@ -55,6 +55,17 @@ class Context:
     def synchronize(self):
         check(lib().hire_ctx_synchronize(self.h))
 
+    def set_profiling(self, on: bool):
+        check(lib().hire_ctx_set_profiling(self.h, int(on)))
+
+    def profile_read(self) -> dict:
+        """{stage: (total_ms, intervals)} since the last read (syncs)."""
+        n = len(L.STAGES)
+        ms = (C.c_double * n)()
+        cnt = (C.c_int64 * n)()
+        check(lib().hire_ctx_profile_read(self.h, ms, cnt, n))
+        return {L.STAGES[i]: (ms[i], cnt[i]) for i in range(n) if cnt[i]}
+
     def __del__(self):
         if getattr(self, "h", None) and L._lib is not None:
             L._lib.hire_ctx_destroy(self.h)

@@ -56,6 +56,14 @@ __host__ __device__ __forceinline__ float key_value(uint64_t k) {
   return value_of_ord(static_cast<uint32_t>(k >> 32));
 }
 
+// ------------------------------------------- programmatic dependent launch --
+// Every kernel is launched with programmatic stream serialization: it may be
+// scheduled while its predecessor drains, and waits here (griddepcontrol
+// .wait) before touching anything the predecessor wrote. launch_dependents
+// lets the next kernel in the chain get scheduled early.
+__device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void griddep_launch() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 // --------------------------------------------------------------- loads --
 __device__ __forceinline__ uint4 ldg_stream(const void* p) {
   uint4 r;

@@ -45,6 +45,8 @@ __global__ void __launch_bounds__(256) recompute_fast(
     const T* __restrict__ w, int d, const uint32_t* __restrict__ cand, int64_t cand_stride,
     int n_cand, const float* __restrict__ x, int phi, float* __restrict__ out,
     int64_t out_stride) {
+  hire_dev::griddep_wait();
+  hire_dev::griddep_launch();
   extern __shared__ __align__(16) unsigned char smem[];
   float* s_x = reinterpret_cast<float*>(smem);
   constexpr int E = Vec16<T>::kElems;
@@ -79,6 +81,8 @@ __global__ void __launch_bounds__(128) recompute_seq(
     const T* __restrict__ w, int d, const uint32_t* __restrict__ cand, int64_t cand_stride,
     int n_cand, const float* __restrict__ x, int phi, float* __restrict__ out,
     int64_t out_stride) {
+  hire_dev::griddep_wait();
+  hire_dev::griddep_launch();
   extern __shared__ __align__(16) unsigned char smem[];
   float* s_x = reinterpret_cast<float*>(smem);
   const int b = blockIdx.y;
@@ -104,6 +108,8 @@ __global__ void __launch_bounds__(256) ffn_down_partial(
     const T* __restrict__ v, int d, const uint32_t* __restrict__ sel,
     const float* __restrict__ act, int64_t sel_stride, int n_sel, int ch,
     float* __restrict__ partial) {
+  hire_dev::griddep_wait();
+  hire_dev::griddep_launch();
   constexpr int E = Vec16<T>::kElems;
   const int c = blockIdx.x, b = blockIdx.y;
   const int lo = c * ch, hi = min(n_sel, lo + ch);
@@ -147,6 +153,8 @@ __global__ void __launch_bounds__(256) ffn_down_partial(
 __global__ void __launch_bounds__(256) ffn_down_reduce(const float* __restrict__ partial,
                                                        int n_chunks, int d, int B,
                                                        float* __restrict__ out) {
+  hire_dev::griddep_wait();
+  hire_dev::griddep_launch();
   const int64_t id = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (id >= static_cast<int64_t>(B) * d) return;
   const int b = static_cast<int>(id / d), col = static_cast<int>(id % d);
@@ -164,6 +172,8 @@ __global__ void __launch_bounds__(256) ffn_down_seq(const T* __restrict__ v, int
                                                     const float* __restrict__ act,
                                                     int64_t sel_stride, int n_sel,
                                                     float* __restrict__ out) {
+  hire_dev::griddep_wait();
+  hire_dev::griddep_launch();
   const int col = blockIdx.x * blockDim.x + threadIdx.x, b = blockIdx.y;
   if (col >= d) return;
   float acc = 0.0f;

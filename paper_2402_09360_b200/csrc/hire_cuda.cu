@@ -77,7 +77,56 @@ struct hire_ctx_s {
   void* io_host = nullptr;
   size_t io_host_cap = 0;
   int64_t launches = 0;
+  bool pdl = true;
+  bool force_dp4a = false;
+  // stage profiling (hire_ctx_set_profiling): event pairs around each stage
+  bool prof = false;
+  std::vector<cudaEvent_t> ev_pool;
+  std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> marks;
+  cudaEvent_t get_event() {
+    if (ev_pool.empty()) {
+      cudaEvent_t e;
+      cudaEventCreate(&e);
+      return e;
+    }
+    cudaEvent_t e = ev_pool.back();
+    ev_pool.pop_back();
+    return e;
+  }
 };
+
+namespace {
+// Stage ids for hire_ctx_profile_read.
+enum Stage { kStageProxy = 0, kStageSelect = 1, kStageRecompute = 2, kStageFinal = 3, kStageDown = 4,
+             kStageComm = 5, kStagePrep = 6, kNumStages = 8 };
+
+struct StageScope {
+  hire_ctx c;
+  int stage;
+  cudaEvent_t e0 = nullptr;
+  // Inside stream capture the records become external event nodes, so the
+  // pairs time the replayed graph.
+  static void record(cudaEvent_t e, cudaStream_t s) {
+    cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
+    cudaStreamIsCapturing(s, &st);
+    if (st == cudaStreamCaptureStatusActive) cudaEventRecordWithFlags(e, s, cudaEventRecordExternal);
+    else cudaEventRecord(e, s);
+  }
+  StageScope(hire_ctx ctx, int st) : c(ctx), stage(st) {
+    if (c->prof) {
+      e0 = c->get_event();
+      record(e0, c->stream);
+    }
+  }
+  ~StageScope() {
+    if (c->prof) {
+      cudaEvent_t e1 = c->get_event();
+      record(e1, c->stream);
+      c->marks.push_back({stage, {e0, e1}});
+    }
+  }
+};
+}  // namespace
 
 struct hire_matrix_s {
   void* ptr = nullptr;
@@ -93,6 +142,8 @@ struct hire_scorer_s {
   uint8_t* codes = nullptr;
   int64_t pitch = 0;
   float* scales = nullptr;
+  uint4* mma = nullptr;        // MMA-tiled copy for the tensor-core proxy (lazy)
+  bool mma_owned = false;
   // low-rank
   void* z1 = nullptr;
   void* z2 = nullptr;
@@ -108,6 +159,27 @@ struct hire_comm_s {
 namespace {
 
 size_t dtype_size(int dt) { return dt == HIRE_BF16 ? 2 : 4; }
+
+// Every launch goes through here: programmatic stream serialization (PDL)
+// so each kernel's launch overlaps its predecessor's tail (kernels call
+// griddepcontrol.wait before consuming). Counted for bench accounting.
+template <typename... KArgs, typename... Args>
+cudaError_t launch_k(hire_ctx ctx, void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                     Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = ctx->stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = ctx->pdl ? 1 : 0;
+  ++ctx->launches;
+  return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
+}
+
 
 int ensure(void** buf, size_t* cap, size_t need, cudaStream_t s) {
   if (need <= *cap) return HIRE_OK;
@@ -230,17 +302,16 @@ int plan_select(int64_t n, int64_t k_prime, int sel_mode, int64_t nb_req, int64_
 int run_select(hire_ctx ctx, const float* scores, int64_t score_stride, int64_t n, int64_t B,
                const SelPlan& sp, uint64_t* surv, uint32_t* cand, int64_t cand_stride,
                int* status) {
+  StageScope scope(ctx, kStageSelect);
   if (sp.mode == 1) {
-    bucket_topt_kernel<<<dim3(sp.n_buckets, static_cast<unsigned>(B)), 256, 0, ctx->stream>>>(
-        scores, score_stride, n, sp.n_buckets, sp.t, surv);
-    ctx->launches++;
+    CK(launch_k(ctx, bucket_topt_kernel, dim3(sp.n_buckets, static_cast<unsigned>(B)), 256, 0, 
+        scores, score_stride, n, sp.n_buckets, sp.t, surv));
     CK(cudaGetLastError());
   }
   const size_t smem = sp.mode == 0 ? static_cast<size_t>(n) * 4 : static_cast<size_t>(kPoolKeys) * 8;
-  select_candidates_kernel<<<static_cast<unsigned>(B), kSelectThreads, smem, ctx->stream>>>(
+  CK(launch_k(ctx, select_candidates_kernel, static_cast<unsigned>(B), kSelectThreads, smem, 
       sp.mode, scores, score_stride, n, surv, sp.n_buckets, sp.t, static_cast<int>(sp.k_eff),
-      sp.exact_fix, cand, cand_stride, status);
-  ctx->launches++;
+      sp.exact_fix, cand, cand_stride, status));
   CK(cudaGetLastError());
   return HIRE_OK;
 }
@@ -275,10 +346,9 @@ int launch_q4_int8(hire_ctx ctx, const hire_scorer_s* a, const ScoreWs& w, int64
   if (!bps) bps = max_blocks(k, 256, 0);
   const int64_t want = ceil_div(a->rows, 16);
   const int grid = static_cast<int>(std::min<int64_t>(want, static_cast<int64_t>(bps) * ctx->num_sms));
-  k<<<grid, 256, 0, ctx->stream>>>(a->codes, a->pitch, a->scales, a->rows, static_cast<int>(a->d),
+  CK(launch_k(ctx, k, grid, 256, 0, a->codes, a->pitch, a->scales, a->rows, static_cast<int>(a->d),
                                     w.xperm + b0 * a->d, w.sx + b0, w.sumxq + b0, phi,
-                                    out + b0 * stride, stride);
-  ctx->launches++;
+                                    out + b0 * stride, stride));
   CK(cudaGetLastError());
   return HIRE_OK;
 }
@@ -306,23 +376,87 @@ int launch_q4_fpx(hire_ctx ctx, const hire_scorer_s* a, const float* x, int64_t 
   const int64_t want = ceil_div(a->rows, 8);
   const int grid = static_cast<int>(std::min<int64_t>(want, static_cast<int64_t>(bps) * ctx->num_sms));
   for (int64_t b = 0; b < B; ++b) {
-    k<<<grid, 256, 0, ctx->stream>>>(a->codes, a->pitch, a->scales, a->rows, static_cast<int>(a->d),
-                                      x + b * a->d, phi, out + b * stride);
-    ctx->launches++;
+    CK(launch_k(ctx, k, grid, 256, 0, a->codes, a->pitch, a->scales, a->rows, static_cast<int>(a->d),
+                                      x + b * a->d, phi, out + b * stride));
   }
   CK(cudaGetLastError());
   return HIRE_OK;
+}
+
+int ensure_mma_layout(hire_ctx ctx, hire_scorer_s* a) {
+  if (a->mma) return HIRE_OK;
+  const int64_t n_rb = ceil_div(a->rows, 16);
+  const int64_t n_words = n_rb * (a->d / 64) * 128;
+  CK(cudaMalloc(&a->mma, static_cast<size_t>(n_words) * 4));
+  a->mma_owned = true;
+  CK(launch_k(ctx, q4_to_mma_layout, static_cast<unsigned>(ceil_div(n_words, 256)), 256, 0, a->codes,
+              a->pitch, a->rows, static_cast<int>(a->d), reinterpret_cast<uint32_t*>(a->mma), n_words));
+  return HIRE_OK;
+}
+
+template <int NT, int KS>
+int launch_q4_mma_t(hire_ctx ctx, const hire_scorer_s* a, const ScoreWs& w, int64_t b0, int64_t nb,
+                    int phi, float* out, int64_t stride) {
+  auto k = q4_score_mma<NT, KS>;
+  const int d = static_cast<int>(a->d);
+  const size_t smem = static_cast<size_t>(NT) * 8 * (d + 16) + (KS > 1 ? 8 * NT * 4 * 32 * 4 : 0);
+  static int bps = 0;
+  if (!bps) {
+    CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    bps = max_blocks(k, 256, smem);
+  }
+  const int64_t n_rb = ceil_div(a->rows, 16);
+  const int64_t want = ceil_div(n_rb, 8 / KS);
+  const int grid = static_cast<int>(std::min<int64_t>(want, static_cast<int64_t>(bps) * ctx->num_sms));
+  CK(launch_k(ctx, k, grid, 256, smem, a->mma, a->rows, d, a->scales, w.xq + b0 * d, w.sx + b0,
+              w.sumxq + b0, static_cast<int>(nb), phi, out + b0 * stride, stride));
+  return HIRE_OK;
+}
+
+template <int NT>
+int launch_q4_mma_nt(hire_ctx ctx, const hire_scorer_s* a, const ScoreWs& w, int64_t b0, int64_t nb,
+                     int phi, float* out, int64_t stride) {
+  // split k across warps until the grid has ~32 warps per SM
+  const int64_t n_rb = ceil_div(a->rows, 16);
+  const int64_t nkb = a->d / 64;
+  int ks = 1;
+  while (ks < 8 && n_rb * ks < 32LL * ctx->num_sms && nkb >= 2 * ks) ks *= 2;
+  switch (ks) {
+    case 1: return launch_q4_mma_t<NT, 1>(ctx, a, w, b0, nb, phi, out, stride);
+    case 2: return launch_q4_mma_t<NT, 2>(ctx, a, w, b0, nb, phi, out, stride);
+    case 4: return launch_q4_mma_t<NT, 4>(ctx, a, w, b0, nb, phi, out, stride);
+    default: return launch_q4_mma_t<NT, 8>(ctx, a, w, b0, nb, phi, out, stride);
+  }
+}
+
+int launch_q4_mma(hire_ctx ctx, const hire_scorer_s* a, const ScoreWs& w, int64_t b0, int64_t nb,
+                  int phi, float* out, int64_t stride) {
+  if (nb <= 8) return launch_q4_mma_nt<1>(ctx, a, w, b0, nb, phi, out, stride);
+  if (nb <= 16) return launch_q4_mma_nt<2>(ctx, a, w, b0, nb, phi, out, stride);
+  if (nb <= 32) return launch_q4_mma_nt<4>(ctx, a, w, b0, nb, phi, out, stride);
+  return launch_q4_mma_nt<8>(ctx, a, w, b0, nb, phi, out, stride);
 }
 
 // phi(Z_approx^T x) for B queries into out [B][stride].
 int run_scores(hire_ctx ctx, const hire_scorer_s* a, const float* x, int64_t B, int phi,
                int x_mode, int strict, const ScoreWs& w, float* out, int64_t stride) {
   const int d = static_cast<int>(a->d);
+  if (a->kind == HIRE_SCORER_Q4 && x_mode == HIRE_X_INT8) {
+    StageScope pscope(ctx, kStagePrep);
+    CK(launch_k(ctx, prep_x_int8_kernel, static_cast<unsigned>(B), 256, 0, x, d, w.xq, w.xperm, w.sx, w.sumxq));
+    CK(cudaGetLastError());
+  }
+  StageScope scope(ctx, kStageProxy);
   if (a->kind == HIRE_SCORER_Q4) {
-    if (x_mode == HIRE_X_INT8) {
-      prep_x_int8_kernel<<<static_cast<unsigned>(B), 256, 0, ctx->stream>>>(x, d, w.xq, w.xperm, w.sx, w.sumxq);
-      ctx->launches++;
-      CK(cudaGetLastError());
+    if (x_mode == HIRE_X_INT8 && d % 64 == 0 && !ctx->force_dp4a) {
+      RET(ensure_mma_layout(ctx, const_cast<hire_scorer_s*>(a)));
+      int64_t b0 = 0;
+      while (b0 < B) {
+        const int64_t nb = std::min<int64_t>(64, B - b0);
+        RET(launch_q4_mma(ctx, a, w, b0, nb, phi, out, stride));
+        b0 += nb;
+      }
+      return HIRE_OK;
     }
     const bool fast_shape = (d % 1024 == 0) && a->pitch == d / 2 && d <= 8192;
     if (fast_shape && x_mode == HIRE_X_INT8) {
@@ -343,10 +477,8 @@ int run_scores(hire_ctx ctx, const hire_scorer_s* a, const float* x, int64_t B, 
       }
     }
     const size_t smem = static_cast<size_t>(d) * 5 + 16;
-    if (smem > 48 * 1024) CK(cudaFuncSetAttribute(q4_score_seq, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-    q4_score_seq<<<dim3(static_cast<unsigned>(ceil_div(a->rows, 128)), static_cast<unsigned>(B)), 128, smem, ctx->stream>>>(
-        a->codes, a->pitch, a->scales, a->rows, d, x, w.xq, w.sx, x_mode == HIRE_X_INT8, phi, out, stride);
-    ctx->launches++;
+    CK(launch_k(ctx, q4_score_seq, dim3(static_cast<unsigned>(ceil_div(a->rows, 128)), static_cast<unsigned>(B)), 128, smem, 
+        a->codes, a->pitch, a->scales, a->rows, d, x, w.xq, w.sx, x_mode == HIRE_X_INT8, phi, out, stride));
     CK(cudaGetLastError());
     return HIRE_OK;
   }
@@ -356,30 +488,25 @@ int run_scores(hire_ctx ctx, const hire_scorer_s* a, const float* x, int64_t B, 
   {
     const int64_t items = static_cast<int64_t>(r) * B;
     const unsigned grid = static_cast<unsigned>(strict ? ceil_div(items, 256) : ceil_div(items * 32, 256));
-    if (bf) lr_t_kernel<__nv_bfloat16><<<grid, 256, 0, ctx->stream>>>(static_cast<const __nv_bfloat16*>(a->z1), r, d, x, static_cast<int>(B), strict, w.t);
-    else lr_t_kernel<float><<<grid, 256, 0, ctx->stream>>>(static_cast<const float*>(a->z1), r, d, x, static_cast<int>(B), strict, w.t);
-    ctx->launches++;
+    if (bf) CK(launch_k(ctx, lr_t_kernel<__nv_bfloat16>, grid, 256, 0, static_cast<const __nv_bfloat16*>(a->z1), r, d, x, static_cast<int>(B), strict, w.t));
+    else CK(launch_k(ctx, lr_t_kernel<float>, grid, 256, 0, static_cast<const float*>(a->z1), r, d, x, static_cast<int>(B), strict, w.t));
     CK(cudaGetLastError());
   }
   const size_t smem = static_cast<size_t>(r) * B * 4;
   const unsigned grid = static_cast<unsigned>(ceil_div(a->rows, 128));
-  auto setsm = [&](const void* f) -> int {
-    if (smem > 48 * 1024) CK(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-    return HIRE_OK;
-  };
+  auto setsm = [&](const void*) -> int { return HIRE_OK; };  // attributes set at ctx creation
   if (smem > 200 * 1024) return invalid("low-rank scores: rank * batch too large");
   if (r == 64 && B * r * 4 <= 200 * 1024) {
-    if (bf && strict) { RET(setsm((const void*)lr_score_kernel<__nv_bfloat16, 64, true>)); lr_score_kernel<__nv_bfloat16, 64, true><<<grid, 128, smem, ctx->stream>>>(static_cast<const __nv_bfloat16*>(a->z2), a->rows, w.t, static_cast<int>(B), phi, out, stride); }
-    else if (bf) { RET(setsm((const void*)lr_score_kernel<__nv_bfloat16, 64, false>)); lr_score_kernel<__nv_bfloat16, 64, false><<<grid, 128, smem, ctx->stream>>>(static_cast<const __nv_bfloat16*>(a->z2), a->rows, w.t, static_cast<int>(B), phi, out, stride); }
-    else if (strict) { RET(setsm((const void*)lr_score_kernel<float, 64, true>)); lr_score_kernel<float, 64, true><<<grid, 128, smem, ctx->stream>>>(static_cast<const float*>(a->z2), a->rows, w.t, static_cast<int>(B), phi, out, stride); }
-    else { RET(setsm((const void*)lr_score_kernel<float, 64, false>)); lr_score_kernel<float, 64, false><<<grid, 128, smem, ctx->stream>>>(static_cast<const float*>(a->z2), a->rows, w.t, static_cast<int>(B), phi, out, stride); }
+    if (bf && strict) { RET(setsm((const void*)lr_score_kernel<__nv_bfloat16, 64, true>)); CK(launch_k(ctx, lr_score_kernel<__nv_bfloat16, 64, true>, grid, 128, smem, static_cast<const __nv_bfloat16*>(a->z2), a->rows, w.t, static_cast<int>(B), phi, out, stride)); }
+    else if (bf) { RET(setsm((const void*)lr_score_kernel<__nv_bfloat16, 64, false>)); CK(launch_k(ctx, lr_score_kernel<__nv_bfloat16, 64, false>, grid, 128, smem, static_cast<const __nv_bfloat16*>(a->z2), a->rows, w.t, static_cast<int>(B), phi, out, stride)); }
+    else if (strict) { RET(setsm((const void*)lr_score_kernel<float, 64, true>)); CK(launch_k(ctx, lr_score_kernel<float, 64, true>, grid, 128, smem, static_cast<const float*>(a->z2), a->rows, w.t, static_cast<int>(B), phi, out, stride)); }
+    else { RET(setsm((const void*)lr_score_kernel<float, 64, false>)); CK(launch_k(ctx, lr_score_kernel<float, 64, false>, grid, 128, smem, static_cast<const float*>(a->z2), a->rows, w.t, static_cast<int>(B), phi, out, stride)); }
   } else {
-    if (bf && strict) { RET(setsm((const void*)lr_score_generic<__nv_bfloat16, true>)); lr_score_generic<__nv_bfloat16, true><<<grid, 128, smem, ctx->stream>>>(static_cast<const __nv_bfloat16*>(a->z2), a->rows, r, w.t, static_cast<int>(B), phi, out, stride); }
-    else if (bf) { RET(setsm((const void*)lr_score_generic<__nv_bfloat16, false>)); lr_score_generic<__nv_bfloat16, false><<<grid, 128, smem, ctx->stream>>>(static_cast<const __nv_bfloat16*>(a->z2), a->rows, r, w.t, static_cast<int>(B), phi, out, stride); }
-    else if (strict) { RET(setsm((const void*)lr_score_generic<float, true>)); lr_score_generic<float, true><<<grid, 128, smem, ctx->stream>>>(static_cast<const float*>(a->z2), a->rows, r, w.t, static_cast<int>(B), phi, out, stride); }
-    else { RET(setsm((const void*)lr_score_generic<float, false>)); lr_score_generic<float, false><<<grid, 128, smem, ctx->stream>>>(static_cast<const float*>(a->z2), a->rows, r, w.t, static_cast<int>(B), phi, out, stride); }
+    if (bf && strict) { RET(setsm((const void*)lr_score_generic<__nv_bfloat16, true>)); CK(launch_k(ctx, lr_score_generic<__nv_bfloat16, true>, grid, 128, smem, static_cast<const __nv_bfloat16*>(a->z2), a->rows, r, w.t, static_cast<int>(B), phi, out, stride)); }
+    else if (bf) { RET(setsm((const void*)lr_score_generic<__nv_bfloat16, false>)); CK(launch_k(ctx, lr_score_generic<__nv_bfloat16, false>, grid, 128, smem, static_cast<const __nv_bfloat16*>(a->z2), a->rows, r, w.t, static_cast<int>(B), phi, out, stride)); }
+    else if (strict) { RET(setsm((const void*)lr_score_generic<float, true>)); CK(launch_k(ctx, lr_score_generic<float, true>, grid, 128, smem, static_cast<const float*>(a->z2), a->rows, r, w.t, static_cast<int>(B), phi, out, stride)); }
+    else { RET(setsm((const void*)lr_score_generic<float, false>)); CK(launch_k(ctx, lr_score_generic<float, false>, grid, 128, smem, static_cast<const float*>(a->z2), a->rows, r, w.t, static_cast<int>(B), phi, out, stride)); }
   }
-  ctx->launches++;
   CK(cudaGetLastError());
   return HIRE_OK;
 }
@@ -391,11 +518,9 @@ int launch_recompute_fast(hire_ctx ctx, const void* w, int d, const uint32_t* ca
                           float* out, int64_t out_stride) {
   const size_t smem = static_cast<size_t>(d) * 4;
   auto k = recompute_fast<T, CPL>;
-  if (smem > 48 * 1024) CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
   const int64_t tiles = std::max<int64_t>(1, std::min<int64_t>(ceil_div(n_cand, 8), std::max<int64_t>(1, 4 * ctx->num_sms / B)));
-  k<<<dim3(static_cast<unsigned>(tiles), static_cast<unsigned>(B)), 256, smem, ctx->stream>>>(
-      static_cast<const T*>(w), d, cand, cand_stride, static_cast<int>(n_cand), x, phi, out, out_stride);
-  ctx->launches++;
+  CK(launch_k(ctx, k, dim3(static_cast<unsigned>(tiles), static_cast<unsigned>(B)), 256, smem, 
+      static_cast<const T*>(w), d, cand, cand_stride, static_cast<int>(n_cand), x, phi, out, out_stride));
   CK(cudaGetLastError());
   return HIRE_OK;
 }
@@ -405,6 +530,7 @@ int run_recompute(hire_ctx ctx, const hire_matrix_s* m, const uint32_t* cand, in
                   int64_t n_cand, const float* x, int64_t B, int phi, int strict, float* out,
                   int64_t out_stride) {
   if (n_cand <= 0) return HIRE_OK;
+  StageScope scope(ctx, kStageRecompute);
   const int d = static_cast<int>(m->d);
   const size_t es = dtype_size(m->dtype);
   const int64_t bytes = static_cast<int64_t>(d) * static_cast<int64_t>(es);
@@ -424,13 +550,10 @@ int run_recompute(hire_ctx ctx, const hire_matrix_s* m, const uint32_t* cand, in
   const size_t smem = static_cast<size_t>(d) * 4;
   const dim3 grid(static_cast<unsigned>(ceil_div(n_cand, 128)), static_cast<unsigned>(B));
   if (m->dtype == HIRE_BF16) {
-    if (smem > 48 * 1024) CK(cudaFuncSetAttribute(recompute_seq<__nv_bfloat16>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-    recompute_seq<__nv_bfloat16><<<grid, 128, smem, ctx->stream>>>(static_cast<const __nv_bfloat16*>(m->ptr), d, cand, cand_stride, static_cast<int>(n_cand), x, phi, out, out_stride);
+    CK(launch_k(ctx, recompute_seq<__nv_bfloat16>, grid, 128, smem, static_cast<const __nv_bfloat16*>(m->ptr), d, cand, cand_stride, static_cast<int>(n_cand), x, phi, out, out_stride));
   } else {
-    if (smem > 48 * 1024) CK(cudaFuncSetAttribute(recompute_seq<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-    recompute_seq<float><<<grid, 128, smem, ctx->stream>>>(static_cast<const float*>(m->ptr), d, cand, cand_stride, static_cast<int>(n_cand), x, phi, out, out_stride);
+    CK(launch_k(ctx, recompute_seq<float>, grid, 128, smem, static_cast<const float*>(m->ptr), d, cand, cand_stride, static_cast<int>(n_cand), x, phi, out, out_stride));
   }
-  ctx->launches++;
   CK(cudaGetLastError());
   return HIRE_OK;
 }
@@ -440,34 +563,42 @@ int run_final(hire_ctx ctx, const float* vals, int64_t vs, const uint32_t* idx, 
               int64_t B, int out_mode, uint32_t* out_idx, float* out_val, float* out_prob,
               uint64_t* out_keys, int64_t out_stride) {
   if (K < 1 || n < 1) return HIRE_OK;
+  StageScope scope(ctx, kStageFinal);
   if (out_mode == 0 && K > kFinalMax) return invalid("final top-k: k exceeds " + std::to_string(kFinalMax));
   int64_t P = 1;
   while (P < K) P <<= 1;
   const size_t smem = out_mode == 0 ? static_cast<size_t>(P) * 8 : 0;
-  final_select_kernel<<<static_cast<unsigned>(B), kSelectThreads, smem, ctx->stream>>>(
+  CK(launch_k(ctx, final_select_kernel, static_cast<unsigned>(B), kSelectThreads, smem, 
       vals, vs, idx, is, src_keys, static_cast<int>(std::max<int64_t>(n_per, 1)), part_stride,
-      static_cast<int>(n), static_cast<int>(K), out_mode, out_idx, out_val, out_prob, out_keys, out_stride);
-  ctx->launches++;
+      static_cast<int>(n), static_cast<int>(K), out_mode, out_idx, out_val, out_prob, out_keys, out_stride));
   CK(cudaGetLastError());
   return HIRE_OK;
 }
 
 __global__ void add_offset_kernel(uint32_t* idx, int64_t n, uint32_t off) {
+  hire_dev::griddep_wait();
+  hire_dev::griddep_launch();
   const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i < n) idx[i] += off;
 }
 
 __global__ void add_offset_strided_kernel(uint32_t* s, int64_t stride, int64_t n, int64_t B, uint32_t off) {
+  hire_dev::griddep_wait();
+  hire_dev::griddep_launch();
   const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i < n * B) s[(i / n) * stride + i % n] += off;
 }
 
 __global__ void iota_mod_kernel(uint32_t* u, int64_t m, int64_t n) {
+  hire_dev::griddep_wait();
+  hire_dev::griddep_launch();
   const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i < n) u[i] = static_cast<uint32_t>(i % m);
 }
 
 __global__ void gather_values_kernel(const float* v, int64_t n, const uint32_t* c, int64_t kk, int64_t B, float* o) {
+  hire_dev::griddep_wait();
+  hire_dev::griddep_launch();
   const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i < kk * B) o[i] = v[(i / kk) * n + c[i]];
 }
@@ -475,6 +606,8 @@ __global__ void gather_values_kernel(const float* v, int64_t n, const uint32_t* 
 // FFN helpers for g > 1 -------------------------------------------------------
 __global__ void group_proxy_kernel(const float* scores, int64_t ss, int64_t ngroups, int g, int B,
                                    float* proxy) {
+  hire_dev::griddep_wait();
+  hire_dev::griddep_launch();
   const int64_t id = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (id >= ngroups * B) return;
   const int64_t b = id / ngroups, j = id % ngroups;
@@ -485,6 +618,8 @@ __global__ void group_proxy_kernel(const float* scores, int64_t ss, int64_t ngro
 
 __global__ void expand_groups_kernel(const uint32_t* groups, int64_t gs, int64_t n, int g, int B,
                                      uint32_t* units) {
+  hire_dev::griddep_wait();
+  hire_dev::griddep_launch();
   const int64_t id = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (id >= n * g * B) return;
   const int64_t b = id / (n * g), r = id % (n * g);
@@ -492,6 +627,8 @@ __global__ void expand_groups_kernel(const uint32_t* groups, int64_t gs, int64_t
 }
 
 __global__ void group_sum_kernel(const float* act, int64_t n, int g, int B, float* out) {
+  hire_dev::griddep_wait();
+  hire_dev::griddep_launch();
   const int64_t id = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (id >= n * B) return;
   const int64_t b = id / n, j = id % n;
@@ -502,6 +639,7 @@ __global__ void group_sum_kernel(const float* act, int64_t n, int g, int B, floa
 
 int run_down(hire_ctx ctx, const hire_matrix_s* v, const uint32_t* units, const float* act,
              int64_t stride, int64_t n_units, int64_t B, int strict, float* partial, float* out) {
+  StageScope scope(ctx, kStageDown);
   const int d = static_cast<int>(v->d);
   const bool bf = v->dtype == HIRE_BF16;
   if (n_units == 0) {
@@ -510,21 +648,18 @@ int run_down(hire_ctx ctx, const hire_matrix_s* v, const uint32_t* units, const 
   }
   if (strict || (static_cast<int64_t>(d) * static_cast<int64_t>(dtype_size(v->dtype))) % 16 != 0) {
     const dim3 grid(static_cast<unsigned>(ceil_div(d, 256)), static_cast<unsigned>(B));
-    if (bf) ffn_down_seq<__nv_bfloat16><<<grid, 256, 0, ctx->stream>>>(static_cast<const __nv_bfloat16*>(v->ptr), d, units, act, stride, static_cast<int>(n_units), out);
-    else ffn_down_seq<float><<<grid, 256, 0, ctx->stream>>>(static_cast<const float*>(v->ptr), d, units, act, stride, static_cast<int>(n_units), out);
-    ctx->launches++;
+    if (bf) CK(launch_k(ctx, ffn_down_seq<__nv_bfloat16>, grid, 256, 0, static_cast<const __nv_bfloat16*>(v->ptr), d, units, act, stride, static_cast<int>(n_units), out));
+    else CK(launch_k(ctx, ffn_down_seq<float>, grid, 256, 0, static_cast<const float*>(v->ptr), d, units, act, stride, static_cast<int>(n_units), out));
     CK(cudaGetLastError());
     return HIRE_OK;
   }
   const int ch = 8;
   const int64_t nch = ceil_div(n_units, ch);
   const dim3 grid(static_cast<unsigned>(nch), static_cast<unsigned>(B));
-  if (bf) ffn_down_partial<__nv_bfloat16><<<grid, 256, 0, ctx->stream>>>(static_cast<const __nv_bfloat16*>(v->ptr), d, units, act, stride, static_cast<int>(n_units), ch, partial);
-  else ffn_down_partial<float><<<grid, 256, 0, ctx->stream>>>(static_cast<const float*>(v->ptr), d, units, act, stride, static_cast<int>(n_units), ch, partial);
-  ctx->launches++;
+  if (bf) CK(launch_k(ctx, ffn_down_partial<__nv_bfloat16>, grid, 256, 0, static_cast<const __nv_bfloat16*>(v->ptr), d, units, act, stride, static_cast<int>(n_units), ch, partial));
+  else CK(launch_k(ctx, ffn_down_partial<float>, grid, 256, 0, static_cast<const float*>(v->ptr), d, units, act, stride, static_cast<int>(n_units), ch, partial));
   CK(cudaGetLastError());
-  ffn_down_reduce<<<static_cast<unsigned>(ceil_div(B * d, 256)), 256, 0, ctx->stream>>>(partial, static_cast<int>(nch), d, static_cast<int>(B), out);
-  ctx->launches++;
+  CK(launch_k(ctx, ffn_down_reduce, static_cast<unsigned>(ceil_div(B * d, 256)), 256, 0, partial, static_cast<int>(nch), d, static_cast<int>(B), out));
   CK(cudaGetLastError());
   return HIRE_OK;
 }
@@ -602,6 +737,28 @@ int hire_ctx_create(int device, void* stream, int own_stream, hire_ctx* out) {
                           kPoolKeys * 8));
   CK(cudaFuncSetAttribute(final_select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                           kFinalMax * 8));
+  // every other kernel with dynamic shared memory: allow up to 200 KB once,
+  // here, so no attribute call ever happens inside a captured graph
+  {
+    const int mx = 200 * 1024;
+    const void* ks[] = {
+        (const void*)q4_score_seq,
+        (const void*)recompute_fast<float, 1>, (const void*)recompute_fast<float, 2>,
+        (const void*)recompute_fast<float, 4>, (const void*)recompute_fast<float, 8>,
+        (const void*)recompute_fast<float, 16>, (const void*)recompute_fast<__nv_bfloat16, 1>,
+        (const void*)recompute_fast<__nv_bfloat16, 2>, (const void*)recompute_fast<__nv_bfloat16, 4>,
+        (const void*)recompute_fast<__nv_bfloat16, 8>, (const void*)recompute_fast<__nv_bfloat16, 16>,
+        (const void*)recompute_seq<float>, (const void*)recompute_seq<__nv_bfloat16>,
+        (const void*)lr_score_kernel<float, 64, true>, (const void*)lr_score_kernel<float, 64, false>,
+        (const void*)lr_score_kernel<__nv_bfloat16, 64, true>,
+        (const void*)lr_score_kernel<__nv_bfloat16, 64, false>,
+        (const void*)lr_score_generic<float, true>, (const void*)lr_score_generic<float, false>,
+        (const void*)lr_score_generic<__nv_bfloat16, true>,
+        (const void*)lr_score_generic<__nv_bfloat16, false>};
+    for (const void* k : ks) CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
+  }
+  if (const char* e = getenv("HIRE_PROXY_KERNEL")) c->force_dp4a = std::strcmp(e, "dp4a") == 0;
+  if (const char* e = getenv("HIRE_NO_PDL")) c->pdl = std::strcmp(e, "1") != 0;
   *out = c;
   return HIRE_OK;
 }
@@ -612,6 +769,8 @@ int hire_ctx_destroy(hire_ctx c) {
   if (c->ws) cudaFree(c->ws);
   if (c->io_dev) cudaFree(c->io_dev);
   if (c->io_host) cudaFreeHost(c->io_host);
+  for (auto& m : c->marks) { cudaEventDestroy(m.second.first); cudaEventDestroy(m.second.second); }
+  for (auto e : c->ev_pool) cudaEventDestroy(e);
   if (c->own_stream) cudaStreamDestroy(c->stream);
   delete c;
   return HIRE_OK;
@@ -630,6 +789,33 @@ int hire_ctx_synchronize(hire_ctx c) {
 }
 
 int64_t hire_ctx_launch_count(hire_ctx c) { return c ? c->launches : 0; }
+
+int hire_ctx_set_profiling(hire_ctx c, int on) {
+  if (!c) return invalid("null handle");
+  c->prof = on != 0;
+  return HIRE_OK;
+}
+
+int hire_ctx_profile_read(hire_ctx c, double* ms, int64_t* counts, int n_stages) {
+  if (!c || !ms || !counts) return invalid("null argument");
+  CK(cudaStreamSynchronize(c->stream));
+  for (int i = 0; i < n_stages; ++i) { ms[i] = 0.0; counts[i] = 0; }
+  cudaError_t err = cudaSuccess;
+  for (auto& m : c->marks) {
+    float t = 0.0f;
+    const cudaError_t e = cudaEventElapsedTime(&t, m.second.first, m.second.second);
+    if (e != cudaSuccess) err = e;
+    else if (m.first < n_stages) { ms[m.first] += t; counts[m.first] += 1; }
+    c->ev_pool.push_back(m.second.first);
+    c->ev_pool.push_back(m.second.second);
+  }
+  c->marks.clear();
+  if (err != cudaSuccess) {
+    cudaGetLastError();
+    return set_err(HIRE_ERR_RUNTIME, std::string("cudaEventElapsedTime: ") + cudaGetErrorString(err));
+  }
+  return HIRE_OK;
+}
 
 // ------------------------------------------------------------- matrices --
 int hire_matrix_create(const void* src, int64_t rows, int64_t d, int dtype, int src_on_device,
@@ -712,6 +898,14 @@ static int make_q4(const std::vector<uint8_t>& packed_rows, const float* scales,
     delete a;
     return set_err(HIRE_ERR_RUNTIME, std::string("q4 upload: ") + cudaGetErrorString(e));
   }
+  if (d % 64 == 0) {
+    hire_ctx_s tmp;
+    tmp.stream = nullptr;
+    tmp.pdl = false;
+    const int rc = ensure_mma_layout(&tmp, a);
+    if (rc == HIRE_OK) CK(cudaStreamSynchronize(nullptr));
+    if (rc != HIRE_OK) { hire_scorer_destroy(a); return rc; }
+  }
   *out = a;
   return HIRE_OK;
 }
@@ -768,16 +962,19 @@ int hire_scorer_quantize(hire_ctx ctx, hire_matrix w, hire_scorer* out) {
   }
   const unsigned grid = static_cast<unsigned>(ceil_div(w->rows * 32, 256));
   if (w->dtype == HIRE_BF16)
-    quantize_q4_kernel<__nv_bfloat16><<<grid, 256, 0, ctx->stream>>>(static_cast<const __nv_bfloat16*>(w->ptr), w->rows, static_cast<int>(w->d), a->codes, a->pitch, a->scales);
+    CK(launch_k(ctx, quantize_q4_kernel<__nv_bfloat16>, grid, 256, 0, static_cast<const __nv_bfloat16*>(w->ptr), w->rows, static_cast<int>(w->d), a->codes, a->pitch, a->scales));
   else
-    quantize_q4_kernel<float><<<grid, 256, 0, ctx->stream>>>(static_cast<const float*>(w->ptr), w->rows, static_cast<int>(w->d), a->codes, a->pitch, a->scales);
-  ctx->launches++;
+    CK(launch_k(ctx, quantize_q4_kernel<float>, grid, 256, 0, static_cast<const float*>(w->ptr), w->rows, static_cast<int>(w->d), a->codes, a->pitch, a->scales));
   e = cudaGetLastError();
   if (e != cudaSuccess) {
     cudaFree(a->codes);
     cudaFree(a->scales);
     delete a;
     return set_err(HIRE_ERR_RUNTIME, std::string("quantize_q4_kernel: ") + cudaGetErrorString(e));
+  }
+  if (a->d % 64 == 0) {
+    const int rc = ensure_mma_layout(ctx, a);
+    if (rc != HIRE_OK) { hire_scorer_destroy(a); return rc; }
   }
   *out = a;
   return HIRE_OK;
@@ -817,9 +1014,12 @@ int hire_scorer_slice(hire_scorer a, int64_t first, int64_t count, hire_scorer* 
   auto* s = new hire_scorer_s(*a);
   s->owned = false;
   s->rows = count;
+  s->mma = nullptr;
+  s->mma_owned = false;
   if (a->kind == HIRE_SCORER_Q4) {
     s->codes = a->codes + first * a->pitch;
     s->scales = a->scales + first;
+    if (a->mma && first % 16 == 0) s->mma = a->mma + (first / 16) * (a->d / 64) * 32;
   } else {
     s->z2 = static_cast<char*>(a->z2) + first * a->r * dtype_size(a->dtype);
   }
@@ -860,6 +1060,7 @@ int hire_scorer_destroy(hire_scorer a) {
     cudaFree(a->z1);
     cudaFree(a->z2);
   }
+  if (a->mma_owned) cudaFree(a->mma);
   delete a;
   return HIRE_OK;
 }
@@ -901,8 +1102,7 @@ int hire_topk_select(hire_ctx ctx, const float* v, int64_t B, int64_t n, int64_t
   ar.take(&cv, static_cast<size_t>(B * sp.k_eff));
   RET(ar.commit(ctx));
   RET(run_select(ctx, v, n, n, B, sp, surv, cand, sp.k_eff, status));
-  gather_values_kernel<<<static_cast<unsigned>(ceil_div(B * sp.k_eff, 256)), 256, 0, ctx->stream>>>(v, n, cand, sp.k_eff, B, cv);
-  ctx->launches++;
+  CK(launch_k(ctx, gather_values_kernel, static_cast<unsigned>(ceil_div(B * sp.k_eff, 256)), 256, 0, v, n, cand, sp.k_eff, B, cv));
   CK(cudaGetLastError());
   RET(run_final(ctx, cv, sp.k_eff, cand, sp.k_eff, nullptr, 0, 0, sp.k_eff, sp.k_eff, B, 0, idx, val,
                 nullptr, nullptr, sp.k_eff));
@@ -1026,8 +1226,7 @@ int ffn_select(hire_ctx ctx, const hire_matrix_s* u, const hire_scorer_s* a, con
   RET(run_scores(ctx, a, x, B, phi, x_mode, strict, fw.t.sw, fw.t.scores, m));
   const float* proxy = fw.t.scores;
   if (g > 1) {
-    group_proxy_kernel<<<static_cast<unsigned>(ceil_div(ng * B, 256)), 256, 0, ctx->stream>>>(fw.t.scores, m, ng, static_cast<int>(g), static_cast<int>(B), fw.proxy);
-    ctx->launches++;
+    CK(launch_k(ctx, group_proxy_kernel, static_cast<unsigned>(ceil_div(ng * B, 256)), 256, 0, fw.t.scores, m, ng, static_cast<int>(g), static_cast<int>(B), fw.proxy));
     CK(cudaGetLastError());
     proxy = fw.proxy;
   }
@@ -1039,17 +1238,14 @@ int ffn_select(hire_ctx ctx, const hire_matrix_s* u, const hire_scorer_s* a, con
                   nullptr, nullptr, sel_stride));
     return HIRE_OK;
   }
-  expand_groups_kernel<<<static_cast<unsigned>(ceil_div(kpg * g * B, 256)), 256, 0, ctx->stream>>>(fw.cand, kpg, kpg, static_cast<int>(g), static_cast<int>(B), fw.units);
-  ctx->launches++;
+  CK(launch_k(ctx, expand_groups_kernel, static_cast<unsigned>(ceil_div(kpg * g * B, 256)), 256, 0, fw.cand, kpg, kpg, static_cast<int>(g), static_cast<int>(B), fw.units));
   CK(cudaGetLastError());
   RET(run_recompute(ctx, u, fw.units, kpg * g, kpg * g, x, B, phi, strict, fw.act, kpg * g));
-  group_sum_kernel<<<static_cast<unsigned>(ceil_div(kpg * B, 256)), 256, 0, ctx->stream>>>(fw.act, kpg, static_cast<int>(g), static_cast<int>(B), fw.gval);
-  ctx->launches++;
+  CK(launch_k(ctx, group_sum_kernel, static_cast<unsigned>(ceil_div(kpg * B, 256)), 256, 0, fw.act, kpg, static_cast<int>(g), static_cast<int>(B), fw.gval));
   CK(cudaGetLastError());
   RET(run_final(ctx, fw.gval, kpg, fw.cand, kpg, nullptr, 0, 0, kpg, kg, B, 1, sel, fw.selv, nullptr,
                 nullptr, sel_stride));
-  expand_groups_kernel<<<static_cast<unsigned>(ceil_div(kg * g * B, 256)), 256, 0, ctx->stream>>>(sel, sel_stride, kg, static_cast<int>(g), static_cast<int>(B), fw.selu);
-  ctx->launches++;
+  CK(launch_k(ctx, expand_groups_kernel, static_cast<unsigned>(ceil_div(kg * g * B, 256)), 256, 0, sel, sel_stride, kg, static_cast<int>(g), static_cast<int>(B), fw.selu));
   CK(cudaGetLastError());
   RET(run_recompute(ctx, u, fw.selu, kg * g, kg * g, x, B, phi, strict, fw.selact, kg * g));
   return HIRE_OK;
@@ -1130,8 +1326,7 @@ int hire_ffn_dense_run(hire_ctx ctx, hire_matrix u, hire_matrix v, const float* 
   ar.take(&partial, static_cast<size_t>(B * ceil_div(m, 8) * u->d));
   RET(ar.commit(ctx));
   RET(run_recompute(ctx, u, nullptr, 0, m, x, B, phi, strict, act, m));
-  iota_mod_kernel<<<static_cast<unsigned>(ceil_div(B * m, 256)), 256, 0, ctx->stream>>>(units, m, B * m);
-  ctx->launches++;
+  CK(launch_k(ctx, iota_mod_kernel, static_cast<unsigned>(ceil_div(B * m, 256)), 256, 0, units, m, B * m));
   CK(cudaGetLastError());
   return run_down(ctx, v, units, act, m, m, B, strict, partial, out);
 }
@@ -1202,8 +1397,7 @@ int da_local(hire_ctx ctx, const hire_matrix_s* w, const hire_scorer_s* a, int64
   RET(ar.commit(ctx));
   RET(local_candidates(ctx, w, a, x, B, p, dp.sp, t, t.cand));
   if (offset) {
-    add_offset_kernel<<<static_cast<unsigned>(ceil_div(B * dp.sp.k_eff, 256)), 256, 0, ctx->stream>>>(t.cand, B * dp.sp.k_eff, static_cast<uint32_t>(offset));
-    ctx->launches++;
+    CK(launch_k(ctx, add_offset_kernel, static_cast<unsigned>(ceil_div(B * dp.sp.k_eff, 256)), 256, 0, t.cand, B * dp.sp.k_eff, static_cast<uint32_t>(offset)));
     CK(cudaGetLastError());
   }
   const int64_t K = merge == HIRE_MERGE_PER_SHARD ? std::min(dp.kl, dp.sp.k_eff) : dp.sp.k_eff;
@@ -1261,6 +1455,7 @@ int hire_da_topk_run(hire_ctx ctx, hire_comm comm, hire_matrix w, hire_scorer a,
   uint64_t* recv = reinterpret_cast<uint64_t*>(static_cast<char*>(ctx->io_dev) + sendb);
   RET(da_local(ctx, w, a, first, x, B, p, dp, merge, world == 1 ? recv : send));
   if (world > 1) {
+    StageScope scope(ctx, kStageComm);
     CKN(ncclAllGather(send, recv, static_cast<size_t>(B * dp.kq_max), ncclUint64, comm->comm, ctx->stream));
   }
   bool cl = false;
@@ -1338,6 +1533,8 @@ int plan_da_ffn(const hire_ffn_params* p, int64_t total_units, int64_t width_gro
 
 __global__ void concat_sel_kernel(const uint32_t* recv, int world, int64_t B, int64_t kg_max,
                                   const int64_t* counts, int64_t kg, uint32_t* sel) {
+  hire_dev::griddep_wait();
+  hire_dev::griddep_launch();
   // counts[r] valid entries per rank (same for every query); rank-major
   // concatenation of ascending shard-local lists is globally ascending.
   const int64_t b = blockIdx.x;
@@ -1372,14 +1569,15 @@ int da_ffn_local(hire_ctx ctx, const hire_matrix_s* u, const hire_matrix_s* v, c
   // global group ids into the send slots (padded rows untouched)
   CK(cudaMemcpy2DAsync(sel_out, sel_stride * 4, sel_local, fp.kgl * 4, fp.kgl * 4, B, cudaMemcpyDeviceToDevice, ctx->stream));
   if (first_group) {
-    add_offset_strided_kernel<<<static_cast<unsigned>(ceil_div(fp.kgl * B, 256)), 256, 0, ctx->stream>>>(sel_out, sel_stride, fp.kgl, B, static_cast<uint32_t>(first_group));
-    ctx->launches++;
+    CK(launch_k(ctx, add_offset_strided_kernel, static_cast<unsigned>(ceil_div(fp.kgl * B, 256)), 256, 0, sel_out, sel_stride, fp.kgl, B, static_cast<uint32_t>(first_group)));
     CK(cudaGetLastError());
   }
   return HIRE_OK;
 }
 
 __global__ void sum_parts_kernel(const float* parts, int world, int64_t n, float* out) {
+  hire_dev::griddep_wait();
+  hire_dev::griddep_launch();
   const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i >= n) return;
   float s = 0.0f;
@@ -1416,6 +1614,7 @@ int hire_da_ffn_run(hire_ctx ctx, hire_comm comm, hire_matrix u, hire_matrix v, 
   int64_t* cnt = reinterpret_cast<int64_t*>(static_cast<char*>(ctx->io_dev) + sendb + recvb);
   RET(da_ffn_local(ctx, u, v, a, fg, x, B, p, fp, world == 1 ? recv : send, fp.kg_max, out));
   if (world > 1) {
+    StageScope scope(ctx, kStageComm);
     CKN(ncclGroupStart());
     CKN(ncclAllGather(send, recv, static_cast<size_t>(B * fp.kg_max), ncclUint32, comm->comm, ctx->stream));
     CKN(ncclAllReduce(out, out, static_cast<size_t>(B * u->d), ncclFloat32, ncclSum, comm->comm, ctx->stream));
@@ -1430,8 +1629,7 @@ int hire_da_ffn_run(hire_ctx ctx, hire_comm comm, hire_matrix u, hire_matrix v, 
     total += counts[r];
   }
   CK(cudaMemcpyAsync(cnt, counts.data(), world * 8, cudaMemcpyHostToDevice, ctx->stream));
-  concat_sel_kernel<<<static_cast<unsigned>(B), 128, 0, ctx->stream>>>(recv, world, B, fp.kg_max, cnt, total, sel);
-  ctx->launches++;
+  CK(launch_k(ctx, concat_sel_kernel, static_cast<unsigned>(B), 128, 0, recv, world, B, fp.kg_max, cnt, total, sel));
   CK(cudaGetLastError());
   CK(cudaStreamSynchronize(ctx->stream));  // counts is a pageable host vector
   return HIRE_OK;
@@ -1478,8 +1676,7 @@ int hire_da_ffn_emulated(hire_ctx ctx, hire_matrix u, hire_matrix v, hire_scorer
     total += counts[r];
   }
   CK(cudaMemcpyAsync(cnt, counts.data(), world * 8, cudaMemcpyHostToDevice, ctx->stream));
-  concat_sel_kernel<<<static_cast<unsigned>(B), 128, 0, ctx->stream>>>(recv, world, B, kg_max, cnt, total, sel);
-  ctx->launches++;
+  CK(launch_k(ctx, concat_sel_kernel, static_cast<unsigned>(B), 128, 0, recv, world, B, kg_max, cnt, total, sel));
   CK(cudaGetLastError());
   if (p->strict) {
     // the reference's own order: one ascending sum over the union
@@ -1489,13 +1686,11 @@ int hire_da_ffn_emulated(hire_ctx ctx, hire_matrix u, hire_matrix v, hire_scorer
     ar.take(&units, static_cast<size_t>(B * total * g));
     ar.take(&act, static_cast<size_t>(B * total * g));
     RET(ar.commit(ctx));
-    expand_groups_kernel<<<static_cast<unsigned>(ceil_div(total * g * B, 256)), 256, 0, ctx->stream>>>(sel, total, total, static_cast<int>(g), static_cast<int>(B), units);
-    ctx->launches++;
+    CK(launch_k(ctx, expand_groups_kernel, static_cast<unsigned>(ceil_div(total * g * B, 256)), 256, 0, sel, total, total, static_cast<int>(g), static_cast<int>(B), units));
     RET(run_recompute(ctx, u, units, total * g, total * g, x, B, p->phi, 1, act, total * g));
     RET(run_down(ctx, v, units, act, total * g, total * g, B, 1, nullptr, out));
   } else {
-    sum_parts_kernel<<<static_cast<unsigned>(ceil_div(B * u->d, 256)), 256, 0, ctx->stream>>>(parts, world, B * u->d, out);
-    ctx->launches++;
+    CK(launch_k(ctx, sum_parts_kernel, static_cast<unsigned>(ceil_div(B * u->d, 256)), 256, 0, parts, world, B * u->d, out));
     CK(cudaGetLastError());
   }
   CK(cudaStreamSynchronize(ctx->stream));

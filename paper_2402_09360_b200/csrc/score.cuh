@@ -30,6 +30,8 @@ __global__ void __launch_bounds__(256) prep_x_int8_kernel(
     const float* __restrict__ x, int d, int8_t* __restrict__ xq,
     int8_t* __restrict__ xperm, float* __restrict__ sx_out,
     int* __restrict__ sumxq_out) {
+  hire_dev::griddep_wait();
+  hire_dev::griddep_launch();
   const int b = blockIdx.x;
   const float* xb = x + static_cast<int64_t>(b) * d;
   __shared__ float s_red[8];
@@ -86,6 +88,8 @@ __global__ void __launch_bounds__(256) q4_score_fast_int8(
     int64_t rows, int d, const int8_t* __restrict__ xperm,
     const float* __restrict__ sx, const int* __restrict__ sumxq, int phi,
     float* __restrict__ scores, int64_t score_stride) {
+  hire_dev::griddep_wait();
+  hire_dev::griddep_launch();
   const int lane = threadIdx.x & 31;
   const int64_t warp = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
@@ -165,6 +169,8 @@ __global__ void __launch_bounds__(256) q4_score_fast_fpx(
     const uint8_t* __restrict__ wq, int64_t pitch, const float* __restrict__ scales,
     int64_t rows, int d, const float* __restrict__ x, int phi,
     float* __restrict__ scores) {
+  hire_dev::griddep_wait();
+  hire_dev::griddep_launch();
   const int lane = threadIdx.x & 31;
   const int64_t warp = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
@@ -213,6 +219,8 @@ __global__ void __launch_bounds__(128) q4_score_seq(
     int64_t rows, int d, const float* __restrict__ x, const int8_t* __restrict__ xq,
     const float* __restrict__ sx, int int8_mode, int phi, float* __restrict__ scores,
     int64_t score_stride) {
+  hire_dev::griddep_wait();
+  hire_dev::griddep_launch();
   extern __shared__ __align__(16) unsigned char smem[];
   float* s_x = reinterpret_cast<float*>(smem);
   int8_t* s_xq = reinterpret_cast<int8_t*>(smem + static_cast<size_t>(d) * 4);
@@ -264,6 +272,8 @@ template <typename T>
 __global__ void __launch_bounds__(256) quantize_q4_kernel(
     const T* __restrict__ w, int64_t rows, int d, uint8_t* __restrict__ wq, int64_t pitch,
     float* __restrict__ scales) {
+  hire_dev::griddep_wait();
+  hire_dev::griddep_launch();
   const int lane = threadIdx.x & 31;
   const int64_t r = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   if (r >= rows) return;
@@ -301,6 +311,8 @@ template <typename T>
 __global__ void __launch_bounds__(256) lr_t_kernel(const T* __restrict__ z1, int r, int d,
                                                    const float* __restrict__ x, int B,
                                                    int strict, float* __restrict__ t) {
+  hire_dev::griddep_wait();
+  hire_dev::griddep_launch();
   if (strict) {
     const int id = blockIdx.x * blockDim.x + threadIdx.x;
     if (id >= r * B) return;
@@ -334,6 +346,8 @@ template <typename T, int R, bool STRICT>
 __global__ void __launch_bounds__(128) lr_score_kernel(
     const T* __restrict__ z2, int64_t rows, const float* __restrict__ t, int B, int phi,
     float* __restrict__ scores, int64_t score_stride) {
+  hire_dev::griddep_wait();
+  hire_dev::griddep_launch();
   extern __shared__ __align__(16) unsigned char smem[];
   float* s_t = reinterpret_cast<float*>(smem);
   for (int i = threadIdx.x; i < R * B; i += blockDim.x) s_t[i] = t[i];
@@ -375,6 +389,8 @@ template <typename T, bool STRICT>
 __global__ void __launch_bounds__(128) lr_score_generic(
     const T* __restrict__ z2, int64_t rows, int r, const float* __restrict__ t, int B, int phi,
     float* __restrict__ scores, int64_t score_stride) {
+  hire_dev::griddep_wait();
+  hire_dev::griddep_launch();
   extern __shared__ __align__(16) unsigned char smem[];
   float* s_t = reinterpret_cast<float*>(smem);
   for (int i = threadIdx.x; i < r * B; i += blockDim.x) s_t[i] = t[i];
@@ -391,6 +407,187 @@ __global__ void __launch_bounds__(128) lr_score_generic(
       else acc = fmaf(zq, tb[q], acc);
     }
     scores[static_cast<int64_t>(b) * score_stride + j] = apply_phi(phi, acc);
+  }
+}
+
+}  // namespace hire_dev
+
+namespace hire_dev {
+
+
+// ---------------------------------------------------------------------
+// MMA-tiled int4 layout for the tensor-core proxy (K1-mma). For row-block
+// rb (16 rows) and k-block kb (64 columns), 512 bytes; lane l (g = l>>2,
+// t = l&3) owns bytes [16l, 16l+16) = words w0..w3 with, for k-tile
+// j = w>>1 and half h = w&1:
+//   low  nibble of byte p = code(row 16rb+g,   col 64kb + 32j + 16h + 4t + p)
+//   high nibble of byte p = code(row 16rb+g+8, col 64kb + 32j + 16h + 4t + p)
+// i.e. after (w ^ 0x88888888) the lo/hi masks are exactly the m16n8k32
+// A-fragment registers {a0,a1} (h=0) and {a2,a3} (h=1) of k-tile j, offset
+// by +8 (unsigned digits 1..15). One 128-bit load per lane feeds 2 MMAs.
+// ---------------------------------------------------------------------
+__global__ void q4_to_mma_layout(const uint8_t* __restrict__ wq, int64_t pitch, int64_t rows,
+                                 int d, uint32_t* __restrict__ out, int64_t n_words) {
+  hire_dev::griddep_wait();
+  hire_dev::griddep_launch();
+  const int64_t id = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (id >= n_words) return;
+  const int nkb = d / 64;
+  const int w = static_cast<int>(id & 3);
+  const int lane = static_cast<int>((id >> 2) & 31);
+  const int64_t blk = id >> 7;
+  const int64_t rb = blk / nkb, kb = blk % nkb;
+  const int g = lane >> 2, t = lane & 3;
+  const int j = w >> 1, h = w & 1;
+  uint32_t word = 0;
+#pragma unroll
+  for (int p = 0; p < 4; ++p) {
+    const int64_t col = kb * 64 + 32 * j + 16 * h + 4 * t + p;
+#pragma unroll
+    for (int hi = 0; hi < 2; ++hi) {
+      const int64_t row = rb * 16 + g + 8 * hi;
+      uint32_t nib = 0;
+      if (row < rows) {
+        const uint8_t byte = wq[row * pitch + col / 2];
+        nib = (col & 1) ? (byte >> 4) : (byte & 0xF);
+      }
+      word |= nib << (8 * p + 4 * hi);
+    }
+  }
+  out[id] = word;
+}
+
+__device__ __forceinline__ void mma_u8s8(int (&c)[4], uint32_t a0, uint32_t a1, uint32_t a2,
+                                         uint32_t a3, uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k32.row.col.s32.u8.s8.s32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+      "{%0,%1,%2,%3};"
+      : "+r"(c[0]), "+r"(c[1]), "+r"(c[2]), "+r"(c[3])
+      : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+
+// ---------------------------------------------------------------------
+// K1 integer mode on the tensor cores: int4 (as u8 digits c+8) x int8 x
+// -> int32, mma.sync m16n8k32. NT n-tiles of 8 queries. A CTA of 8 warps
+// owns 8/KS row-blocks; the KS warps of a row-block split its k range and
+// their int32 accumulators are summed exactly through shared memory.
+// Persistent over row-block groups; x (int8, natural order, padded rows)
+// staged in shared memory once per CTA. Exact: identical integers to the
+// dp4a path and the oracle.
+// ---------------------------------------------------------------------
+template <int NT, int KS>
+__global__ void __launch_bounds__(256) q4_score_mma(
+    const uint4* __restrict__ wmma, int64_t rows, int d, const float* __restrict__ scales,
+    const int8_t* __restrict__ xq, const float* __restrict__ sx, const int* __restrict__ sumxq,
+    int B, int phi, float* __restrict__ scores, int64_t score_stride) {
+  hire_dev::griddep_wait();
+  hire_dev::griddep_launch();
+  extern __shared__ __align__(16) unsigned char smem[];
+  constexpr int RB_PER_CTA = 8 / KS;
+  const int xs = d + 16;  // padded query stride (bank spread)
+  int8_t* s_x = reinterpret_cast<int8_t*>(smem);
+  int* s_acc = reinterpret_cast<int*>(smem + static_cast<size_t>(NT) * 8 * xs);  // [8 warps][NT][4][32]
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  const int nkb = d / 64;
+  const int64_t n_rb = (rows + 15) / 16;
+  const int rb_local = wid / KS, ks = wid % KS;
+  const int kb0 = ks * nkb / KS, kb1 = (ks + 1) * nkb / KS;
+
+  // prologue independent of the producer kernel: first weight loads
+  int64_t rb = static_cast<int64_t>(blockIdx.x) * RB_PER_CTA + rb_local;
+  const int64_t rb_stride = static_cast<int64_t>(gridDim.x) * RB_PER_CTA;
+  constexpr int U = 4;
+  uint4 a[U];
+  if (rb < n_rb) {
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (kb0 + u < kb1) a[u] = ldg_stream(wmma + ((rb * nkb + kb0 + u) * 32 + lane));
+  }
+  griddep_wait();  // x quantisation (prep_x_int8_kernel) is complete
+  griddep_launch();
+  for (int i = threadIdx.x; i < NT * 8 * (d / 16); i += blockDim.x) {
+    const int n = i / (d / 16), c = i % (d / 16);
+    int4 v = make_int4(0, 0, 0, 0);
+    if (n < B) v = *reinterpret_cast<const int4*>(xq + static_cast<int64_t>(n) * d + c * 16);
+    *reinterpret_cast<int4*>(s_x + n * xs + c * 16) = v;
+  }
+  __syncthreads();
+
+  for (int64_t rb_base = static_cast<int64_t>(blockIdx.x) * RB_PER_CTA; rb_base < n_rb; rb_base += rb_stride) {
+    rb = rb_base + rb_local;
+    int acc[NT][4];
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) acc[nt][0] = acc[nt][1] = acc[nt][2] = acc[nt][3] = 0;
+    if (rb < n_rb) {
+      for (int kb = kb0; kb < kb1; kb += U) {
+        uint4 nxt[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+          if (kb + U + u < kb1) nxt[u] = ldg_stream(wmma + ((rb * nkb + kb + U + u) * 32 + lane));
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          if (kb + u >= kb1) break;
+          const uint32_t w4[4] = {a[u].x, a[u].y, a[u].z, a[u].w};
+#pragma unroll
+          for (int j = 0; j < 2; ++j) {
+            const uint32_t u0 = w4[2 * j] ^ 0x88888888u, u1 = w4[2 * j + 1] ^ 0x88888888u;
+            const uint32_t a0 = u0 & 0x0F0F0F0Fu, a1 = (u0 >> 4) & 0x0F0F0F0Fu;
+            const uint32_t a2 = u1 & 0x0F0F0F0Fu, a3 = (u1 >> 4) & 0x0F0F0F0Fu;
+            const int k0 = (kb + u) * 64 + 32 * j;
+#pragma unroll
+            for (int nt = 0; nt < NT; ++nt) {
+              const int8_t* xr = s_x + (nt * 8 + g) * xs + k0 + 4 * t;
+              const uint32_t b0 = *reinterpret_cast<const uint32_t*>(xr);
+              const uint32_t b1 = *reinterpret_cast<const uint32_t*>(xr + 16);
+              mma_u8s8(acc[nt], a0, a1, a2, a3, b0, b1);
+            }
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) a[u] = nxt[u];
+      }
+    }
+    // next row-block's first loads (software pipeline across row-blocks)
+    const int64_t rbn = rb + rb_stride;
+    if (rbn < n_rb) {
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        if (kb0 + u < kb1) a[u] = ldg_stream(wmma + ((rbn * nkb + kb0 + u) * 32 + lane));
+    }
+    if constexpr (KS > 1) {
+      int* mine = s_acc + (wid * NT * 4) * 32;
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) mine[(nt * 4 + e) * 32 + lane] = acc[nt][e];
+      __syncthreads();
+      if (ks == 0) {
+        for (int o = 1; o < KS; ++o) {
+          const int* other = s_acc + ((wid + o) * NT * 4) * 32;
+#pragma unroll
+          for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+            for (int e = 0; e < 4; ++e) acc[nt][e] += other[(nt * 4 + e) * 32 + lane];
+        }
+      }
+      __syncthreads();
+    }
+    if (ks == 0 && rb < n_rb) {
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const int64_t row = rb * 16 + g + ((e & 2) ? 8 : 0);
+          const int n = nt * 8 + 2 * t + (e & 1);
+          if (row < rows && n < B) {
+            const int aint = acc[nt][e] - 8 * sumxq[n];
+            const float cs = __fmul_rn(scales[row], sx[n]);
+            scores[static_cast<int64_t>(n) * score_stride + row] =
+                apply_phi(phi, __fmul_rn(static_cast<float>(aint), cs));
+          }
+        }
+    }
   }
 }
 

@@ -151,6 +151,8 @@ constexpr int kBucketMaxWidth = 4096;
 __global__ void __launch_bounds__(256) bucket_topt_kernel(
     const float* __restrict__ scores, int64_t score_stride, int64_t n, int n_buckets, int t,
     uint64_t* __restrict__ surv) {
+  hire_dev::griddep_wait();
+  hire_dev::griddep_launch();
   __shared__ uint64_t s_keys[kBucketMaxWidth];
   __shared__ SelectScratch sc;
   const int bk = blockIdx.x, b = blockIdx.y;
@@ -185,6 +187,8 @@ __global__ void __launch_bounds__(kSelectThreads) select_candidates_kernel(
     int mode, const float* __restrict__ scores, int64_t score_stride, int64_t n,
     const uint64_t* __restrict__ surv, int n_buckets, int t, int K, int exact_fix,
     uint32_t* __restrict__ cand, int64_t cand_stride, int* __restrict__ status) {
+  hire_dev::griddep_wait();
+  hire_dev::griddep_launch();
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ SelectScratch sc;
   __shared__ int s_flag[2];
@@ -293,6 +297,8 @@ __global__ void __launch_bounds__(kSelectThreads) final_select_kernel(
     const uint64_t* __restrict__ src_keys, int n_per, int64_t part_stride, int n, int K,
     int out_mode, uint32_t* __restrict__ out_idx, float* __restrict__ out_val,
     float* __restrict__ out_prob, uint64_t* __restrict__ out_keys, int64_t out_stride) {
+  hire_dev::griddep_wait();
+  hire_dev::griddep_launch();
   constexpr int NT = kSelectThreads;
   __shared__ SelectScratch sc;
   extern __shared__ __align__(16) unsigned char smem_final[];

@@ -58,7 +58,8 @@ def test_quantize_int4_bitexact(H, O, V, d, dtype):
 
 # ------------------------------------------------------------------ K1 ---
 @pytest.mark.parametrize("V,d,B", [(1000, 1024, 1), (513, 2048, 3), (77, 4096, 5), (100, 33, 2),
-                                   (4099, 2048, 8)])
+                                   (4099, 2048, 8), (300, 1024, 12), (200, 2048, 40),
+                                   (100, 1024, 70), (50, 192, 3), (8192, 2048, 8)])
 @pytest.mark.parametrize("phi", [0, 1])
 def test_q4_scores_int8_bitexact(H, O, V, d, B, phi):
     w = _data.rng(V + d).standard_normal((V, d), dtype=np.float32)
@@ -68,6 +69,23 @@ def test_q4_scores_int8_bitexact(H, O, V, d, B, phi):
     got = N(a.scores(T(x), phi=phi, x_mode=H.X_INT8))
     for b in range(B):
         want = O.q4_scores_int8(codes, scales, x[b], phi)
+        assert np.array_equal(got[b].view(np.uint32), want.view(np.uint32)), b
+
+
+@pytest.mark.parametrize("V,d,B", [(1000, 1024, 5), (513, 2048, 3), (4099, 2048, 8)])
+def test_q4_scores_int8_dp4a_path_bitexact(H, O, V, d, B, monkeypatch):
+    """The CUDA-core dp4a kernel (HIRE_PROXY_KERNEL=dp4a) gives the same
+    integers as the tensor-core kernel and the oracle."""
+    monkeypatch.setenv("HIRE_PROXY_KERNEL", "dp4a")
+    ctx = H.Context(0)
+    w = _data.rng(V * 3 + d).standard_normal((V, d), dtype=np.float32)
+    codes, scales = O.quantize_int4(w)
+    a = H.ApproxScorer.quantized(codes, scales)
+    x = _data.queries(B, d, 8, scale=1.0)
+    got = N(a.scores(T(x), phi=0, x_mode=H.X_INT8, ctx=ctx))
+    torch.cuda.synchronize()
+    for b in range(B):
+        want = O.q4_scores_int8(codes, scales, x[b], 0)
         assert np.array_equal(got[b].view(np.uint32), want.view(np.uint32)), b
 
 
