@@ -105,6 +105,13 @@ HIRE_API int64_t hire_ctx_launch_count(hire_ctx ctx);
 HIRE_API int hire_ctx_set_profiling(hire_ctx ctx, int on);
 HIRE_API int hire_ctx_profile_read(hire_ctx ctx, double* ms, int64_t* counts, int n_stages);
 
+/* ---- device buffers (for wrappers that start from host data) ------------ */
+HIRE_API int hire_device_alloc(int64_t bytes, void** out);
+HIRE_API int hire_device_free(void* p);
+/* kind: 0 host->device, 1 device->host, 2 device->device; ordered on the
+ * context stream; returns after the copy completes when sync != 0 */
+HIRE_API int hire_copy(hire_ctx ctx, void* dst, const void* src, int64_t bytes, int kind, int sync);
+
 /* ---- dense matrices (ScoreMatrix, linalg.hpp:44-90) --------------------- */
 /* Copies src (host or device) into an owned device buffer; dtype HIRE_F32 or
  * HIRE_BF16 (the device storage type; src has the same type). */

@@ -25,6 +25,7 @@ EXPORTS = [
     "hire_last_error", "hire_abi_version",
     "hire_ctx_create", "hire_ctx_destroy", "hire_ctx_stream", "hire_ctx_synchronize",
     "hire_ctx_launch_count", "hire_ctx_set_profiling", "hire_ctx_profile_read",
+    "hire_device_alloc", "hire_device_free", "hire_copy",
     "hire_matrix_create", "hire_matrix_view", "hire_matrix_slice", "hire_matrix_destroy",
     "hire_matrix_info",
     "hire_scorer_create_q4_codes", "hire_scorer_create_q4_hirq", "hire_scorer_quantize",
@@ -77,6 +78,9 @@ def _sig(L):
         "hire_ctx_synchronize": [_vp],
         "hire_ctx_set_profiling": [_vp, _i32],
         "hire_ctx_profile_read": [_vp, _vp, _vp, _i32],
+        "hire_device_alloc": [_i64, _p(_vp)],
+        "hire_device_free": [_vp],
+        "hire_copy": [_vp, _vp, _vp, _i64, _i32, _i32],
         "hire_matrix_create": [_vp, _i64, _i64, _i32, _i32, _p(_vp)],
         "hire_matrix_view": [_vp, _i64, _i64, _i32, _p(_vp)],
         "hire_matrix_slice": [_vp, _i64, _i64, _p(_vp)],

@@ -817,6 +817,30 @@ int hire_ctx_profile_read(hire_ctx c, double* ms, int64_t* counts, int n_stages)
   return HIRE_OK;
 }
 
+// ------------------------------------------------------- device buffers --
+int hire_device_alloc(int64_t bytes, void** out) {
+  if (!out || bytes < 0) return invalid("bad allocation request");
+  *out = nullptr;
+  if (bytes == 0) return HIRE_OK;
+  CK(cudaMalloc(out, static_cast<size_t>(bytes)));
+  return HIRE_OK;
+}
+
+int hire_device_free(void* p) {
+  if (p) CK(cudaFree(p));
+  return HIRE_OK;
+}
+
+int hire_copy(hire_ctx ctx, void* dst, const void* src, int64_t bytes, int kind, int sync) {
+  if (!ctx || (!dst && bytes) || (!src && bytes) || bytes < 0) return invalid("bad copy request");
+  if (bytes == 0) return HIRE_OK;
+  const cudaMemcpyKind k = kind == 0 ? cudaMemcpyHostToDevice
+                                     : (kind == 1 ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice);
+  CK(cudaMemcpyAsync(dst, src, static_cast<size_t>(bytes), k, ctx->stream));
+  if (sync) CK(cudaStreamSynchronize(ctx->stream));
+  return HIRE_OK;
+}
+
 // ------------------------------------------------------------- matrices --
 int hire_matrix_create(const void* src, int64_t rows, int64_t d, int dtype, int src_on_device,
                        hire_matrix* out) {
