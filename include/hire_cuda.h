@@ -100,9 +100,12 @@ HIRE_API int64_t hire_ctx_launch_count(hire_ctx ctx);
  * events on the context stream. profile_read synchronises, returns the
  * summed milliseconds and the number of timed intervals per stage
  * (0 proxy scores, 1 candidate select, 2 gather recompute, 3 final top-k,
- * 4 FFN down-projection, 5 NCCL collective, 6 int8 x quantisation), and
- * clears the record. */
+ * 4 FFN down-projection, 5 NCCL collective, 6 int8 x quantisation,
+ * 7 the fused single-launch HiRE-FFN layer), and clears the record. */
 HIRE_API int hire_ctx_set_profiling(hire_ctx ctx, int on);
+/* Phase timestamps (%globaltimer, ns) of the last fused-kernel launch, when the
+ * context was created with HIRE_FUSED_TRACE=1 in the environment. */
+HIRE_API int hire_ctx_read_trace(hire_ctx ctx, long long* out, int n);
 HIRE_API int hire_ctx_profile_read(hire_ctx ctx, double* ms, int64_t* counts, int n_stages);
 
 /* ---- device buffers (for wrappers that start from host data) ------------ */

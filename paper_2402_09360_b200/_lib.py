@@ -18,13 +18,13 @@ SCORER_LOWRANK, SCORER_Q4 = 1, 2
 X_FP32, X_INT8 = 0, 1
 SELECT_EXACT, SELECT_BUCKETED = 0, 1
 MERGE_PER_SHARD, MERGE_GLOBAL = 0, 1
-STAGES = ["proxy", "select", "recompute", "final", "down", "comm", "prep_x"]
+STAGES = ["proxy", "select", "recompute", "final", "down", "comm", "prep_x", "ffn_fused"]
 
 # Every symbol include/hire_cuda.h declares (checked by tests/test_lib_symbols.py).
 EXPORTS = [
     "hire_last_error", "hire_abi_version",
     "hire_ctx_create", "hire_ctx_destroy", "hire_ctx_stream", "hire_ctx_synchronize",
-    "hire_ctx_launch_count", "hire_ctx_set_profiling", "hire_ctx_profile_read",
+    "hire_ctx_launch_count", "hire_ctx_set_profiling", "hire_ctx_profile_read", "hire_ctx_read_trace",
     "hire_device_alloc", "hire_device_free", "hire_copy",
     "hire_matrix_create", "hire_matrix_view", "hire_matrix_slice", "hire_matrix_destroy",
     "hire_matrix_info",
@@ -77,6 +77,7 @@ def _sig(L):
         "hire_ctx_stream": [_vp, _p(_vp)],
         "hire_ctx_synchronize": [_vp],
         "hire_ctx_set_profiling": [_vp, _i32],
+        "hire_ctx_read_trace": [_vp, _vp, _i32],
         "hire_ctx_profile_read": [_vp, _vp, _vp, _i32],
         "hire_device_alloc": [_i64, _p(_vp)],
         "hire_device_free": [_vp],

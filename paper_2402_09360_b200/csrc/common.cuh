@@ -76,6 +76,35 @@ __device__ __forceinline__ uint4 ldg_stream(const void* p) {
 __device__ __forceinline__ float bf16_lo(uint32_t w) { return __uint_as_float(w << 16); }
 __device__ __forceinline__ float bf16_hi(uint32_t w) { return __uint_as_float(w & 0xFFFF0000u); }
 
+// ------------------------------------------------- block staging copies --
+// Global -> shared copies with U loads in flight per thread (a plain
+// `for (i = tid; ...) dst[i] = src[i]` loop serialises one L2/HBM latency
+// per iteration because each store waits for its load).
+template <int U = 8, typename T, typename F>
+__device__ __forceinline__ void block_copy_tf(T* __restrict__ dst, int n, F load) {
+  for (int i0 = threadIdx.x; i0 < n; i0 += static_cast<int>(blockDim.x) * U) {
+    T v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int i = i0 + u * static_cast<int>(blockDim.x);
+      if (i < n) v[u] = load(i);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int i = i0 + u * static_cast<int>(blockDim.x);
+      if (i < n) dst[i] = v[u];
+    }
+  }
+}
+template <int U = 8, typename T>
+__device__ __forceinline__ void block_copy(T* __restrict__ dst, const T* __restrict__ src, int n) {
+  block_copy_tf<U, T>(dst, n, [&](int i) { return src[i]; });
+}
+template <int U = 8, typename T>
+__device__ __forceinline__ void block_copy_cg(T* __restrict__ dst, const T* __restrict__ src, int n) {
+  block_copy_tf<U, T>(dst, n, [&](int i) { return __ldcg(src + i); });
+}
+
 // ------------------------------------------------------ warp reductions --
 __device__ __forceinline__ int warp_sum_i32(int v) {
 #pragma unroll

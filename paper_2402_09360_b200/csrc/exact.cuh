@@ -21,6 +21,18 @@ namespace hire_dev {
 
 template <typename T>
 struct Vec16;
+// E consecutive fp32 values of x from shared memory as 128-bit loads (the
+// scalar form compiles to E LDS.32 with a 4*E-byte lane stride — an E-way
+// bank conflict on every load).
+template <int E>
+__device__ __forceinline__ void load_x_vec(const float* p, float* out) {
+#pragma unroll
+  for (int q = 0; q < E / 4; ++q) {
+    const float4 v = *reinterpret_cast<const float4*>(p + 4 * q);
+    out[4 * q] = v.x; out[4 * q + 1] = v.y; out[4 * q + 2] = v.z; out[4 * q + 3] = v.w;
+  }
+}
+
 template <>
 struct Vec16<__nv_bfloat16> {
   static constexpr int kElems = 8;
@@ -51,7 +63,7 @@ __global__ void __launch_bounds__(256) recompute_fast(
   float* s_x = reinterpret_cast<float*>(smem);
   constexpr int E = Vec16<T>::kElems;
   const int b = blockIdx.y;
-  for (int i = threadIdx.x; i < d; i += blockDim.x) s_x[i] = x[static_cast<int64_t>(b) * d + i];
+  block_copy(s_x, x + static_cast<int64_t>(b) * d, d);
   __syncthreads();
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int64_t pitch_vec = static_cast<int64_t>(d) / E;  // 16-byte vectors per row
@@ -64,11 +76,11 @@ __global__ void __launch_bounds__(256) recompute_fast(
     float acc = 0.0f;
 #pragma unroll
     for (int c = 0; c < CPL; ++c) {
-      float f[E];
+      float f[E], xv[E];
       Vec16<T>::expand(v[c], f);
-      const float* xs = s_x + (lane + 32 * c) * E;
+      load_x_vec<E>(s_x + (lane + 32 * c) * E, xv);
 #pragma unroll
-      for (int e = 0; e < E; ++e) acc = fmaf(f[e], xs[e], acc);
+      for (int e = 0; e < E; ++e) acc = fmaf(f[e], xv[e], acc);
     }
     acc = warp_sum_f32(acc);
     if (lane == 0) out[b * out_stride + i] = apply_phi(phi, acc);
@@ -86,7 +98,7 @@ __global__ void __launch_bounds__(128) recompute_seq(
   extern __shared__ __align__(16) unsigned char smem[];
   float* s_x = reinterpret_cast<float*>(smem);
   const int b = blockIdx.y;
-  for (int i = threadIdx.x; i < d; i += blockDim.x) s_x[i] = x[static_cast<int64_t>(b) * d + i];
+  block_copy(s_x, x + static_cast<int64_t>(b) * d, d);
   __syncthreads();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n_cand) return;

@@ -24,6 +24,7 @@
 #include "../../include/hire_cuda.h"
 #include "common.cuh"
 #include "exact.cuh"
+#include "ffn_fused.cuh"
 #include "score.cuh"
 #include "select.cuh"
 
@@ -79,6 +80,9 @@ struct hire_ctx_s {
   int64_t launches = 0;
   bool pdl = true;
   bool force_dp4a = false;
+  bool ffn_fused = true;
+  bool trace = false;
+  int* counters = nullptr;  // zeroed hand-off counters of the fused kernels
   // stage profiling (hire_ctx_set_profiling): event pairs around each stage
   bool prof = false;
   std::vector<cudaEvent_t> ev_pool;
@@ -98,7 +102,7 @@ struct hire_ctx_s {
 namespace {
 // Stage ids for hire_ctx_profile_read.
 enum Stage { kStageProxy = 0, kStageSelect = 1, kStageRecompute = 2, kStageFinal = 3, kStageDown = 4,
-             kStageComm = 5, kStagePrep = 6, kNumStages = 8 };
+             kStageComm = 5, kStagePrep = 6, kStageFused = 7, kNumStages = 8 };
 
 struct StageScope {
   hire_ctx c;
@@ -304,7 +308,8 @@ int run_select(hire_ctx ctx, const float* scores, int64_t score_stride, int64_t 
                int* status) {
   StageScope scope(ctx, kStageSelect);
   if (sp.mode == 1) {
-    CK(launch_k(ctx, bucket_topt_kernel, dim3(sp.n_buckets, static_cast<unsigned>(B)), 256, 0, 
+    CK(launch_k(ctx, bucket_topt_kernel, dim3(sp.n_buckets, static_cast<unsigned>(B)), 256,
+                static_cast<size_t>(ceil_div(n, sp.n_buckets)) * 8, 
         scores, score_stride, n, sp.n_buckets, sp.t, surv));
     CK(cudaGetLastError());
   }
@@ -737,6 +742,8 @@ int hire_ctx_create(int device, void* stream, int own_stream, hire_ctx* out) {
                           kPoolKeys * 8));
   CK(cudaFuncSetAttribute(final_select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                           kFinalMax * 8));
+  CK(cudaFuncSetAttribute(bucket_topt_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                          kBucketMaxWidth * 8));
   // every other kernel with dynamic shared memory: allow up to 200 KB once,
   // here, so no attribute call ever happens inside a captured graph
   {
@@ -758,6 +765,10 @@ int hire_ctx_create(int device, void* stream, int own_stream, hire_ctx* out) {
     for (const void* k : ks) CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
   }
   if (const char* e = getenv("HIRE_PROXY_KERNEL")) c->force_dp4a = std::strcmp(e, "dp4a") == 0;
+  if (const char* e = getenv("HIRE_FFN_FUSED")) c->ffn_fused = std::strcmp(e, "0") != 0;
+  if (const char* e = getenv("HIRE_FUSED_TRACE")) c->trace = std::strcmp(e, "1") == 0;
+  CK(cudaMalloc(&c->counters, 256 * sizeof(int)));
+  CK(cudaMemset(c->counters, 0, 256 * sizeof(int)));
   if (const char* e = getenv("HIRE_NO_PDL")) c->pdl = std::strcmp(e, "1") != 0;
   *out = c;
   return HIRE_OK;
@@ -767,6 +778,7 @@ int hire_ctx_destroy(hire_ctx c) {
   if (!c) return HIRE_OK;
   cudaStreamSynchronize(c->stream);
   if (c->ws) cudaFree(c->ws);
+  if (c->counters) cudaFree(c->counters);
   if (c->io_dev) cudaFree(c->io_dev);
   if (c->io_host) cudaFreeHost(c->io_host);
   for (auto& m : c->marks) { cudaEventDestroy(m.second.first); cudaEventDestroy(m.second.second); }
@@ -789,6 +801,13 @@ int hire_ctx_synchronize(hire_ctx c) {
 }
 
 int64_t hire_ctx_launch_count(hire_ctx c) { return c ? c->launches : 0; }
+
+int hire_ctx_read_trace(hire_ctx c, long long* out, int n) {
+  if (!c || !out || n > 28) return invalid("bad trace request");
+  CK(cudaStreamSynchronize(c->stream));
+  CK(cudaMemcpy(out, c->counters + 192, static_cast<size_t>(n) * 8, cudaMemcpyDeviceToHost));
+  return HIRE_OK;
+}
 
 int hire_ctx_set_profiling(hire_ctx c, int on) {
   if (!c) return invalid("null handle");
@@ -1293,10 +1312,111 @@ void take_ffn_ws(Arena& ar, FfnWs* fw, const hire_scorer_s* a, int64_t B, int64_
 }
 }  // namespace
 
+}  // extern "C"
+
+namespace {
+template <typename T, int NT, int KS>
+int launch_ffn_fused_t(hire_ctx ctx, const FusedFfnArgs& args, size_t smem) {
+  auto k = ffn_fused_kernel<T, NT, KS>;
+  static int max_dyn = 0;
+  if (!max_dyn) {
+    cudaFuncAttributes fa;
+    CK(cudaFuncGetAttributes(&fa, k));
+    int optin = 0;
+    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, ctx->device);
+    max_dyn = optin - static_cast<int>(fa.sharedSizeBytes);
+    CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, max_dyn));
+  }
+  if (static_cast<int>(smem) > max_dyn) return 1;  // not taken: fall back to the kernel chain
+  const int bps = max_blocks(k, kFusedThreads, smem);
+  if (bps < 1) return invalid("fused FFN: does not fit one CTA per SM");
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(ctx->num_sms);
+  cfg.blockDim = dim3(kFusedThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = ctx->stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  ++ctx->launches;
+  CK(cudaLaunchKernelEx(&cfg, k, args));
+  return HIRE_OK;
+}
+
+template <typename T>
+int launch_ffn_fused_nt(hire_ctx ctx, const FusedFfnArgs& args, size_t smem, int nt, int ks) {
+  if (nt == 1) {
+    if (ks == 8) return launch_ffn_fused_t<T, 1, 8>(ctx, args, smem);
+    if (ks == 4) return launch_ffn_fused_t<T, 1, 4>(ctx, args, smem);
+    if (ks == 2) return launch_ffn_fused_t<T, 1, 2>(ctx, args, smem);
+    return launch_ffn_fused_t<T, 1, 1>(ctx, args, smem);
+  }
+  if (ks == 8) return launch_ffn_fused_t<T, 2, 8>(ctx, args, smem);
+  if (ks == 4) return launch_ffn_fused_t<T, 2, 4>(ctx, args, smem);
+  if (ks == 2) return launch_ffn_fused_t<T, 2, 2>(ctx, args, smem);
+  return launch_ffn_fused_t<T, 2, 1>(ctx, args, smem);
+}
+
+// One cooperative launch for the whole layer (ffn_fused.cuh) when the shape
+// allows it; returns 1 (not taken) otherwise.
+int try_ffn_fused(hire_ctx ctx, const hire_matrix_s* u, const hire_matrix_s* v, hire_scorer_s* a,
+                  const float* x, int64_t B, const hire_ffn_params* p, uint32_t* sel, float* out) {
+  if (!ctx->ffn_fused || p->group_size != 1 || p->x_mode != HIRE_X_INT8 || p->strict) return 1;
+  if (a->kind != HIRE_SCORER_Q4 || B < 1 || B > 16 || u->d % 64 != 0 || u->d > 8192) return 1;
+  if (u->rows > 16384 || p->k_prime > u->rows || p->k > p->k_prime) return 1;
+  if (u->dtype != v->dtype) return 1;
+  RET(ensure_mma_layout(ctx, a));
+  const int64_t m = u->rows, d = u->d, kp = p->k_prime, k = p->k;
+  const int nt = B <= 8 ? 1 : 2;
+  const int64_t nkb = d / 64, n_rb = ceil_div(m, 16);
+  int ks = 1;
+  while (ks < 8 && n_rb * ks < static_cast<int64_t>(ctx->num_sms) * kFusedWarps && nkb >= 2 * ks) ks *= 2;
+  const size_t xq_acc = static_cast<size_t>(nt) * 8 * (d + 16) + (ks > 1 ? static_cast<size_t>(kFusedWarps) * nt * 4 * 32 * 4 : 0);
+  const size_t pool = std::max({xq_acc, static_cast<size_t>(m) * 4, static_cast<size_t>(kp) * 8});
+  const size_t smem = static_cast<size_t>(B) * d * 4 + pool;
+  if (smem > 200 * 1024) return 1;
+  const int64_t nch = ceil_div(k, kFusedCh);
+  Arena ar;
+  FusedFfnArgs args{};
+  ar.take(&args.scores, static_cast<size_t>(B * m));
+  ar.take(&args.cand, static_cast<size_t>(B * kp));
+  ar.take(&args.act, static_cast<size_t>(B * kp));
+  ar.take(&args.selact, static_cast<size_t>(B * k));
+  ar.take(&args.partial, static_cast<size_t>(B * nch * d));
+  RET(ar.commit(ctx));
+  args.u_mma = a->mma;
+  args.scales = a->scales;
+  args.u = u->ptr;
+  args.v = v->ptr;
+  args.x = x;
+  args.B = static_cast<int>(B);
+  args.m = static_cast<int>(m);
+  args.d = static_cast<int>(d);
+  args.kp = static_cast<int>(kp);
+  args.k = static_cast<int>(k);
+  args.phi = p->phi;
+  args.sel = sel;
+  args.out = out;
+  args.counters = ctx->counters;
+  args.trace = ctx->trace ? reinterpret_cast<long long*>(ctx->counters + 192) : nullptr;
+  StageScope scope(ctx, kStageFused);
+  if (u->dtype == HIRE_BF16) return launch_ffn_fused_nt<__nv_bfloat16>(ctx, args, smem, nt, ks);
+  return launch_ffn_fused_nt<float>(ctx, args, smem, nt, ks);
+}
+}  // namespace
+
+extern "C" {
+
 int hire_ffn_run(hire_ctx ctx, hire_matrix u, hire_matrix v, hire_scorer a, const float* x, int64_t B,
                  const hire_ffn_params* p, uint32_t* sel, float* out) {
   if (!ctx || !x || !sel || !out) return invalid("null argument");
   RET(validate_ffn(u, v, a, B, p));
+  {
+    const int rc = try_ffn_fused(ctx, u, v, a, x, B, p, sel, out);
+    if (rc != 1) return rc;
+  }
   const int64_t g = p->group_size, m = u->rows, kg = p->k / g, kpg = p->k_prime / g;
   SelPlan sp;
   RET(plan_select(m / g, kpg, HIRE_SELECT_EXACT, 0, 0, &sp));

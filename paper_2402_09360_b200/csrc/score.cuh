@@ -350,7 +350,7 @@ __global__ void __launch_bounds__(128) lr_score_kernel(
   hire_dev::griddep_launch();
   extern __shared__ __align__(16) unsigned char smem[];
   float* s_t = reinterpret_cast<float*>(smem);
-  for (int i = threadIdx.x; i < R * B; i += blockDim.x) s_t[i] = t[i];
+  block_copy(s_t, t, R * B);
   __syncthreads();
   const int64_t j = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (j >= rows) return;
@@ -393,7 +393,7 @@ __global__ void __launch_bounds__(128) lr_score_generic(
   hire_dev::griddep_launch();
   extern __shared__ __align__(16) unsigned char smem[];
   float* s_t = reinterpret_cast<float*>(smem);
-  for (int i = threadIdx.x; i < r * B; i += blockDim.x) s_t[i] = t[i];
+  block_copy(s_t, t, r * B);
   __syncthreads();
   const int64_t j = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (j >= rows) return;

@@ -317,3 +317,31 @@ def test_da_group_sparse_emulated(H, O, s):
         assert np.array_equal(N(sel_s[b]).astype(np.uint32), ids)
         assert np.array_equal(N(out_s[b]).view(np.uint32), out.view(np.uint32))
         np.testing.assert_allclose(N(out_f[b]), out, rtol=1e-4, atol=1e-4 * np.abs(out).max())
+
+
+@pytest.mark.parametrize("B", [1, 8, 13])
+def test_ffn_fused_equals_unfused_and_oracle(H, O, B, monkeypatch):
+    """The single-launch fused HiRE-FFN (cfg2 shape) is bit-identical to the
+    unfused kernel chain, and matches the oracle (integer candidate step
+    exact; final selection up to near-ties; outputs within 1e-3)."""
+    m, d, k, kp = 8192, 2048, 410, 820
+    u, v = _data.ffn_family(m, d, 40 + B, r=64)
+    u, v = _data.bf16_round(u), _data.bf16_round(v)
+    f = H.GroupedFFN(H.ScoreMatrix(T(u, torch.bfloat16)), H.ScoreMatrix(T(v, torch.bfloat16)), 1, "relu")
+    a = H.ApproxScorer.quantize(f.u)
+    codes, scales = a.export_q4()
+    x = _data.queries(B, d, 41, scale=1.0)
+    out_f, sel_f = H.ffn_group_sparse(f, T(x), a, k, kp, x_mode=H.X_INT8)
+    monkeypatch.setenv("HIRE_FFN_FUSED", "0")
+    ctx = H.Context(0)
+    out_u, sel_u = H.ffn_group_sparse(f, T(x), a, k, kp, x_mode=H.X_INT8, ctx=ctx)
+    torch.cuda.synchronize()
+    assert torch.equal(sel_f, sel_u)
+    assert torch.equal(out_f.view(torch.int32), out_u.view(torch.int32))
+    for b in range(B):
+        s = O.q4_scores_int8(codes, scales, x[b], 1)
+        ids, want = O.ffn_group_sparse(u, v, x[b], s, k, kp, 1, 1)
+        acts = O.matvec(u, x[b], 1)
+        assert_sets_near_tie(N(sel_f[b]), ids, acts)
+        if set(N(sel_f[b]).tolist()) == set(ids.tolist()):
+            np.testing.assert_allclose(N(out_f[b]), want, rtol=1e-3, atol=1e-3 * np.abs(want).max())
