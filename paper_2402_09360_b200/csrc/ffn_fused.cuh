@@ -38,14 +38,18 @@ struct FusedFfnArgs {
   const float* x;          // [B][d]
   int B, m, d, kp, k, phi;
   float* scores;           // [B][m]
-  uint32_t* cand;          // [B][kp]
-  float* act;              // [B][kp]
+  uint64_t* piv;           // [B][2] bracket pivots (hi, lo)
+  uint64_t* thr;           // [B] exact k'-th proxy key
+  int* qcnt;               // [B][4] above / window / pairs counts (zeroed per launch)
+  uint64_t* win;           // [B][wcap] bracket windows
+  int wcap;
+  uint64_t* pairs;         // [B][kp] (exact activation, unit) keys of the candidates
   uint32_t* sel;           // [B][k]   (out, ascending)
   float* selact;           // [B][k]
   float* partial;          // [B][nch][d]
   float* out;              // [B][d]
-  int* counters;           // [8] zeroed between launches
-  long long* trace;        // optional [16] %globaltimer stamps (CTA 0, thread 0)
+  int* counters;           // hand-off counters, one 128-B line each
+  long long* trace;        // optional %globaltimer stamps (CTA 0, thread 0)
 };
 
 __device__ __forceinline__ long long globaltimer() {
@@ -54,7 +58,8 @@ __device__ __forceinline__ long long globaltimer() {
   return t;
 }
 
-enum { kCntGemv = 0, kCntCand = 32, kCntAct = 64, kCntSel = 96, kCntDown = 128, kCntExit = 160 };  // one 128-B line each
+enum { kCntGemv = 0, kCntPiv = 32, kCntWin = 64, kCntThr = 96, kCntPairs = 128, kCntSel = 160, kCntDown = 192,
+       kCntExit = 224 };  // one 128-B line each
 
 __device__ __forceinline__ int ld_acquire(const int* p) {
   int v;
@@ -70,7 +75,7 @@ __device__ __forceinline__ void cta_wait_geq(const int* p, int target) {
     unsigned ns = 32;
     while (ld_acquire(p) < target) {
       __nanosleep(ns);
-      ns = ns < 1024 ? ns * 2 : 1024;
+      ns = ns < 128 ? ns * 2 : 128;
     }
   }
   __syncthreads();
@@ -134,39 +139,50 @@ __global__ void __launch_bounds__(kFusedThreads, 1) ffn_fused_kernel(FusedFfnArg
   }
 
   // ---- P0: x -> smem (fp32) and int8 quantisation (prep_x_int8 rule) ----
-  // all warps work on every query: max|x| (block reduce), sx = max/127,
-  // xq = RHAZ(x/sx), sum(xq) (block reduce)
+  // all queries at once: warps are split evenly over the B queries (wpq
+  // warps each); two barriers in total, independent of B.
   block_copy(s_xf, a.x, B * d);
   __syncthreads();
-  for (int b = 0; b < B; ++b) {
+  FUSED_STAMP(13);
+  {
+    const int wpq = kFusedWarps / B > 0 ? kFusedWarps / B : 1;  // warps per query
+    const int qb = wid / wpq, qw = wid % wpq;                     // my query, my rank in it
+    const bool active = qb < B;
     float mx = 0.0f;
-    for (int i = tid; i < d; i += kFusedThreads) mx = fmaxf(mx, fabsf(s_xf[b * d + i]));
+    if (active)
+      for (int i = qw * 32 + lane; i < d; i += wpq * 32) mx = fmaxf(mx, fabsf(s_xf[qb * d + i]));
     mx = warp_max_f32(mx);
     if (lane == 0) s_red[wid] = mx;
     __syncthreads();
-    float v = 0.0f;
-#pragma unroll
-    for (int w = 0; w < kFusedWarps; ++w) v = fmaxf(v, s_red[w]);
-    const float sx = v > 0.0f ? __fdiv_rn(v, 127.0f) : 1.0f;
+    float sx = 1.0f;
+    if (active) {
+      float v = 0.0f;
+      for (int w = 0; w < wpq; ++w) v = fmaxf(v, s_red[qb * wpq + w]);
+      sx = v > 0.0f ? __fdiv_rn(v, 127.0f) : 1.0f;
+    }
     int local = 0;
-    for (int i = tid; i < d; i += kFusedThreads) {
-      const int q = rhaz_clamp(__fdiv_rn(s_xf[b * d + i], sx), 127);
-      local += q;
-      s_xq[b * xs + i] = static_cast<int8_t>(q);
-    }
+    if (active)
+      for (int i = qw * 32 + lane; i < d; i += wpq * 32) {
+        const int q = rhaz_clamp(__fdiv_rn(s_xf[qb * d + i], sx), 127);
+        local += q;
+        s_xq[qb * xs + i] = static_cast<int8_t>(q);
+      }
     local = warp_sum_i32(local);
-    __syncthreads();  // s_red reuse
     if (lane == 0) s_redi[wid] = local;
-    if (tid == 0) s_sx[b] = sx;
-    __syncthreads();
-    if (tid == 0) {
-      int sum = 0;
-      for (int w = 0; w < kFusedWarps; ++w) sum += s_redi[w];
-      s_sum[b] = sum;
+    if (active && qw == 0 && lane == 0) s_sx[qb] = sx;
+    // zero the padded queries of the MMA B operand (16-byte stores)
+    for (int i = tid; i < (NT * 8 - B) * (d / 16); i += kFusedThreads) {
+      const int n = B + i / (d / 16), c = i % (d / 16);
+      *reinterpret_cast<int4*>(s_xq + n * xs + c * 16) = make_int4(0, 0, 0, 0);
     }
+    __syncthreads();
+    if (tid < B) {
+      int sum = 0;
+      for (int w = 0; w < wpq; ++w) sum += s_redi[tid * wpq + w];
+      s_sum[tid] = sum;
+    }
+    __syncthreads();
   }
-  for (int i = tid; i < (NT * 8 - B) * d; i += kFusedThreads) s_xq[(B + i / d) * xs + i % d] = 0;
-  __syncthreads();
   FUSED_STAMP(1);
 
   // ---- P1: proxy scores on the tensor cores -------------------------------
@@ -245,54 +261,173 @@ __global__ void __launch_bounds__(kFusedThreads, 1) ffn_fused_kernel(FusedFfnArg
   FUSED_STAMP(2);
   cta_arrive(a.counters + kCntGemv, 1);
 
-  // ---- P2: candidate selection, one CTA per query ------------------------
+  // ---- P2a: bracket pivots for the k'-th proxy key (CTA b per query) ------
+  // A 128-key sample of scores[b] ranked by counting; the sample keys at
+  // ranks (k'-1)S/m -/+ 3.5 sigma bracket the k'-th key (select.cuh).
+  int f_row, w_row;  // this CTA's row slice (width rule)
+  {
+    const int base = m / G, extra = m % G;
+    f_row = blockIdx.x * base + (blockIdx.x < extra ? blockIdx.x : extra);
+    w_row = base + (blockIdx.x < extra ? 1 : 0);
+  }
   if (blockIdx.x < B) {
     const int b = blockIdx.x;
     cta_wait_geq(a.counters + kCntGemv, G);
     FUSED_STAMP(3);
-    float* s_val = reinterpret_cast<float*>(s_pool);
-    block_copy_cg(s_val, a.scores + static_cast<int64_t>(b) * m, m);
+    constexpr int S = 128;
+    if (tid < S) {
+      const int i = static_cast<int>((static_cast<int64_t>(tid) * m) / S);
+      sc.samp[tid] = make_key(__ldcg(a.scores + static_cast<int64_t>(b) * m + i), static_cast<uint32_t>(i));
+    }
+    if (tid == 0) {
+      sc.piv[0] = ~0ull;
+      sc.piv[1] = 0ull;
+    }
     __syncthreads();
-    FUSED_STAMP(13);
-    uint64_t prefix, mask;
-    auto key_at = [&](int i) { return make_key(s_val[i], static_cast<uint32_t>(i)); };
-    block_select_kth<kFusedThreads>(key_at, m, a.kp, &sc, &prefix, &mask);
-    FUSED_STAMP(14);
-    uint32_t* cb = a.cand + static_cast<int64_t>(b) * a.kp;
-    block_compact<kFusedThreads>(key_at, m, prefix, mask, &sc,
-                                 [&](int pos, int i, uint64_t) { cb[pos] = static_cast<uint32_t>(i); });
-    FUSED_STAMP(15);
-    cta_arrive(a.counters + kCntCand, 1);
+    const float p = static_cast<float>(a.kp) / static_cast<float>(m);
+    const float mu = static_cast<float>(a.kp - 1) * S / static_cast<float>(m);
+    const float delta = fmaxf(3.5f * sqrtf(S * p * (1.0f - p)), 3.0f);
+    const int r_hi = static_cast<int>(floorf(mu - delta));
+    const int r_lo = static_cast<int>(ceilf(mu + delta));
+    block_rank_256<kFusedThreads>(sc.samp, S, [&](int jj, int r) {
+      if (r == r_hi) sc.piv[0] = sc.samp[jj];
+      if (r == r_lo) sc.piv[1] = sc.samp[jj];
+    });
+    __syncthreads();
+    if (tid == 0) {
+      a.piv[2 * b] = sc.piv[0];
+      a.piv[2 * b + 1] = sc.piv[1];
+    }
+    cta_arrive(a.counters + kCntPiv, 1);
   }
 
-  // ---- P3: exact activations of the B*k' candidates ---------------------
+  // ---- P2b: every CTA counts / gathers the bracket over its own rows ------
+  // query-aligned warp groups (wpq warps per query) walk the slice; ballot
+  // counts go to per-query shared counters; one global atomic per query.
+  cta_wait_geq(a.counters + kCntPiv, B);
   FUSED_STAMP(4);
-  cta_wait_geq(a.counters + kCntCand, B);
-  FUSED_STAMP(5);
   {
+    __shared__ int s_above[16], s_win[16], s_wbase[16];
+    uint64_t* s_stage = reinterpret_cast<uint64_t*>(s_pool);  // [B][w_row]
+    if (tid < B) s_above[tid] = s_win[tid] = 0;
+    __syncthreads();
+    const int wpq = kFusedWarps / B > 0 ? kFusedWarps / B : 1;
+    const int qb = wid / wpq, qw = wid % wpq;
+    if (qb < B) {
+      const uint64_t hi = __ldcg(a.piv + 2 * qb), lo = __ldcg(a.piv + 2 * qb + 1);
+      for (int r0 = qw * 32; r0 < w_row; r0 += wpq * 32) {
+        const int r = r0 + lane;
+        uint64_t key = 0;
+        bool above = false, in = false;
+        if (r < w_row) {
+          key = make_key(__ldcg(a.scores + static_cast<int64_t>(qb) * m + f_row + r), static_cast<uint32_t>(f_row + r));
+          above = key > hi;
+          in = key > lo && key <= hi;
+        }
+        const unsigned ba = __ballot_sync(0xffffffffu, above), bi = __ballot_sync(0xffffffffu, in);
+        int base = 0;
+        if (lane == 0) {
+          if (ba) atomicAdd(&s_above[qb], __popc(ba));
+          if (bi) base = atomicAdd(&s_win[qb], __popc(bi));
+        }
+        base = __shfl_sync(0xffffffffu, base, 0);
+        if (in) s_stage[qb * w_row + base + __popc(bi & ((1u << lane) - 1u))] = key;
+      }
+    }
+    __syncthreads();
+    if (tid < B) {
+      if (s_above[tid]) atomicAdd(a.qcnt + 4 * tid, s_above[tid]);
+      s_wbase[tid] = s_win[tid] ? atomicAdd(a.qcnt + 4 * tid + 1, s_win[tid]) : 0;
+    }
+    __syncthreads();
+    for (int t2 = tid; t2 < B * w_row; t2 += kFusedThreads) {
+      const int b = t2 / w_row, j2 = t2 % w_row;
+      if (j2 < s_win[b] && s_wbase[b] + j2 < a.wcap)
+        a.win[static_cast<int64_t>(b) * a.wcap + s_wbase[b] + j2] = s_stage[t2];
+    }
+  }
+  cta_arrive(a.counters + kCntWin, 1);
+
+  // ---- P2c: exact k'-th key per query from its window (CTA b) -------------
+  if (blockIdx.x < B) {
+    const int b = blockIdx.x;
+    cta_wait_geq(a.counters + kCntWin, G);
+    FUSED_STAMP(5);
+    const int above = __ldcg(a.qcnt + 4 * b), nw = __ldcg(a.qcnt + 4 * b + 1);
+    const int need = a.kp - above;
+    uint64_t T;
+    if (need >= 1 && need <= nw && nw <= a.wcap) {
+      uint64_t* s_w = reinterpret_cast<uint64_t*>(s_pool);
+      block_copy_cg(s_w, a.win + static_cast<int64_t>(b) * a.wcap, nw);
+      __syncthreads();
+      T = block_kth_key<kFusedThreads>([&](int i) { return s_w[i]; }, nw, need, &sc);
+    } else {  // bracket missed: exact select over all m scores
+      float* s_val = reinterpret_cast<float*>(s_pool);
+      block_copy_cg(s_val, a.scores + static_cast<int64_t>(b) * m, m);
+      __syncthreads();
+      T = block_kth_key<kFusedThreads>([&](int i) { return make_key(s_val[i], static_cast<uint32_t>(i)); },
+                                       m, a.kp, &sc);
+    }
+    if (tid == 0) a.thr[b] = T;
+    cta_arrive(a.counters + kCntThr, 1);
+  }
+
+  // ---- P3: every CTA recomputes the candidates in its own rows ------------
+  cta_wait_geq(a.counters + kCntThr, B);
+  FUSED_STAMP(6);
+  {
+    // stage (b, row) candidates of this slice, query-major
+    int* s_cand = reinterpret_cast<int*>(s_pool);                    // [B*w_row] rows
+    float* s_act = reinterpret_cast<float*>(s_pool) + B * w_row;      // [B*w_row]
+    __shared__ int s_off[17];
+    __shared__ int s_nb[16];
+    __shared__ int s_pbase[16];
+    if (tid < B) s_nb[tid] = 0;
+    __syncthreads();
+    {
+      const int wpq = kFusedWarps / B > 0 ? kFusedWarps / B : 1;
+      const int qb = wid / wpq, qw = wid % wpq;
+      if (qb < B) {
+        const uint64_t T = __ldcg(a.thr + qb);
+        for (int r0 = qw * 32; r0 < w_row; r0 += wpq * 32) {
+          const int r = r0 + lane;
+          bool c = false;
+          if (r < w_row)
+            c = make_key(__ldcg(a.scores + static_cast<int64_t>(qb) * m + f_row + r), static_cast<uint32_t>(f_row + r)) >= T;
+          const unsigned bc = __ballot_sync(0xffffffffu, c);
+          int base = 0;
+          if (lane == 0 && bc) base = atomicAdd(&s_nb[qb], __popc(bc));
+          base = __shfl_sync(0xffffffffu, base, 0);
+          if (c) s_cand[qb * w_row + base + __popc(bc & ((1u << lane) - 1u))] = f_row + r;
+        }
+      }
+    }
+    __syncthreads();
+    if (tid == 0) {
+      s_off[0] = 0;
+      for (int b = 0; b < B; ++b) s_off[b + 1] = s_off[b] + s_nb[b];
+    }
+    __syncthreads();
+    const int ntask = s_off[B];
     const T* U_ = static_cast<const T*>(a.u);
     const int64_t pitch_vec = d / E;
-    const int tasks = B * a.kp;
-    const int stride = G * kFusedWarps;
     // two rows in flight per warp; per-row arithmetic identical to recompute_fast
-    // CTA-minor task order: consecutive tasks land on different SMs, so a
-    // small B*k' spreads over all SMs (x is re-read from smem per row)
-    const int tbase = wid * G + blockIdx.x;
-    for (int t0 = tbase; t0 < tasks; t0 += 2 * stride) {
-      int bt[2], it[2];
+    for (int t0 = wid; t0 < ntask; t0 += 2 * kFusedWarps) {
+      int bt[2], rw[2], slot[2];
       bool ok[2];
       const uint4* rp[2];
 #pragma unroll
       for (int r = 0; r < 2; ++r) {
-        const int task = t0 + r * stride;
-        ok[r] = task < tasks;
-        bt[r] = ok[r] ? task / a.kp : 0;
-        it[r] = ok[r] ? task % a.kp : 0;
-        const int64_t row = ok[r] ? __ldcg(a.cand + static_cast<int64_t>(bt[r]) * a.kp + it[r]) : 0;
-        rp[r] = reinterpret_cast<const uint4*>(U_) + row * pitch_vec;
+        const int task = t0 + r * kFusedWarps;
+        ok[r] = task < ntask;
+        int b = 0;
+        if (ok[r])
+          while (task >= s_off[b + 1]) ++b;
+        bt[r] = b;
+        slot[r] = ok[r] ? b * w_row + (task - s_off[b]) : 0;
+        rw[r] = ok[r] ? s_cand[slot[r]] : 0;
+        rp[r] = reinterpret_cast<const uint4*>(U_) + static_cast<int64_t>(rw[r]) * pitch_vec;
       }
-      if (t0 == tbase) FUSED_STAMP(16);
-      long long c_a = clock64();
       float accf[2] = {0.0f, 0.0f};
       for (int c0 = 0; c0 < pitch_vec; c0 += 256) {  // 8 vectors per lane per pass
         uint4 vv[2][8];
@@ -303,11 +438,6 @@ __global__ void __launch_bounds__(kFusedThreads, 1) ffn_fused_kernel(FusedFfnArg
             const int vi = c0 + lane + 32 * c;
             vv[r][c] = (ok[r] && vi < pitch_vec) ? ldg_stream(rp[r] + vi) : make_uint4(0, 0, 0, 0);
           }
-        if (a.trace && blockIdx.x == 0 && threadIdx.x == 0 && c0 == 0) {
-          a.trace[22] = clock64() - c_a;
-          a.trace[23] = static_cast<long long>(vv[0][0].x ^ vv[0][7].w);  // forces the loads
-          a.trace[24] = clock64() - c_a;
-        }
 #pragma unroll
         for (int r = 0; r < 2; ++r)
 #pragma unroll
@@ -322,38 +452,65 @@ __global__ void __launch_bounds__(kFusedThreads, 1) ffn_fused_kernel(FusedFfnArg
             }
           }
       }
-      if (t0 == tbase) FUSED_STAMP(17);
-      if (a.trace && blockIdx.x == 0 && threadIdx.x == 0 && t0 == tbase) a.trace[25] = clock64() - c_a;
 #pragma unroll
       for (int r = 0; r < 2; ++r) {
         const float s2 = warp_sum_f32(accf[r]);
-        if (lane == 0 && ok[r]) a.act[static_cast<int64_t>(bt[r]) * a.kp + it[r]] = apply_phi(a.phi, s2);
+        if (lane == 0 && ok[r]) s_act[slot[r]] = apply_phi(a.phi, s2);
       }
     }
+    __syncthreads();
+    if (tid < B) s_pbase[tid] = s_nb[tid] ? atomicAdd(a.qcnt + 4 * tid + 2, s_nb[tid]) : 0;
+    __syncthreads();
+    for (int task = tid; task < ntask; task += kFusedThreads) {
+      int b = 0;
+      while (task >= s_off[b + 1]) ++b;
+      const int j2 = task - s_off[b];
+      const int sl = b * w_row + j2;
+      a.pairs[static_cast<int64_t>(b) * a.kp + s_pbase[b] + j2] = make_key(s_act[sl], static_cast<uint32_t>(s_cand[sl]));
+    }
   }
-  FUSED_STAMP(18);
-  cta_arrive(a.counters + kCntAct, 1);
-  FUSED_STAMP(19);
+  cta_arrive(a.counters + kCntPairs, 1);
 
-  // ---- P4: final top-k per query, ascending unit order --------------------
+  // ---- P4: top-k by exact activation, emitted in ascending unit order ----
   if (blockIdx.x < B) {
     const int b = blockIdx.x;
-    FUSED_STAMP(6);
-    cta_wait_geq(a.counters + kCntAct, G);
+    cta_wait_geq(a.counters + kCntPairs, G);
     FUSED_STAMP(7);
     uint64_t* s_keys = reinterpret_cast<uint64_t*>(s_pool);
-    block_copy_tf(s_keys, a.kp, [&](int i) {
-      return make_key(__ldcg(a.act + static_cast<int64_t>(b) * a.kp + i),
-                      __ldcg(a.cand + static_cast<int64_t>(b) * a.kp + i));
-    });
+    unsigned* s_bits = reinterpret_cast<unsigned*>(s_keys + a.kp);
+    const int nwords = (m + 31) / 32;
+    float* s_au = reinterpret_cast<float*>(s_bits + nwords);
+    block_copy_cg(s_keys, a.pairs + static_cast<int64_t>(b) * a.kp, a.kp);
+    for (int w = tid; w < nwords; w += kFusedThreads) s_bits[w] = 0u;
     __syncthreads();
-    uint64_t prefix, mask;
-    auto key_at = [&](int i) { return s_keys[i]; };
-    block_select_kth<kFusedThreads>(key_at, a.kp, a.k, &sc, &prefix, &mask);
-    block_compact<kFusedThreads>(key_at, a.kp, prefix, mask, &sc, [&](int pos, int, uint64_t key) {
-      a.sel[static_cast<int64_t>(b) * a.k + pos] = key_index(key);
-      a.selact[static_cast<int64_t>(b) * a.k + pos] = key_value(key);
-    });
+    const uint64_t T2 = block_kth_key<kFusedThreads>([&](int i) { return s_keys[i]; }, a.kp, a.k, &sc);
+    for (int i = tid; i < a.kp; i += kFusedThreads) {
+      const uint64_t key = s_keys[i];
+      if (key >= T2) {
+        const uint32_t u = key_index(key);
+        atomicOr(&s_bits[u >> 5], 1u << (u & 31));
+        s_au[u] = key_value(key);
+      }
+    }
+    __syncthreads();
+    // ordered emit: thread t owns words [t*per, (t+1)*per)
+    const int per = (nwords + kFusedThreads - 1) / kFusedThreads;
+    const int w0 = min(nwords, tid * per), w1 = min(nwords, w0 + per);
+    int cnt = 0;
+    for (int w = w0; w < w1; ++w) cnt += __popc(s_bits[w]);
+    int total;
+    int pos = block_exclusive_scan<kFusedThreads>(cnt, sc.scan, &total);
+    for (int w = w0; w < w1; ++w) {
+      unsigned bits = s_bits[w];
+      while (bits) {
+        const int bit = __ffs(bits) - 1;
+        bits &= bits - 1;
+        const int u = w * 32 + bit;
+        a.sel[static_cast<int64_t>(b) * a.k + pos] = static_cast<uint32_t>(u);
+        a.selact[static_cast<int64_t>(b) * a.k + pos] = s_au[u];
+        ++pos;
+      }
+    }
     cta_arrive(a.counters + kCntSel, 1);
   }
 
@@ -423,6 +580,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1) ffn_fused_kernel(FusedFfnArg
     const int prev = atomicAdd(a.counters + kCntExit, 1);
     if (prev == G - 1) {
       for (int i = 0; i <= kCntExit; i += 32) a.counters[i] = 0;
+      for (int i = 0; i < 4 * B; ++i) a.qcnt[i] = 0;
       __threadfence();
     }
   }

@@ -767,8 +767,8 @@ int hire_ctx_create(int device, void* stream, int own_stream, hire_ctx* out) {
   if (const char* e = getenv("HIRE_PROXY_KERNEL")) c->force_dp4a = std::strcmp(e, "dp4a") == 0;
   if (const char* e = getenv("HIRE_FFN_FUSED")) c->ffn_fused = std::strcmp(e, "0") != 0;
   if (const char* e = getenv("HIRE_FUSED_TRACE")) c->trace = std::strcmp(e, "1") == 0;
-  CK(cudaMalloc(&c->counters, 256 * sizeof(int)));
-  CK(cudaMemset(c->counters, 0, 256 * sizeof(int)));
+  CK(cudaMalloc(&c->counters, 512 * sizeof(int)));
+  CK(cudaMemset(c->counters, 0, 512 * sizeof(int)));
   if (const char* e = getenv("HIRE_NO_PDL")) c->pdl = std::strcmp(e, "1") != 0;
   *out = c;
   return HIRE_OK;
@@ -805,7 +805,7 @@ int64_t hire_ctx_launch_count(hire_ctx c) { return c ? c->launches : 0; }
 int hire_ctx_read_trace(hire_ctx c, long long* out, int n) {
   if (!c || !out || n > 28) return invalid("bad trace request");
   CK(cudaStreamSynchronize(c->stream));
-  CK(cudaMemcpy(out, c->counters + 192, static_cast<size_t>(n) * 8, cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(out, c->counters + 320, static_cast<size_t>(n) * 8, cudaMemcpyDeviceToHost));
   return HIRE_OK;
 }
 
@@ -1374,15 +1374,22 @@ int try_ffn_fused(hire_ctx ctx, const hire_matrix_s* u, const hire_matrix_s* v, 
   int ks = 1;
   while (ks < 8 && n_rb * ks < static_cast<int64_t>(ctx->num_sms) * kFusedWarps && nkb >= 2 * ks) ks *= 2;
   const size_t xq_acc = static_cast<size_t>(nt) * 8 * (d + 16) + (ks > 1 ? static_cast<size_t>(kFusedWarps) * nt * 4 * 32 * 4 : 0);
-  const size_t pool = std::max({xq_acc, static_cast<size_t>(m) * 4, static_cast<size_t>(kp) * 8});
+  const int wcap = 4096;
+  const int64_t wrow = ceil_div(m, ctx->num_sms);
+  const size_t pool = std::max({xq_acc, static_cast<size_t>(m) * 4, static_cast<size_t>(wcap) * 8,
+                                static_cast<size_t>(wrow) * 8, static_cast<size_t>(B * wrow) * 8,
+                                static_cast<size_t>(kp) * 8 + static_cast<size_t>((m + 31) / 32) * 4 +
+                                    static_cast<size_t>(m) * 4});
   const size_t smem = static_cast<size_t>(B) * d * 4 + pool;
   if (smem > 200 * 1024) return 1;
   const int64_t nch = ceil_div(k, kFusedCh);
   Arena ar;
   FusedFfnArgs args{};
   ar.take(&args.scores, static_cast<size_t>(B * m));
-  ar.take(&args.cand, static_cast<size_t>(B * kp));
-  ar.take(&args.act, static_cast<size_t>(B * kp));
+  ar.take(&args.piv, static_cast<size_t>(2 * B));
+  ar.take(&args.thr, static_cast<size_t>(B));
+  ar.take(&args.win, static_cast<size_t>(B) * wcap);
+  ar.take(&args.pairs, static_cast<size_t>(B * kp));
   ar.take(&args.selact, static_cast<size_t>(B * k));
   ar.take(&args.partial, static_cast<size_t>(B * nch * d));
   RET(ar.commit(ctx));
@@ -1397,10 +1404,12 @@ int try_ffn_fused(hire_ctx ctx, const hire_matrix_s* u, const hire_matrix_s* v, 
   args.kp = static_cast<int>(kp);
   args.k = static_cast<int>(k);
   args.phi = p->phi;
+  args.wcap = wcap;
+  args.qcnt = ctx->counters + 256;  // zeroed at creation, reset by the kernel's last CTA
   args.sel = sel;
   args.out = out;
   args.counters = ctx->counters;
-  args.trace = ctx->trace ? reinterpret_cast<long long*>(ctx->counters + 192) : nullptr;
+  args.trace = ctx->trace ? reinterpret_cast<long long*>(ctx->counters + 320) : nullptr;
   StageScope scope(ctx, kStageFused);
   if (u->dtype == HIRE_BF16) return launch_ffn_fused_nt<__nv_bfloat16>(ctx, args, smem, nt, ks);
   return launch_ffn_fused_nt<float>(ctx, args, smem, nt, ks);

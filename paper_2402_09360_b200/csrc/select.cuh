@@ -397,6 +397,32 @@ __device__ void block_select_kth(KeyAt key_at, int n, int K, SelectScratch* sc,
   SEL_STAMP(7);
 }
 
+// The exact K-th largest key (block_select_kth may return a (prefix, mask)
+// bin rule from its radix fallback; this turns any result into one key).
+template <int NT, class KeyAt>
+__device__ uint64_t block_kth_key(KeyAt key_at, int n, int K, SelectScratch* sc) {
+  uint64_t prefix, mask;
+  block_select_kth<NT>(key_at, n, K, sc, &prefix, &mask);
+  if (mask == ~0ull) return prefix;
+  uint64_t t = ~0ull;
+  for (int i = threadIdx.x; i < n; i += NT) {
+    const uint64_t k = key_at(i);
+    if (key_selected(k, prefix, mask) && k < t) t = k;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const uint64_t u = __shfl_xor_sync(0xffffffffu, t, o);
+    t = u < t ? u : t;
+  }
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if (lane == 0) sc->red[0][wid] = t;
+  __syncthreads();
+  uint64_t tt = ~0ull;
+  for (int w = 0; w < NT / 32; ++w) tt = sc->red[0][w] < tt ? sc->red[0][w] : tt;
+  __syncthreads();
+  return tt;
+}
+
 // Order-preserving compaction of the selected keys. Warp w owns the
 // contiguous range [w*seg, (w+1)*seg), walked 32 keys at a time
 // (lane-contiguous, bank-conflict free). The count pass stores its ballots
