@@ -283,6 +283,171 @@ class SoftmaxWorkload:
                 "select": "1024 buckets x top-1 (literal)" if self.select == "bucketed" else "exact top-k'"}
 
 
+class LowRankSoftmaxWorkload:
+    """cfg1: HiRE-softmax, fp32, d=1024, V=32768, W = A B / 8 + 0.1 N(0,1),
+    rank-64 truncated-SVD proxy, exact top-k'=256, k=32, batch 1. 16 copies
+    of (W, Z1, Z2) are cycled so the 9.7 MB per-step working set streams from
+    HBM (one copy would sit in L2)."""
+    name = "cfg1"
+
+    def __init__(self, H, batch, copies=16, seed=0):
+        self.H = H
+        self.V, self.d, self.r, self.kp, self.k, self.B = 32768, 1024, 64, 256, 32, batch
+        gen = torch.Generator(device="cuda").manual_seed(seed)
+        A = torch.randn(self.V, 64, device="cuda", generator=gen)
+        Bm = torch.randn(64, self.d, device="cuda", generator=gen)
+        W = (A @ Bm) / 8.0 + 0.1 * torch.randn(self.V, self.d, device="cuda", generator=gen)
+        # Z (d x V) = W^T = U S Vt  ->  Z1 = (U_r S_r)^T [r, d], Z2 = Vt_r^T [V, r]
+        U, S, Vt = torch.linalg.svd(W.T.double(), full_matrices=False)
+        z1 = (U[:, :self.r] * S[:self.r]).T.float().contiguous()
+        z2 = Vt[:self.r].T.float().contiguous()
+        self.copies = []
+        for _ in range(copies):
+            Wc = W.clone()
+            self.copies.append((H.ScoreMatrix(Wc), H.ApproxScorer.low_rank(z1.clone(), z2.clone())))
+        self.cfg = H.HireConfig(k=self.k, k_prime=self.kp)
+        self.gen = gen
+        self.W, self.A = self.copies[0]
+        self._z = (z1, z2)
+        torch.cuda.synchronize()
+
+    lowrank = True
+    proxy_kernel = "lr_score_kernel (K2 low-rank proxy, fp32 FMA)"
+    dtype = "fp32 (W, factors, x; fp32 accumulation)"
+
+    def host_factors(self):
+        return self._z[0].cpu().numpy(), self._z[1].cpu().numpy()
+
+    def inputs(self, n):
+        return torch.randn(n, self.B, self.d, device="cuda", generator=self.gen) / self.d ** 0.5
+
+    def step(self, i, x):
+        z, a = self.copies[i % len(self.copies)]
+        return self.H.hire_topk(x, z, a, self.cfg, want_candidates=False)
+
+    def host_step(self, i, x_host, idx_host, val_host, ctx):
+        H = self.H
+        z, a = self.copies[i % len(self.copies)]
+        p = self.cfg.params()
+        n1, n2, cl = C.c_int64(), C.c_int64(), C.c_int()
+        H._lib.check(H.lib().hire_topk_host(ctx.h, z.h, a.h, x_host.ctypes.data_as(C.c_void_p), self.B,
+                                            C.byref(p), None, idx_host.ctypes.data_as(C.c_void_p),
+                                            val_host.ctypes.data_as(C.c_void_p), None, C.byref(n1),
+                                            C.byref(n2), C.byref(cl)))
+
+    def io_bytes(self):
+        return self.B * self.d * 4, self.B * self.k * 8
+
+    def proxy_bytes(self):
+        return (self.V + self.d) * self.r * 4
+
+    def step_bytes(self, x):
+        z, a = self.copies[0]
+        r = self.H.hire_topk(x, z, a, self.cfg)
+        nu = int(torch.unique(r.cand.long()).numel())
+        return self.proxy_bytes() + nu * self.d * 4, nu, 0
+
+    def recall(self, x):
+        H = self.H
+        z, a = self.copies[0]
+        r = H.hire_topk(x, z, a, self.cfg)
+        ex, _, _ = H.exact_topk(z, x, self.k)
+        return float(np.mean([H.recall(r.cand[b].cpu().numpy(), ex[b].cpu().numpy())[0]
+                              for b in range(x.shape[0])]))
+
+    def config(self):
+        return {"workload": "cfg1 HiRE-softmax fp32, rank-64 SVD proxy (BASELINE.json configs[0])",
+                "V": self.V, "d": self.d, "rank": self.r, "k_prime": self.kp, "k": self.k,
+                "global_batch": self.B, "weights": "fp32 W = A B / 8 + 0.1 N(0,1), truncated SVD factors",
+                "l2": f"{len(self.copies)} copies cycled", "select": "exact top-k'"}
+
+
+class DaSoftmaxWorkload:
+    """cfg4: DA-TOP-k sharded softmax, bf16 W [256000, 4096] (low-rank +
+    noise), rank-64 proxy (generator factors), B=16, k'=2048, k=128. Each
+    rank holds its contiguous vocab shard; merge = one ncclAllGather of rank
+    keys (hire_da_topk_run). global merge (BASELINE.json cfg4 wording)."""
+    name = "cfg4"
+
+    def __init__(self, H, batch, world=1, rank=0, seed=0):
+        import paper_2402_09360_b200.parallel as P
+        self.H, self.P = H, P
+        self.V, self.d, self.r, self.kp, self.k, self.B = 256000, 4096, 64, 2048, 128, batch
+        self.world, self.rank = world, rank
+        first, width = P.shard_range(self.V, world, rank)
+        self.first, self.width = first, width
+        gen = torch.Generator(device="cuda").manual_seed(seed)
+        Bm = torch.randn(self.r, self.d, device="cuda", generator=gen)
+        # every rank draws the full A so shards are consistent; keeps its rows
+        A = torch.randn(self.V, self.r, device="cuda", generator=gen)[first:first + width].contiguous()
+        W = torch.empty(width, self.d, device="cuda", dtype=torch.bfloat16)
+        g2 = torch.Generator(device="cuda").manual_seed(seed * 7919 + rank + 1)
+        for s0 in range(0, width, 16384):
+            e = min(width, s0 + 16384)
+            W[s0:e] = ((A[s0:e] @ Bm) / self.r ** 0.5 + 0.1 * torch.randn(e - s0, self.d, device="cuda",
+                                                                        generator=g2)).to(torch.bfloat16)
+        self.W = H.ScoreMatrix(W)
+        z1 = (Bm / self.r ** 0.5).to(torch.bfloat16).contiguous()   # [r, d]
+        z2 = A.to(torch.bfloat16).contiguous()                        # [width, r]
+        self.A = H.ApproxScorer.low_rank(z1, z2)
+        self.cfg = H.HireConfig(k=self.k, k_prime=self.kp)
+        self.comm = P.Communicator(world, rank) if world > 1 else None
+        self.gen = torch.Generator(device="cuda").manual_seed(seed + 99)
+        self._z = (z1, z2)
+        torch.cuda.synchronize()
+
+    lowrank = True
+    proxy_kernel = "lr_score_kernel (K2 low-rank proxy, bf16 factors, fp32 acc)"
+    dtype = "bf16 W and factors, fp32 x and accumulation"
+
+    def host_factors(self):
+        return self._z[0].float().cpu().numpy(), self._z[1].float().cpu().numpy()
+
+    def inputs(self, n):
+        return torch.randn(n, self.B, self.d, device="cuda", generator=self.gen) / self.d ** 0.5
+
+    def step(self, i, x):
+        return self.P.da_topk(self.W, self.A, self.V, x, self.cfg, self.comm,
+                              merge=self.H.MERGE_GLOBAL)
+
+    def host_step(self, i, x_host, idx_host, val_host, ctx):
+        xd = torch.from_numpy(x_host).cuda(non_blocking=False)
+        ti, tv, _ = self.P.da_topk(self.W, self.A, self.V, xd, self.cfg, self.comm,
+                                   merge=self.H.MERGE_GLOBAL, ctx=None)
+        idx_host[:] = ti.cpu().numpy()
+        val_host[:] = tv.cpu().numpy()
+
+    def io_bytes(self):
+        return self.B * self.d * 4, self.B * self.k * 8
+
+    def proxy_bytes(self):
+        return (self.width + self.d) * self.r * 2
+
+    def step_bytes(self, x):
+        # local candidates of this shard: union over the batch of k'/D rows
+        s = self.A.scores(x)
+        kpl = self.P.quota(self.kp, self.world, self.rank)
+        cand, _, _ = self.H.topk_select(s, kpl)
+        nu = int(torch.unique(cand.long()).numel())
+        return self.proxy_bytes() + nu * self.d * 2 + self.world * self.B * self.kp // self.world * 8, nu, 0
+
+    def recall(self, x):
+        if self.world > 1:
+            return None
+        H = self.H
+        ti, _, _ = self.step(0, x)
+        ex, _, _ = H.exact_topk(self.W, x, self.k)
+        return float(np.mean([np.isin(ex[b].cpu().numpy(), ti[b].cpu().numpy()).mean()
+                              for b in range(x.shape[0])]))
+
+    def config(self):
+        return {"workload": "cfg4 DA-TOP-k sharded softmax (BASELINE.json configs[3])", "V": self.V,
+                "d": self.d, "rank": self.r, "k_prime": self.kp, "k": self.k, "global_batch": self.B,
+                "shard_rows": self.width, "merge": "global (all k' exact pairs all-gathered)",
+                "weights": "bf16 W = rank-64 (unit variance) + 0.1 N(0,1); proxy = generator factors",
+                "l2": "W shard + proxy > 126 MB L2", "select": "exact top-k'/D per shard"}
+
+
 # ------------------------------------------------------------- reference ---
 def make_ref_runner(wl, threads):
     """The reference's own CPU implementation of the workload's path:
@@ -317,11 +482,17 @@ def make_ref_runner(wl, threads):
             threads = 1
         return run, threads, kind, desc
     W = wl.W.tensor.float().cpu().numpy()
-    codes, scales = wl.A.export_q4()
-    desc = "hire::hire_topk (reference int4 scorer, fp32 x, exact top-k')"
+    lowrank = getattr(wl, "lowrank", False)
+    if lowrank:
+        z1, z2 = wl.host_factors()
+        desc = "hire::hire_topk (reference low-rank scorer, exact top-k')"
+    else:
+        codes, scales = wl.A.export_q4()
+        desc = "hire::hire_topk (reference int4 scorer, fp32 x, exact top-k')"
     if kind == "reference":
         rm = O.RefMatrix(W)
-        ra = O.RefScorer("quantized", codes=codes, scales=scales)
+        ra = (O.RefScorer("lowrank", z1=z1, z2=z2) if lowrank else
+              O.RefScorer("quantized", codes=codes, scales=scales))
 
         def run(xb):
             idx = np.empty((xb.shape[0], wl.k), dtype=np.uint32)
@@ -333,7 +504,8 @@ def make_ref_runner(wl, threads):
     else:
         def run(xb):
             for b in range(xb.shape[0]):
-                s = O.q4_scores_fpx(codes, scales, xb[b], 0)
+                s = (O.lowrank_scores(z1, z2, xb[b], 0) if lowrank else
+                     O.q4_scores_fpx(codes, scales, xb[b], 0))
                 O.hire_topk(W, xb[b], s, wl.k, wl.kp, 0)
         threads = 1
     return run, threads, kind, desc
@@ -363,9 +535,13 @@ def cpu_baseline(wl, seconds):
 
 
 # ------------------------------------------------------------------- main ---
-def make_workload(H, args):
+def make_workload(H, args, world=1, rank=0):
     if args.workload == "cfg3":
         return SoftmaxWorkload(H, args.batch or 1, select=args.select)
+    if args.workload == "cfg1":
+        return LowRankSoftmaxWorkload(H, args.batch or 1)
+    if args.workload == "cfg4":
+        return DaSoftmaxWorkload(H, args.batch or 16, world, rank)
     return FfnWorkload(H, args.batch or 8)
 
 
@@ -377,7 +553,7 @@ def run_ours(args):
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     import paper_2402_09360_b200 as H
     H.lib()
-    wl = make_workload(H, args)
+    wl = make_workload(H, args, world, rank)
     K, W = args.steps, args.warmup
     xs = wl.inputs(K + W)
     # Each timed step replays from one CUDA graph holding the K layer calls
@@ -458,7 +634,7 @@ def run_ours(args):
         pb = step_b
         k_us = prof["ffn_fused"][0] * 1e3 / max(prof["ffn_fused"][1], 1)
     else:
-        kname = "q4_score_mma (K1 proxy GEMV, tensor-core IMMA)"
+        kname = getattr(wl, "proxy_kernel", "q4_score_mma (K1 proxy GEMV, tensor-core IMMA)")
         pb = wl.proxy_bytes()
         k_us = prof["proxy"][0] * 1e3 / max(prof["proxy"][1], 1)
     achieved = pb / (k_us * 1e-6) / 1e9
@@ -487,10 +663,10 @@ def run_ours(args):
         "metric": "HiRE decode tokens/s (µs/token, HBM roofline fraction, recall@k)",
         "value": round(value, 2), "unit": "tokens/s", "n_gpus": world, "steps": K, "warmup": W,
         "ms_per_step": round(ms_step, 5), "us_per_token": round(ms_step * 1e3 / wl.B, 4),
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int4xint8->int32 proxy, bf16 rows, fp32 acc",
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": getattr(wl, "dtype", "int4xint8->int32 proxy, bf16 rows, fp32 acc"),
         "data": "synthetic (seeded random-init weights of the BASELINE family; random queries)",
         "config": {**wl.config(), "parallelism": f"replicas x{world}" if world > 1 else "single GPU"},
-        "recall_at_k": round(rec, 5),
+        "recall_at_k": round(rec, 5) if rec is not None else None,
         "roofline": {"bound": "hbm", "kernel": kname,
                      "achieved": round(achieved, 1), "peak": peaks["hbm_gbs"], "unit": "GB/s",
                      "frac": round(achieved / peaks["hbm_gbs"], 4), "traffic": None,
@@ -557,7 +733,7 @@ def main():
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="cfg2", choices=["cfg2", "cfg3"])
+    ap.add_argument("--workload", default="cfg2", choices=["cfg1", "cfg2", "cfg3", "cfg4"])
     ap.add_argument("--batch", type=int, default=0)
     ap.add_argument("--select", default="exact", choices=["exact", "bucketed"])
     ap.add_argument("--cpu-seconds", type=float, default=8.0)

@@ -106,6 +106,10 @@ HIRE_API int hire_ctx_set_profiling(hire_ctx ctx, int on);
 /* Phase timestamps (%globaltimer, ns) of the last fused-kernel launch, when the
  * context was created with HIRE_FUSED_TRACE=1 in the environment. */
 HIRE_API int hire_ctx_read_trace(hire_ctx ctx, long long* out, int n);
+/* Debug: per-kernel %globaltimer window (min CTA start, max CTA end) for the
+ * kernels launched while enabled. op 1 enable+reset, 2 read n words
+ * (pairs per kernel id, see common.cuh KtId), 0 disable. */
+HIRE_API int hire_debug_ktrace(hire_ctx ctx, int op, unsigned long long* out, int n);
 HIRE_API int hire_ctx_profile_read(hire_ctx ctx, double* ms, int64_t* counts, int n_stages);
 
 /* ---- device buffers (for wrappers that start from host data) ------------ */

@@ -24,7 +24,7 @@ STAGES = ["proxy", "select", "recompute", "final", "down", "comm", "prep_x", "ff
 EXPORTS = [
     "hire_last_error", "hire_abi_version",
     "hire_ctx_create", "hire_ctx_destroy", "hire_ctx_stream", "hire_ctx_synchronize",
-    "hire_ctx_launch_count", "hire_ctx_set_profiling", "hire_ctx_profile_read", "hire_ctx_read_trace",
+    "hire_ctx_launch_count", "hire_ctx_set_profiling", "hire_ctx_profile_read", "hire_ctx_read_trace", "hire_debug_ktrace",
     "hire_device_alloc", "hire_device_free", "hire_copy",
     "hire_matrix_create", "hire_matrix_view", "hire_matrix_slice", "hire_matrix_destroy",
     "hire_matrix_info",
@@ -78,6 +78,7 @@ def _sig(L):
         "hire_ctx_synchronize": [_vp],
         "hire_ctx_set_profiling": [_vp, _i32],
         "hire_ctx_read_trace": [_vp, _vp, _i32],
+        "hire_debug_ktrace": [_vp, _i32, _vp, _i32],
         "hire_ctx_profile_read": [_vp, _vp, _vp, _i32],
         "hire_device_alloc": [_i64, _p(_vp)],
         "hire_device_free": [_vp],

@@ -58,6 +58,38 @@ class Context:
     def set_profiling(self, on: bool):
         check(lib().hire_ctx_set_profiling(self.h, int(on)))
 
+    KT_NAMES = ["pivot", "window", "window_select", "emit", "final", "recompute", "proxy", "gather",
+                "prep_x", "lr_t", "lr_score", "down"]
+
+    def ktrace(self, op: int):
+        """Debug kernel timeline (hire_debug_ktrace): op 1 enable+reset, 0 disable,
+        2 -> {kernel: (start_us, end_us)} relative to the earliest start."""
+        if op != 2:
+            check(lib().hire_debug_ktrace(self.h, op, None, 0))
+            return None
+        buf = (C.c_ulonglong * 64)()
+        
+        check(lib().hire_debug_ktrace(self.h, 2, buf, 64))
+        spans = {}
+        for i, name in enumerate(self.KT_NAMES):
+            a, b = buf[2 * i], buf[2 * i + 1]
+            if b:
+                spans[name] = (a, b)
+        t0 = min(a for a, _ in spans.values()) if spans else 0
+        if buf[39]:
+            spans["emit_last_cta"] = (buf[39], buf[42])
+            spans["emit_phases"] = (buf[40], buf[41])
+            spans["emit_max_start_max_publish"] = (buf[43], buf[44])
+        if buf[45]:
+            spans["ws_counts"] = (buf[45], buf[46])
+            spans["ws_bin"] = (buf[46], buf[47])
+            if buf[48]:
+                spans["ws_gather"] = (buf[47], buf[48])
+                spans["ws_select"] = (buf[48], buf[49])
+                spans["ws_m"] = (0, buf[50] * 1000)
+        return {k: (round((a - t0) / 1e3, 2), round((b - t0) / 1e3, 2)) for k, (a, b) in
+                sorted(spans.items(), key=lambda t: t[1][0])}
+
     def profile_read(self) -> dict:
         """{stage: (total_ms, intervals)} since the last read (syncs)."""
         n = len(L.STAGES)

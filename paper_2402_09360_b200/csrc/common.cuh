@@ -64,6 +64,43 @@ __host__ __device__ __forceinline__ float key_value(uint64_t k) {
 __device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void griddep_launch() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
+// ------------------------------------------------- kernel timeline trace --
+// Debug aid (hire_debug_ktrace): when g_ktrace is set, thread 0 of every CTA
+// records min(start) / max(end) %globaltimer per kernel id.
+__device__ unsigned long long* g_ktrace = nullptr;
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+struct KTrace {
+  int id;
+  __device__ __forceinline__ explicit KTrace(int i) : id(i) {
+    unsigned long long* t = g_ktrace;
+    if (t && threadIdx.x == 0) atomicMin(t + 2 * id, gtimer());
+  }
+  __device__ __forceinline__ ~KTrace() {
+    unsigned long long* t = g_ktrace;
+    if (t && threadIdx.x == 0) atomicMax(t + 2 * id + 1, gtimer());
+  }
+};
+enum KtId { kKtPivot = 0, kKtWindow = 1, kKtWindowSel = 2, kKtEmit = 3, kKtFinal = 4, kKtRecompute = 5,
+            kKtProxy = 6, kKtGather = 7, kKtPrep = 8, kKtLrT = 9, kKtLrScore = 10, kKtDown = 11,
+            kKtNum = 32 };
+
+// ------------------------------------------------ cross-CTA flag access --
+// Polling with ld.acquire costs an L1 invalidate (CCTL.IVALL) per probe;
+// spin with relaxed loads and fence once after the flag is seen.
+__device__ __forceinline__ unsigned ld_relaxed_gpu(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_relaxed_gpu(unsigned* p, unsigned v) {
+  asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void fence_acq_rel_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
+
 // --------------------------------------------------------------- loads --
 __device__ __forceinline__ uint4 ldg_stream(const void* p) {
   uint4 r;

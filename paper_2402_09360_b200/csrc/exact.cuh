@@ -59,6 +59,7 @@ __global__ void __launch_bounds__(256) recompute_fast(
     int64_t out_stride) {
   hire_dev::griddep_wait();
   hire_dev::griddep_launch();
+  KTrace kt_(kKtRecompute);
   extern __shared__ __align__(16) unsigned char smem[];
   float* s_x = reinterpret_cast<float*>(smem);
   constexpr int E = Vec16<T>::kElems;
@@ -95,6 +96,7 @@ __global__ void __launch_bounds__(128) recompute_seq(
     int64_t out_stride) {
   hire_dev::griddep_wait();
   hire_dev::griddep_launch();
+  KTrace kt_(kKtRecompute);
   extern __shared__ __align__(16) unsigned char smem[];
   float* s_x = reinterpret_cast<float*>(smem);
   const int b = blockIdx.y;
@@ -122,6 +124,7 @@ __global__ void __launch_bounds__(256) ffn_down_partial(
     float* __restrict__ partial) {
   hire_dev::griddep_wait();
   hire_dev::griddep_launch();
+  KTrace kt_(kKtDown);
   constexpr int E = Vec16<T>::kElems;
   const int c = blockIdx.x, b = blockIdx.y;
   const int lo = c * ch, hi = min(n_sel, lo + ch);

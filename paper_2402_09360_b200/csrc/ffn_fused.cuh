@@ -67,16 +67,13 @@ __device__ __forceinline__ int ld_acquire(const int* p) {
   return v;
 }
 
-// One poller per CTA with exponential backoff: 148 SMs spinning on one line
-// at ~64 ns would saturate its L2 slice and stall every other access that
-// maps there (measured: a 4 KB row gather taking 8.5 us).
+// One poller per CTA: relaxed probes (an acquire probe invalidates the
+// SM's L1 every time), one acquire fence once the target is reached.
 __device__ __forceinline__ void cta_wait_geq(const int* p, int target) {
   if (threadIdx.x == 0) {
-    unsigned ns = 32;
-    while (ld_acquire(p) < target) {
-      __nanosleep(ns);
-      ns = ns < 128 ? ns * 2 : 128;
+    while (static_cast<int>(ld_relaxed_gpu(reinterpret_cast<const unsigned*>(p))) < target) {
     }
+    fence_acq_rel_gpu();
   }
   __syncthreads();
 }

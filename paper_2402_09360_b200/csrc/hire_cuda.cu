@@ -27,6 +27,7 @@
 #include "ffn_fused.cuh"
 #include "score.cuh"
 #include "select.cuh"
+#include "select2.cuh"
 
 using namespace hire_dev;
 
@@ -83,6 +84,8 @@ struct hire_ctx_s {
   bool ffn_fused = true;
   bool trace = false;
   int* counters = nullptr;  // zeroed hand-off counters of the fused kernels
+  unsigned* selc = nullptr;  // zeroed selection counters (select2.cuh qc / agg)
+  size_t selc_cap = 0;
   // stage profiling (hire_ctx_set_profiling): event pairs around each stage
   bool prof = false;
   std::vector<cudaEvent_t> ev_pool;
@@ -211,6 +214,21 @@ int ensure_host(void** buf, size_t* cap, size_t need, cudaStream_t s) {
   return HIRE_OK;
 }
 
+// Zero-at-rest counters for select2.cuh (the kernels restore the zeros).
+int ensure_selc(hire_ctx ctx, size_t words) {
+  if (words <= ctx->selc_cap) return HIRE_OK;
+  if (ctx->selc) {
+    CK(cudaStreamSynchronize(ctx->stream));
+    CK(cudaFree(ctx->selc));
+    ctx->selc = nullptr;
+  }
+  const size_t n = std::max<size_t>(words, 4096);
+  CK(cudaMalloc(&ctx->selc, n * sizeof(unsigned)));
+  CK(cudaMemset(ctx->selc, 0, n * sizeof(unsigned)));
+  ctx->selc_cap = n;
+  return HIRE_OK;
+}
+
 // Bump allocator over the context workspace. Offsets first, then one
 // ensure(); pointers are only valid for the current call.
 struct Arena {
@@ -236,13 +254,39 @@ int max_blocks(K kernel, int threads, size_t smem) {
 }
 
 // ----------------------------------------------------- selection policy --
+constexpr int64_t kSelGridChunks = 4 * 148;  // S2/S3 CTAs over a whole batch (co-resident)
+
 struct SelPlan {
-  int mode = 0;          // 0 direct, 1 bucket
+  int mode = 0;          // 0 direct, 1 bucket, 2 grid-wide pivot/window/emit (select2.cuh)
   int n_buckets = 0, t = 0;
   int exact_fix = 1;
   int64_t k_eff = 0;     // candidates produced
   bool clamped = false;
+  int64_t wcap = 0;      // mode 2: window capacity per chunk
+  int64_t wseg = 0;      // mode 2: window segment (keys) per chunk
+  // u64 workspace words for B queries ("surv" buffer); mode 2: pivots,
+  // thresholds and one window segment per chunk (<= kSelGridChunks chunks
+  // over the whole batch)
+  int64_t surv_words(int64_t B) const {
+    // piv, thr, 8 x 256-bin hists, 8 x 256 x 32 bin lists, chunk windows
+    if (mode == 2) return 5 * B + B * 1024 + B * 65536 + wseg * kSelGridChunks;
+    return B * std::max(n_buckets * t, 1);
+  }
 };
+
+// Prime multiplier coprime with nblk for the S1 sample permutation.
+uint32_t sample_perm(uint64_t nblk) {
+  auto is_prime = [](uint64_t v) {
+    if (v < 2) return false;
+    for (uint64_t f = 2; f * f <= v; ++f)
+      if (v % f == 0) return false;
+    return true;
+  };
+  uint64_t p = std::max<uint64_t>(3, static_cast<uint64_t>(0.6180339887 * static_cast<double>(nblk)));
+  while (!is_prime(p) || nblk % p == 0) ++p;
+  const uint32_t r = static_cast<uint32_t>(p % std::max<uint64_t>(nblk, 1));
+  return r ? r : 1u;
+}
 
 int plan_select(int64_t n, int64_t k_prime, int sel_mode, int64_t nb_req, int64_t t_req,
                 SelPlan* sp) {
@@ -268,6 +312,15 @@ int plan_select(int64_t n, int64_t k_prime, int sel_mode, int64_t nb_req, int64_
   }
   sp->k_eff = std::min(k_prime, n);
   sp->clamped = k_prime > n;
+  if (nb_req == 0 && std::getenv("HIRE_SELECT_V1") == nullptr) {
+    sp->mode = 2;
+    if (n > kSel2Exact) {
+      // window segment per chunk: the chunk width, capped (a chunk holding
+      // more window keys than its segment falls back to the slow path)
+      sp->wseg = std::min<int64_t>(n, 1024);
+    }
+    return HIRE_OK;
+  }
   if (n <= kDirectMax && nb_req == 0) {
     sp->mode = 0;
     return HIRE_OK;
@@ -307,6 +360,44 @@ int run_select(hire_ctx ctx, const float* scores, int64_t score_stride, int64_t 
                const SelPlan& sp, uint64_t* surv, uint32_t* cand, int64_t cand_stride,
                int* status) {
   StageScope scope(ctx, kStageSelect);
+  if (sp.mode == 2) {
+    const uint32_t nn = static_cast<uint32_t>(n), K = static_cast<uint32_t>(sp.k_eff);
+    if (n <= kSel2Exact) {
+      CK(launch_k(ctx, sel_exact_kernel, static_cast<unsigned>(B), kSel2Threads, 0, scores, score_stride,
+                  nn, K, cand, cand_stride));
+      CK(cudaGetLastError());
+      return HIRE_OK;
+    }
+    // chunks per query: every S3 CTA of the grid must be co-resident (the
+    // look-back waits on lower chunks), 4 x 256-thread CTAs per SM
+    const int64_t C = std::max<int64_t>(
+        1, std::min<int64_t>({std::min<int64_t>(4 * ctx->num_sms, kSelGridChunks) / B,
+                              ceil_div(n, kWinThreads * kScanBatch), kWselMaxChunks}));
+    if (C * B > std::min<int64_t>(4 * ctx->num_sms, kSelGridChunks))
+      return invalid("selection: batch too large for the grid-wide selector");
+    const uint32_t seg = static_cast<uint32_t>(sp.wseg);
+    RET(ensure_selc(ctx, static_cast<size_t>(B * 3 * C)));
+    unsigned* cnt = ctx->selc;
+    unsigned* agg = ctx->selc + B * 2 * C;
+    uint64_t* piv = surv;                                        // [B][4]
+    uint64_t* thr = surv + 4 * B;                                // [B]
+    unsigned* gh = reinterpret_cast<unsigned*>(surv + 5 * B);    // [B][kWinGroups][kWinBins]
+    uint64_t* lists = surv + 5 * B + B * kWinBins * kWinGroups / 2;  // [B][groups][bins][cap]
+    uint64_t* win = lists + B * kWinGroups * kWinBins * kBinCap;      // [B][C][seg]
+    const uint32_t perm = sample_perm(static_cast<uint64_t>(n) / 4);
+    CK(launch_k(ctx, sel_pivot_kernel, static_cast<unsigned>(B), kPivThreads, 0, scores, score_stride,
+                nn, K, perm, piv, gh));
+    CK(launch_k(ctx, sel_window_kernel, dim3(static_cast<unsigned>(C), static_cast<unsigned>(B)), kWinThreads, 0,
+                scores, score_stride, nn, static_cast<const uint64_t*>(piv), win, seg, cnt, agg, gh, lists));
+    CK(launch_k(ctx, sel_wselect_kernel, static_cast<unsigned>(B), kWselThreads, 0, scores, score_stride, nn, K,
+                static_cast<int>(C), static_cast<const uint64_t*>(piv), static_cast<const uint64_t*>(win), seg,
+                static_cast<const unsigned*>(cnt), static_cast<const unsigned*>(gh),
+                static_cast<const uint64_t*>(lists), thr, status));
+    CK(launch_k(ctx, sel_emit_kernel, dim3(static_cast<unsigned>(C), static_cast<unsigned>(B)), kEmitThreads, 0,
+                scores, score_stride, nn, static_cast<const uint64_t*>(thr), agg, cand, cand_stride));
+    CK(cudaGetLastError());
+    return HIRE_OK;
+  }
   if (sp.mode == 1) {
     CK(launch_k(ctx, bucket_topt_kernel, dim3(sp.n_buckets, static_cast<unsigned>(B)), 256,
                 static_cast<size_t>(ceil_div(n, sp.n_buckets)) * 8, 
@@ -573,6 +664,20 @@ int run_final(hire_ctx ctx, const float* vals, int64_t vs, const uint32_t* idx, 
   int64_t P = 1;
   while (P < K) P <<= 1;
   const size_t smem = out_mode == 0 ? static_cast<size_t>(P) * 8 : 0;
+  if (n <= kFinal2Max && !std::getenv("HIRE_SELECT_V1")) {
+    const int np = static_cast<int>(std::max<int64_t>(n_per, 1));
+#define HIRE_F2(NT_, KPT)                                                                               \
+    if (n <= NT_ * KPT) {                                                                               \
+      CK(launch_k(ctx, final2_kernel<NT_, KPT>, static_cast<unsigned>(B), NT_, smem, vals, vs, idx, is, \
+                  src_keys, np, part_stride, static_cast<int>(n), static_cast<int>(K), out_mode, out_idx,   \
+                  out_val, out_prob, out_keys, out_stride));                                            \
+      CK(cudaGetLastError());                                                                           \
+      return HIRE_OK;                                                                                   \
+    }
+    HIRE_F2(128, 1) HIRE_F2(128, 2) HIRE_F2(128, 4) HIRE_F2(128, 8) HIRE_F2(128, 16)
+    HIRE_F2(256, 16) HIRE_F2(256, 32) HIRE_F2(512, 32)
+#undef HIRE_F2
+  }
   CK(launch_k(ctx, final_select_kernel, static_cast<unsigned>(B), kSelectThreads, smem, 
       vals, vs, idx, is, src_keys, static_cast<int>(std::max<int64_t>(n_per, 1)), part_stride,
       static_cast<int>(n), static_cast<int>(K), out_mode, out_idx, out_val, out_prob, out_keys, out_stride));
@@ -604,6 +709,7 @@ __global__ void iota_mod_kernel(uint32_t* u, int64_t m, int64_t n) {
 __global__ void gather_values_kernel(const float* v, int64_t n, const uint32_t* c, int64_t kk, int64_t B, float* o) {
   hire_dev::griddep_wait();
   hire_dev::griddep_launch();
+  KTrace kt_(hire_dev::kKtGather);
   const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i < kk * B) o[i] = v[(i / kk) * n + c[i]];
 }
@@ -698,7 +804,7 @@ void take_topk_ws(Arena& ar, TopkWs* t, const hire_scorer_s* a, int64_t B, const
                   bool need_cand) {
   take_score_ws(ar, &t->sw, a, B);
   ar.take(&t->scores, static_cast<size_t>(B * a->rows));
-  ar.take(&t->surv, static_cast<size_t>(B) * std::max(sp.n_buckets * sp.t, 1));
+  ar.take(&t->surv, static_cast<size_t>(sp.surv_words(B)));
   if (need_cand) ar.take(&t->cand, static_cast<size_t>(B * sp.k_eff));
   ar.take(&t->vals, static_cast<size_t>(B * sp.k_eff));
   ar.take(&t->status, 1);
@@ -740,6 +846,17 @@ int hire_ctx_create(int device, void* stream, int own_stream, hire_ctx* out) {
   // opt-in shared memory for the selectors
   CK(cudaFuncSetAttribute(select_candidates_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                           kPoolKeys * 8));
+  {
+    const int f2 = kFinalMax * 8;
+    CK(cudaFuncSetAttribute(final2_kernel<128, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, f2));
+    CK(cudaFuncSetAttribute(final2_kernel<128, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, f2));
+    CK(cudaFuncSetAttribute(final2_kernel<128, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, f2));
+    CK(cudaFuncSetAttribute(final2_kernel<128, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, f2));
+    CK(cudaFuncSetAttribute(final2_kernel<128, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, f2));
+    CK(cudaFuncSetAttribute(final2_kernel<256, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, f2));
+    CK(cudaFuncSetAttribute(final2_kernel<256, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize, f2));
+    CK(cudaFuncSetAttribute(final2_kernel<512, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize, f2));
+  }
   CK(cudaFuncSetAttribute(final_select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                           kFinalMax * 8));
   CK(cudaFuncSetAttribute(bucket_topt_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -779,6 +896,7 @@ int hire_ctx_destroy(hire_ctx c) {
   cudaStreamSynchronize(c->stream);
   if (c->ws) cudaFree(c->ws);
   if (c->counters) cudaFree(c->counters);
+  if (c->selc) cudaFree(c->selc);
   if (c->io_dev) cudaFree(c->io_dev);
   if (c->io_host) cudaFreeHost(c->io_host);
   for (auto& m : c->marks) { cudaEventDestroy(m.second.first); cudaEventDestroy(m.second.second); }
@@ -806,6 +924,28 @@ int hire_ctx_read_trace(hire_ctx c, long long* out, int n) {
   if (!c || !out || n > 28) return invalid("bad trace request");
   CK(cudaStreamSynchronize(c->stream));
   CK(cudaMemcpy(out, c->counters + 320, static_cast<size_t>(n) * 8, cudaMemcpyDeviceToHost));
+  return HIRE_OK;
+}
+
+int hire_debug_ktrace(hire_ctx c, int op, unsigned long long* out, int n) {
+  // op 1: enable + reset, 2: read n (<= 64) words, 0: disable
+  if (!c) return invalid("null handle");
+  static unsigned long long* buf = nullptr;
+  constexpr int kWords = 2 * hire_dev::kKtNum;
+  CK(cudaStreamSynchronize(c->stream));
+  if (op == 1) {
+    if (!buf) CK(cudaMalloc(&buf, kWords * sizeof(unsigned long long)));
+    unsigned long long init[kWords];
+    for (int i = 0; i < kWords; ++i) init[i] = (i & 1) || i >= 39 ? 0ull : ~0ull;
+    CK(cudaMemcpy(buf, init, sizeof(init), cudaMemcpyHostToDevice));
+    CK(cudaMemcpyToSymbol(hire_dev::g_ktrace, &buf, sizeof(buf)));
+  } else if (op == 2) {
+    if (!buf || !out || n > kWords) return invalid("ktrace not enabled / bad size");
+    CK(cudaMemcpy(out, buf, static_cast<size_t>(n) * 8, cudaMemcpyDeviceToHost));
+  } else {
+    unsigned long long* z = nullptr;
+    CK(cudaMemcpyToSymbol(hire_dev::g_ktrace, &z, sizeof(z)));
+  }
   return HIRE_OK;
 }
 
@@ -1139,7 +1279,7 @@ int hire_topk_select(hire_ctx ctx, const float* v, int64_t B, int64_t n, int64_t
   uint32_t* cand;
   int* status;
   float* cv;
-  ar.take(&surv, static_cast<size_t>(B) * std::max(sp.n_buckets * sp.t, 1));
+  ar.take(&surv, static_cast<size_t>(sp.surv_words(B)));
   ar.take(&cand, static_cast<size_t>(B * sp.k_eff));
   ar.take(&status, 1);
   ar.take(&cv, static_cast<size_t>(B * sp.k_eff));
@@ -1298,7 +1438,7 @@ void take_ffn_ws(Arena& ar, FfnWs* fw, const hire_scorer_s* a, int64_t B, int64_
                  int64_t g, int64_t kg, int64_t kpg, const SelPlan& sp, int64_t max_chunks) {
   take_score_ws(ar, &fw->t.sw, a, B);
   ar.take(&fw->t.scores, static_cast<size_t>(B * m));
-  ar.take(&fw->t.surv, static_cast<size_t>(B) * std::max(sp.n_buckets * sp.t, 1));
+  ar.take(&fw->t.surv, static_cast<size_t>(sp.surv_words(B)));
   ar.take(&fw->t.status, 1);
   ar.take(&fw->proxy, static_cast<size_t>(B * (m / g)));
   ar.take(&fw->cand, static_cast<size_t>(B * kpg));

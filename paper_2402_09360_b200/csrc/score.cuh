@@ -32,6 +32,7 @@ __global__ void __launch_bounds__(256) prep_x_int8_kernel(
     int* __restrict__ sumxq_out) {
   hire_dev::griddep_wait();
   hire_dev::griddep_launch();
+  KTrace kt_(kKtPrep);
   const int b = blockIdx.x;
   const float* xb = x + static_cast<int64_t>(b) * d;
   __shared__ float s_red[8];
@@ -90,6 +91,7 @@ __global__ void __launch_bounds__(256) q4_score_fast_int8(
     float* __restrict__ scores, int64_t score_stride) {
   hire_dev::griddep_wait();
   hire_dev::griddep_launch();
+  KTrace kt_(kKtProxy);
   const int lane = threadIdx.x & 31;
   const int64_t warp = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
@@ -171,6 +173,7 @@ __global__ void __launch_bounds__(256) q4_score_fast_fpx(
     float* __restrict__ scores) {
   hire_dev::griddep_wait();
   hire_dev::griddep_launch();
+  KTrace kt_(kKtProxy);
   const int lane = threadIdx.x & 31;
   const int64_t warp = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
@@ -221,6 +224,7 @@ __global__ void __launch_bounds__(128) q4_score_seq(
     int64_t score_stride) {
   hire_dev::griddep_wait();
   hire_dev::griddep_launch();
+  KTrace kt_(kKtProxy);
   extern __shared__ __align__(16) unsigned char smem[];
   float* s_x = reinterpret_cast<float*>(smem);
   int8_t* s_xq = reinterpret_cast<int8_t*>(smem + static_cast<size_t>(d) * 4);
@@ -313,6 +317,7 @@ __global__ void __launch_bounds__(256) lr_t_kernel(const T* __restrict__ z1, int
                                                    int strict, float* __restrict__ t) {
   hire_dev::griddep_wait();
   hire_dev::griddep_launch();
+  KTrace kt_(kKtLrT);
   if (strict) {
     const int id = blockIdx.x * blockDim.x + threadIdx.x;
     if (id >= r * B) return;
@@ -348,6 +353,7 @@ __global__ void __launch_bounds__(128) lr_score_kernel(
     float* __restrict__ scores, int64_t score_stride) {
   hire_dev::griddep_wait();
   hire_dev::griddep_launch();
+  KTrace kt_(kKtLrScore);
   extern __shared__ __align__(16) unsigned char smem[];
   float* s_t = reinterpret_cast<float*>(smem);
   block_copy(s_t, t, R * B);
@@ -391,6 +397,7 @@ __global__ void __launch_bounds__(128) lr_score_generic(
     float* __restrict__ scores, int64_t score_stride) {
   hire_dev::griddep_wait();
   hire_dev::griddep_launch();
+  KTrace kt_(kKtLrScore);
   extern __shared__ __align__(16) unsigned char smem[];
   float* s_t = reinterpret_cast<float*>(smem);
   block_copy(s_t, t, r * B);
@@ -482,6 +489,7 @@ __global__ void __launch_bounds__(256) q4_score_mma(
     int B, int phi, float* __restrict__ scores, int64_t score_stride) {
   hire_dev::griddep_wait();
   hire_dev::griddep_launch();
+  KTrace kt_(kKtProxy);
   extern __shared__ __align__(16) unsigned char smem[];
   constexpr int RB_PER_CTA = 8 / KS;
   const int xs = d + 16;  // padded query stride (bank spread)

@@ -1,0 +1,116 @@
+"""GPU: the grid-wide candidate selector (select2.cuh) against the oracle's
+topk_select (linalg.hpp:157-176) — bit-exact indices and values, ties by
+ascending index, over sizes that hit every path (single-CTA small mode,
+sampled pivots + window, window overflow / bracket-miss fallback) and
+adversarial value distributions."""
+import numpy as np
+import pytest
+import torch
+
+
+pytestmark = pytest.mark.gpu
+
+
+def T(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+def N(t):
+    return t.cpu().numpy()
+
+
+def _rows(n, seed):
+    g = np.random.default_rng(seed)
+    rows = {
+        "normal": g.standard_normal(n),
+        "int_ties": g.integers(-20, 20, size=n),
+        "all_equal": np.zeros(n),
+        "relu": np.maximum(g.standard_normal(n) - 2.0, 0.0),
+        "ascending": np.sort(g.standard_normal(n)),
+        "descending": -np.sort(g.standard_normal(n)),
+        "spiky": np.where(g.random(n) < 0.001, 100.0 + g.random(n), g.random(n) * 1e-3),
+        "two_level": np.where(np.arange(n) % 97 == 0, 1.0, 0.5),
+    }
+    return {k: v.astype(np.float32) for k, v in rows.items()}
+
+
+def _check(H, O, v, k):
+    idx, val, cl = H.topk_select(T(v), k)
+    for b in range(v.shape[0]):
+        wi, wv, wcl = O.topk_select(v[b], k)
+        gi = N(idx[b]).astype(np.uint32)
+        assert np.array_equal(gi, wi), (b, k, gi[:8], wi[:8])
+        assert np.array_equal(N(val[b]).view(np.uint32), wv.view(np.uint32))
+        assert cl == wcl
+
+
+@pytest.mark.parametrize("n", [1, 2, 63, 64, 65, 1000, 8191, 8192, 8193, 9000, 32768, 256000])
+def test_select_distributions(H, O, n):
+    rows = _rows(n, n)
+    v = np.stack(list(rows.values()))
+    ks = sorted({1, min(n, 7), max(1, n // 100), max(1, n // 8), max(1, n - 1), n})
+    for k in [k for k in ks if k <= 16384]:  # ranked output: k <= kFinalMax
+        _check(H, O, v, k)
+
+
+@pytest.mark.parametrize("n,k", [(1_000_000, 2048), (1_000_000, 16384), (300_000, 9000)])
+def test_select_large(H, O, n, k):
+    g = np.random.default_rng(7)
+    v = np.stack([g.standard_normal(n), np.maximum(g.standard_normal(n), 0.0)]).astype(np.float32)
+    _check(H, O, v, k)
+
+
+@pytest.mark.parametrize("n,kp", [(60000, 30000), (60000, 59999), (60000, 60000), (20000, 19000)])
+def test_candidate_sets_large_k_prime(H, O, n, kp):
+    # candidate sets (ascending indices) for k' near n go through hire_topk
+    g = np.random.default_rng(n + kp)
+    d, r = 16, 4
+    z1 = g.standard_normal((r, d)).astype(np.float32)
+    z2 = np.round(g.standard_normal((n, r)) * 2).astype(np.float32)  # integer proxy scores: ties
+    w = g.standard_normal((n, d)).astype(np.float32)
+    x = np.round(g.standard_normal((2, d))).astype(np.float32)
+    a = H.ApproxScorer.low_rank(T(z1), T(z2))
+    cfg = H.HireConfig(k=5, k_prime=kp, strict=True)
+    res = H.hire_topk(T(x), H.ScoreMatrix(T(w)), a, cfg)
+    for b in range(2):
+        s = O.lowrank_scores(z1, z2, x[b], 0)
+        want = O.hire_topk(w, x[b], s, 5, kp, 0)
+        assert np.array_equal(N(res.cand[b]).astype(np.uint32), want["cand"])
+        assert np.array_equal(N(res.top_idx[b]).astype(np.uint32), want["top_idx"])
+
+
+def test_select_repeated_calls_reset_counters(H, O):
+    # zero-at-rest counters: back-to-back calls with different shapes
+    g = np.random.default_rng(3)
+    for it in range(6):
+        n = [50000, 9000, 256000, 20000, 256000, 8193][it]
+        B = [1, 4, 2, 16, 1, 3][it]
+        v = g.standard_normal((B, n)).astype(np.float32)
+        _check(H, O, v, [1024, 100, 2048, 256, 1024, 8000][it])
+
+
+def test_select_batch_many_queries(H, O):
+    g = np.random.default_rng(5)
+    v = g.standard_normal((64, 30000)).astype(np.float32)
+    v[::3] = np.round(v[::3] * 4)  # ties on every third query
+    _check(H, O, v, 300)
+
+
+def test_select_in_cuda_graph(H, O):
+    g = np.random.default_rng(9)
+    v = T(g.standard_normal((2, 100000)).astype(np.float32))
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        H.topk_select(v, 1000)  # workspace exists before capture
+        torch.cuda.synchronize()
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph, stream=s):
+            idx, val, _ = H.topk_select(v, 1000)
+    for _ in range(3):
+        v.copy_(T(g.standard_normal((2, 100000)).astype(np.float32)))
+        graph.replay()
+        torch.cuda.synchronize()
+        h = N(v)
+        for b in range(2):
+            wi, wv, _ = O.topk_select(h[b], 1000)
+            assert np.array_equal(N(idx[b]).astype(np.uint32), wi)
