@@ -53,7 +53,7 @@ struct Vec16<float> {
 // grid = (tiles, B); 8 warps per CTA; warp-strided over the n_cand rows of
 // query b. cand == nullptr means row i itself (dense exact, K8).
 template <typename T, int CPL>
-__global__ void __launch_bounds__(256) recompute_fast(
+__global__ void __launch_bounds__(256, 2) recompute_fast(
     const T* __restrict__ w, int d, const uint32_t* __restrict__ cand, int64_t cand_stride,
     int n_cand, const float* __restrict__ x, int phi, float* __restrict__ out,
     int64_t out_stride) {
@@ -85,6 +85,107 @@ __global__ void __launch_bounds__(256) recompute_fast(
     }
     acc = warp_sum_f32(acc);
     if (lane == 0) out[b * out_stride + i] = apply_phi(phi, acc);
+  }
+}
+
+// Same arithmetic as recompute_fast (lane chunk order, fmaf order, fixed
+// butterfly -> bit-identical values), but the gathered rows are moved by
+// the bulk-copy engine into shared memory (cp.async.bulk + mbarrier), so the
+// bytes in flight are not bounded by registers. Each warp owns two groups
+// of G row slots and alternates: while one group is consumed the other is
+// in flight. A group is consumed chunk by chunk with each x chunk read once
+// for all G rows (x is the larger smem stream: fp32 vs bf16 rows). x sits in
+// shared memory split into low / high 16-byte halves of each lane chunk so
+// the 128-bit reads are conflict-free. 4 warps, one CTA per SM.
+template <typename T, int G>
+__global__ void __launch_bounds__(128, 1) recompute_tma(
+    const T* __restrict__ w, int d, const uint32_t* __restrict__ cand, int64_t cand_stride,
+    int n_cand, const float* __restrict__ x, int phi, float* __restrict__ out, int64_t out_stride) {
+  hire_dev::griddep_wait();
+  hire_dev::griddep_launch();
+  KTrace kt_(kKtRecompute);
+  constexpr int NW = 4, S = 2 * G;
+  constexpr int E = Vec16<T>::kElems;  // elements per 16-byte chunk
+  extern __shared__ __align__(128) unsigned char smem[];
+  const int b = blockIdx.y;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const unsigned row_bytes = static_cast<unsigned>(d) * sizeof(T);
+  const int cpl = static_cast<int>(row_bytes / 512);
+  const int nchunk = d / E;
+  float* s_xa = reinterpret_cast<float*>(smem);            // [nchunk][min(E,4)]
+  float* s_xb = s_xa + static_cast<size_t>(nchunk) * 4;    // [nchunk][4] (E == 8 only)
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + static_cast<size_t>(d) * 4);
+  unsigned char* rows = smem + ((static_cast<size_t>(d) * 4 + NW * S * 8 + 127) & ~static_cast<size_t>(127));
+  uint64_t* mybar = bars + wid * S;
+  unsigned char* myrows = rows + static_cast<size_t>(wid) * S * row_bytes;
+  if (lane == 0)
+    for (int s = 0; s < S; ++s) mbar_init(&mybar[s], 1);
+  fence_mbar_init();
+  {
+    const float* xb = x + static_cast<int64_t>(b) * d;
+    for (int i = threadIdx.x; i < d; i += blockDim.x) {
+      const int ch = i / E, e = i % E;
+      if (E == 8) (e < 4 ? s_xa : s_xb)[ch * 4 + (e & 3)] = xb[i];
+      else s_xa[i] = xb[i];
+    }
+  }
+  __syncthreads();
+  const int gw = blockIdx.x * NW + wid, nw = gridDim.x * NW;
+  const int cnt = n_cand > gw ? (n_cand - gw + nw - 1) / nw : 0;  // rows of this warp: gw + k*nw
+  auto issue = [&](int k, int s) {
+    const int i = gw + k * nw;
+    const int64_t row = cand ? static_cast<int64_t>(cand[b * cand_stride + i]) : i;
+    mbar_arrive_expect_tx(&mybar[s], row_bytes);
+    bulk_g2s(myrows + static_cast<size_t>(s) * row_bytes,
+             reinterpret_cast<const unsigned char*>(w) + row * row_bytes, row_bytes, &mybar[s]);
+  };
+  const int ngroups = (cnt + G - 1) / G;
+  if (lane == 0)
+    for (int k = 0; k < S && k < cnt; ++k) issue(k, k);
+  for (int gi = 0; gi < ngroups; ++gi) {
+    const int half = gi & 1;
+    const unsigned ph = static_cast<unsigned>((gi >> 1) & 1);
+    const int k0 = gi * G;
+    float acc[G];
+#pragma unroll
+    for (int r = 0; r < G; ++r) {
+      acc[r] = 0.0f;
+      if (k0 + r < cnt) mbar_wait(&mybar[half * G + r], ph);
+    }
+    const uint4* rp = reinterpret_cast<const uint4*>(myrows + static_cast<size_t>(half * G) * row_bytes);
+    const int rstride = static_cast<int>(row_bytes / 16);
+#pragma unroll 2
+    for (int c = 0; c < cpl; ++c) {
+      const int ch = lane + 32 * c;
+      float xv[E];
+      {
+        const float4 a = *reinterpret_cast<const float4*>(s_xa + ch * 4);
+        xv[0] = a.x; xv[1] = a.y; xv[2] = a.z; xv[3] = a.w;
+        if (E == 8) {
+          const float4 bq = *reinterpret_cast<const float4*>(s_xb + ch * 4);
+          xv[4 % E] = bq.x; xv[5 % E] = bq.y; xv[6 % E] = bq.z; xv[7 % E] = bq.w;
+        }
+      }
+#pragma unroll
+      for (int r = 0; r < G; ++r) {
+        float f[E];
+        Vec16<T>::expand(rp[r * rstride + ch], f);
+#pragma unroll
+        for (int e = 0; e < E; ++e) acc[r] = fmaf(f[e], xv[e], acc[r]);
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < G; ++r) {
+      const float v = warp_sum_f32(acc[r]);
+      if (lane == 0 && k0 + r < cnt) out[b * out_stride + gw + (k0 + r) * nw] = apply_phi(phi, v);
+    }
+    __syncwarp();
+    if (lane == 0) {
+      fence_proxy_async_smem();  // this group's reads precede its refill
+#pragma unroll
+      for (int r = 0; r < G; ++r)
+        if (k0 + r + S < cnt) issue(k0 + r + S, half * G + r);
+    }
   }
 }
 

@@ -581,6 +581,27 @@ int run_scores(hire_ctx ctx, const hire_scorer_s* a, const float* x, int64_t B, 
   // low-rank
   const int r = static_cast<int>(a->r);
   const bool bf = a->dtype == HIRE_BF16;
+  if (!strict && d % 8 == 0 && (r == 32 || r == 64 || r == 128) && B <= 64 && !std::getenv("HIRE_LR_SIMT")) {
+    const dim3 gt(static_cast<unsigned>(r), static_cast<unsigned>(ceil_div(B, 4)));
+    if (bf) CK(launch_k(ctx, lr_t_fast<__nv_bfloat16>, gt, 256, 0, static_cast<const __nv_bfloat16*>(a->z1), d, x, static_cast<int>(B), r, w.t));
+    else CK(launch_k(ctx, lr_t_fast<float>, gt, 256, 0, static_cast<const float*>(a->z1), d, x, static_cast<int>(B), r, w.t));
+    const int64_t tiles = ceil_div(a->rows, 16);
+    const unsigned grid = static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>(ceil_div(tiles, kLrThreads / 32), 3 * ctx->num_sms)));
+#define LRM(TT, RR, NN)                                                                                    \
+    CK(launch_k(ctx, lr_score_mma<TT, RR, NN>, grid, kLrThreads, 0, static_cast<const TT*>(a->z2), a->rows, \
+                static_cast<const float*>(w.t), static_cast<int>(B), static_cast<int>(b0), phi, out, stride))
+#define LRR(TT, NN) \
+    { if (r == 32) LRM(TT, 32, NN); else if (r == 64) LRM(TT, 64, NN); else LRM(TT, 128, NN); }
+    for (int64_t b0 = 0; b0 < B; b0 += 16) {
+      const bool one = B - b0 <= 8;
+      if (bf) { if (one) LRR(__nv_bfloat16, 1) else LRR(__nv_bfloat16, 2) }
+      else { if (one) LRR(float, 1) else LRR(float, 2) }
+    }
+#undef LRR
+#undef LRM
+    CK(cudaGetLastError());
+    return HIRE_OK;
+  }
   {
     const int64_t items = static_cast<int64_t>(r) * B;
     const unsigned grid = static_cast<unsigned>(strict ? ceil_div(items, 256) : ceil_div(items * 32, 256));
@@ -614,10 +635,48 @@ int launch_recompute_fast(hire_ctx ctx, const void* w, int d, const uint32_t* ca
                           float* out, int64_t out_stride) {
   const size_t smem = static_cast<size_t>(d) * 4;
   auto k = recompute_fast<T, CPL>;
-  const int64_t tiles = std::max<int64_t>(1, std::min<int64_t>(ceil_div(n_cand, 8), std::max<int64_t>(1, 4 * ctx->num_sms / B)));
+  // one wave of 2 CTAs/SM (8 warps each); warps stride over the rows
+  const int64_t tiles = std::max<int64_t>(1, std::min<int64_t>(ceil_div(n_cand, 8), std::max<int64_t>(1, 2 * ctx->num_sms / B)));
   CK(launch_k(ctx, k, dim3(static_cast<unsigned>(tiles), static_cast<unsigned>(B)), 256, smem, 
       static_cast<const T*>(w), d, cand, cand_stride, static_cast<int>(n_cand), x, phi, out, out_stride));
   CK(cudaGetLastError());
+  return HIRE_OK;
+}
+
+// Bulk-copy ring variant (exact.cuh recompute_tma); *done = false when the
+// rows do not fit two groups of slots.
+template <typename T, int G>
+int launch_recompute_tma_g(hire_ctx ctx, const void* w, int d, const uint32_t* cand, int64_t cand_stride,
+                           int64_t n_cand, const float* x, int64_t B, int phi, float* out, int64_t out_stride) {
+  const size_t row_bytes = static_cast<size_t>(d) * sizeof(T);
+  const size_t smem = ((static_cast<size_t>(d) * 4 + 4 * 2 * G * 8 + 127) & ~static_cast<size_t>(127)) +
+                      4 * 2 * G * row_bytes;
+  static bool attr = false;
+  if (!attr) {
+    CK(cudaFuncSetAttribute(recompute_tma<T, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+    attr = true;
+  }
+  const int64_t per_q = std::max<int64_t>(1, std::min<int64_t>(ctx->num_sms / std::max<int64_t>(B, 1), ceil_div(n_cand, 8)));
+  CK(launch_k(ctx, recompute_tma<T, G>, dim3(static_cast<unsigned>(per_q), static_cast<unsigned>(B)), 128, smem,
+              static_cast<const T*>(w), d, cand, cand_stride, static_cast<int>(n_cand), x, phi, out, out_stride));
+  CK(cudaGetLastError());
+  return HIRE_OK;
+}
+
+template <typename T>
+int launch_recompute_tma(hire_ctx ctx, const void* w, int d, const uint32_t* cand, int64_t cand_stride,
+                         int64_t n_cand, const float* x, int64_t B, int phi, float* out, int64_t out_stride,
+                         bool* done) {
+  *done = false;
+  const size_t row_bytes = static_cast<size_t>(d) * sizeof(T);
+  const size_t fixed = static_cast<size_t>(d) * 4 + 1024;
+  const size_t budget = 224 * 1024;
+  auto fits = [&](int g) { return fixed + 4 * 2 * static_cast<size_t>(g) * row_bytes <= budget; };
+  if (fits(4)) { RET((launch_recompute_tma_g<T, 4>(ctx, w, d, cand, cand_stride, n_cand, x, B, phi, out, out_stride))); }
+  else if (fits(3)) { RET((launch_recompute_tma_g<T, 3>(ctx, w, d, cand, cand_stride, n_cand, x, B, phi, out, out_stride))); }
+  else if (fits(2)) { RET((launch_recompute_tma_g<T, 2>(ctx, w, d, cand, cand_stride, n_cand, x, B, phi, out, out_stride))); }
+  else return HIRE_OK;
+  *done = true;
   return HIRE_OK;
 }
 
@@ -630,6 +689,16 @@ int run_recompute(hire_ctx ctx, const hire_matrix_s* m, const uint32_t* cand, in
   const int d = static_cast<int>(m->d);
   const size_t es = dtype_size(m->dtype);
   const int64_t bytes = static_cast<int64_t>(d) * static_cast<int64_t>(es);
+  // bulk-copy ring for large gathers (many rows per SM); the register
+  // version has less set-up latency for a few thousand rows
+  if (!strict && bytes % 512 == 0 && n_cand * B >= 8192 && !std::getenv("HIRE_RECOMPUTE_REGS")) {
+    bool done = false;
+    if (m->dtype == HIRE_BF16)
+      RET(launch_recompute_tma<__nv_bfloat16>(ctx, m->ptr, d, cand, cand_stride, n_cand, x, B, phi, out, out_stride, &done));
+    else
+      RET(launch_recompute_tma<float>(ctx, m->ptr, d, cand, cand_stride, n_cand, x, B, phi, out, out_stride, &done));
+    if (done) return HIRE_OK;
+  }
   if (!strict && bytes % 512 == 0) {
     const int cpl = static_cast<int>(bytes / 512);
     const bool bf = m->dtype == HIRE_BF16;

@@ -390,6 +390,221 @@ __global__ void __launch_bounds__(128) lr_score_kernel(
   }
 }
 
+// ---------------------------------------------------------------------
+// K2 step 1, fast: t[b][q] = sum_i Z1[q][i] x[b][i]. grid (r, ceil(B/4)),
+// 256 threads; each thread owns 8-element chunks i = 8(tid + 256 j) and up
+// to 4 queries; all loads issued up front; fixed-order reduction
+// (per-thread chunk order, butterfly, warps in order) -> deterministic.
+// ---------------------------------------------------------------------
+template <typename T>
+__global__ void __launch_bounds__(256) lr_t_fast(const T* __restrict__ z1, int d,
+                                                 const float* __restrict__ x, int B, int r,
+                                                 float* __restrict__ t) {
+  hire_dev::griddep_wait();
+  hire_dev::griddep_launch();
+  KTrace kt_(kKtLrT);
+  __shared__ float s_part[8][4];
+  const int q = blockIdx.x, b0 = blockIdx.y * 4;
+  const int nb = min(4, B - b0);
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const T* zr = z1 + static_cast<int64_t>(q) * d;
+  float acc[4] = {0.f, 0.f, 0.f, 0.f};
+  for (int ch = threadIdx.x; ch < d / 8; ch += 256) {
+    float zf[8];
+    if constexpr (sizeof(T) == 2) {
+      const uint4 u = *reinterpret_cast<const uint4*>(zr + 8 * ch);
+      zf[0] = bf16_lo(u.x); zf[1] = bf16_hi(u.x); zf[2] = bf16_lo(u.y); zf[3] = bf16_hi(u.y);
+      zf[4] = bf16_lo(u.z); zf[5] = bf16_hi(u.z); zf[6] = bf16_lo(u.w); zf[7] = bf16_hi(u.w);
+    } else {
+      const float4 u0 = *reinterpret_cast<const float4*>(zr + 8 * ch);
+      const float4 u1 = *reinterpret_cast<const float4*>(zr + 8 * ch + 4);
+      zf[0] = u0.x; zf[1] = u0.y; zf[2] = u0.z; zf[3] = u0.w;
+      zf[4] = u1.x; zf[5] = u1.y; zf[6] = u1.z; zf[7] = u1.w;
+    }
+#pragma unroll
+    for (int bb = 0; bb < 4; ++bb) {
+      if (bb < nb) {
+        const float* xb = x + static_cast<int64_t>(b0 + bb) * d + 8 * ch;
+        const float4 x0 = *reinterpret_cast<const float4*>(xb);
+        const float4 x1 = *reinterpret_cast<const float4*>(xb + 4);
+        acc[bb] = fmaf(zf[0], x0.x, acc[bb]); acc[bb] = fmaf(zf[1], x0.y, acc[bb]);
+        acc[bb] = fmaf(zf[2], x0.z, acc[bb]); acc[bb] = fmaf(zf[3], x0.w, acc[bb]);
+        acc[bb] = fmaf(zf[4], x1.x, acc[bb]); acc[bb] = fmaf(zf[5], x1.y, acc[bb]);
+        acc[bb] = fmaf(zf[6], x1.z, acc[bb]); acc[bb] = fmaf(zf[7], x1.w, acc[bb]);
+      }
+    }
+  }
+#pragma unroll
+  for (int bb = 0; bb < 4; ++bb) {
+    const float v = warp_sum_f32(acc[bb]);
+    if (lane == 0) s_part[wid][bb] = v;
+  }
+  __syncthreads();
+  if (threadIdx.x < nb) {
+    float v = 0.0f;
+#pragma unroll
+    for (int w8 = 0; w8 < 8; ++w8) v += s_part[w8][threadIdx.x];
+    t[static_cast<int64_t>(b0 + threadIdx.x) * r + q] = v;
+  }
+}
+
+// ---------------------------------------------------------------------
+// K2 step 2 on the tensor cores: s[b][j] = phi(sum_q Z2[j][q] t[b][q]).
+// mma.sync m16n8k16 bf16 -> fp32. t is split exactly into three bf16 terms
+// (hi + mid + lo carry its 24 bits); a bf16 Z2 operand is exact, an fp32 Z2
+// is split the same way and the six terms above 2^-24 relative are summed.
+// Every product is exact in fp32; only the accumulation order differs from
+// the sequential reference (fast mode, within tolerance).
+// The k order inside each 32-wide block is permuted consistently for A and
+// B so that one 16-byte load per row and block feeds two k-steps:
+// lane (g, c) holds row elements 8c..8c+7 of the block; k-step s takes
+// elements 4s, 4s+1 as logical k 2c, 2c+1 and 4s+2, 4s+3 as 2c+8, 2c+9.
+// One warp per 16-row tile (grid-stride), NTN n-tiles of 8 queries per pass.
+// ---------------------------------------------------------------------
+__device__ __forceinline__ void mma_bf16(float (&c)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3,
+                                         uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+      "{%0,%1,%2,%3};"
+      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+      : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+
+__device__ __forceinline__ void split3_bf16(float v, __nv_bfloat16* o) {
+  const __nv_bfloat16 h = __float2bfloat16_rn(v);
+  const float r1 = v - __bfloat162float(h);
+  const __nv_bfloat16 m = __float2bfloat16_rn(r1);
+  const float r2 = r1 - __bfloat162float(m);
+  o[0] = h;
+  o[1] = m;
+  o[2] = __float2bfloat16_rn(r2);
+}
+
+__device__ __forceinline__ uint32_t pack_bf16(__nv_bfloat16 lo, __nv_bfloat16 hi) {
+  return static_cast<uint32_t>(__bfloat16_as_ushort(lo)) | (static_cast<uint32_t>(__bfloat16_as_ushort(hi)) << 16);
+}
+
+constexpr int kLrThreads = 256;
+
+template <typename T, int R>
+struct LrTile {
+  static constexpr int KB = R / 32;
+  static constexpr int NL = sizeof(T) == 2 ? 1 : 2;  // 16-byte loads per row and k block
+  uint4 u[KB][2][NL];
+  __device__ __forceinline__ void load(const T* z2, int64_t rows, int64_t tile, int g, int c) {
+#pragma unroll
+    for (int kb = 0; kb < KB; ++kb)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int64_t rr = tile * 16 + g + 8 * h;
+#pragma unroll
+        for (int l = 0; l < NL; ++l)
+          u[kb][h][l] = rr < rows ? ldg_stream(z2 + rr * R + kb * 32 + 8 * c + 4 * l) : make_uint4(0, 0, 0, 0);
+      }
+  }
+};
+
+// NTN n-tiles (<= 8 * NTN queries of the batch, starting at query b0) per
+// launch; the B fragments of all (n-tile, k-step, split) live in registers
+// for the whole kernel, the NTN accumulator chains interleave.
+template <typename T, int R, int NTN>
+__global__ void __launch_bounds__(kLrThreads) lr_score_mma(
+    const T* __restrict__ z2, int64_t rows, const float* __restrict__ t, int B, int b0, int phi,
+    float* __restrict__ scores, int64_t score_stride) {
+  constexpr int KB = R / 32;                       // 32-wide k blocks
+  constexpr int NS = sizeof(T) == 2 ? 1 : 3;       // A splits
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int g = lane >> 2, c = lane & 3;
+  const int64_t tiles = (rows + 15) / 16;
+  const int64_t tstride = static_cast<int64_t>(gridDim.x) * (kLrThreads / 32);
+  int64_t tile = static_cast<int64_t>(blockIdx.x) * (kLrThreads / 32) + wid;
+  // Z2 is not produced by the previous kernel: start streaming the first
+  // tile before the programmatic-dependency wait
+  LrTile<T, R> cur;
+  if (tile < tiles) cur.load(z2, rows, tile, g, c);
+  hire_dev::griddep_wait();
+  hire_dev::griddep_launch();
+  KTrace kt_(kKtLrScore);
+  const int nb = min(B - b0, 8 * NTN);
+  // t split once per CTA into shared memory in fragment order:
+  // s_bf[nt][kb][s2][p][lane] = {pack(t[q][k0], t[q][k0+1]), pack(t[q][k0+2], t[q][k0+3])},
+  // q = 8 nt + g, k0 = kb*32 + 8c + 4 s2
+  __shared__ uint2 s_bf[NTN][KB][2][3][32];
+  for (int i = threadIdx.x; i < NTN * KB * 2 * 32; i += kLrThreads) {
+    const int ln = i & 31, s2 = (i >> 5) & 1, kb = (i >> 6) % KB, nt = (i >> 6) / KB;
+    const int q = 8 * nt + (ln >> 2);
+    const int k0 = kb * 32 + 8 * (ln & 3) + 4 * s2;
+    __nv_bfloat16 sp[4][3];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) split3_bf16(q < nb ? t[static_cast<int64_t>(b0 + q) * R + k0 + e] : 0.0f, sp[e]);
+#pragma unroll
+    for (int p = 0; p < 3; ++p)
+      s_bf[nt][kb][s2][p][ln] = make_uint2(pack_bf16(sp[0][p], sp[1][p]), pack_bf16(sp[2][p], sp[3][p]));
+  }
+  __syncthreads();
+  for (; tile < tiles; tile += tstride) {
+    LrTile<T, R> nxt;
+    if (tile + tstride < tiles) nxt.load(z2, rows, tile + tstride, g, c);  // next tile in flight
+    uint32_t a[KB][NS][2][4];  // [kb][split][row half][bf16 pairs]
+#pragma unroll
+    for (int kb = 0; kb < KB; ++kb) {
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        if constexpr (sizeof(T) == 2) {
+          const uint4 u = cur.u[kb][h][0];
+          a[kb][0][h][0] = u.x; a[kb][0][h][1] = u.y; a[kb][0][h][2] = u.z; a[kb][0][h][3] = u.w;
+        } else {
+          const uint4 u0 = cur.u[kb][h][0], u1 = cur.u[kb][h][NS > 1 ? 1 : 0];
+          const float e[8] = {__uint_as_float(u0.x), __uint_as_float(u0.y), __uint_as_float(u0.z),
+                              __uint_as_float(u0.w), __uint_as_float(u1.x), __uint_as_float(u1.y),
+                              __uint_as_float(u1.z), __uint_as_float(u1.w)};
+          __nv_bfloat16 sp[8][3];
+#pragma unroll
+          for (int q = 0; q < 8; ++q) split3_bf16(e[q], sp[q]);
+#pragma unroll
+          for (int p = 0; p < NS; ++p)
+#pragma unroll
+            for (int w = 0; w < 4; ++w) a[kb][p][h][w] = pack_bf16(sp[2 * w][p], sp[2 * w + 1][p]);
+        }
+      }
+    }
+    float acc[NTN][4];
+#pragma unroll
+    for (int nt = 0; nt < NTN; ++nt) acc[nt][0] = acc[nt][1] = acc[nt][2] = acc[nt][3] = 0.f;
+#pragma unroll
+    for (int kb = 0; kb < KB; ++kb)
+#pragma unroll
+      for (int s2 = 0; s2 < 2; ++s2)
+#pragma unroll
+        for (int pa = 0; pa < NS; ++pa)
+#pragma unroll
+          for (int pb = 0; pb < 3; ++pb) {
+            if (pa + pb > 2) continue;  // terms below 2^-24 relative
+#pragma unroll
+            for (int nt = 0; nt < NTN; ++nt) {
+              const uint2 bq = s_bf[nt][kb][s2][pb][lane];
+              mma_bf16(acc[nt], a[kb][pa][0][2 * s2], a[kb][pa][1][2 * s2], a[kb][pa][0][2 * s2 + 1],
+                       a[kb][pa][1][2 * s2 + 1], bq.x, bq.y);
+            }
+          }
+    const int64_t r0 = tile * 16 + g, r1 = r0 + 8;
+#pragma unroll
+    for (int nt = 0; nt < NTN; ++nt) {
+      const int q0 = nt * 8 + 2 * c;
+      float* o0 = scores + static_cast<int64_t>(b0 + q0) * score_stride;
+      if (q0 < nb) {
+        if (r0 < rows) o0[r0] = apply_phi(phi, acc[nt][0]);
+        if (r1 < rows) o0[r1] = apply_phi(phi, acc[nt][2]);
+      }
+      if (q0 + 1 < nb) {
+        if (r0 < rows) o0[score_stride + r0] = apply_phi(phi, acc[nt][1]);
+        if (r1 < rows) o0[score_stride + r1] = apply_phi(phi, acc[nt][3]);
+      }
+    }
+    cur = nxt;
+  }
+}
+
 // Generic-rank fallback (any r): same arithmetic, row streamed from memory.
 template <typename T, bool STRICT>
 __global__ void __launch_bounds__(128) lr_score_generic(

@@ -954,7 +954,8 @@ __global__ void __launch_bounds__(NT) final2_kernel(
   for (int v = 0; v < NT / 32; ++v) n_valid += rs.scan[v];
   __syncthreads();
   const int Kq = min(K, n_valid);
-  const uint64_t T = Kq >= 1 ? block_range_select<NT>(src, n_valid, Kq, &rs) : ~0ull;
+  // K >= pool: everything is selected (no order statistic needed)
+  const uint64_t T = Kq >= n_valid ? 1ull : (Kq >= 1 ? block_range_select<NT>(src, n_valid, Kq, &rs) : ~0ull);
   int c = 0;
 #pragma unroll
   for (int j = 0; j < KPT; ++j) c += (src.k[j] && src.k[j] >= T) ? 1 : 0;
