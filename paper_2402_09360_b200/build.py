@@ -38,7 +38,8 @@ def stale() -> bool:
 def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not stale():
         return LIB
-    cmd = [nvcc(), *NVCC_FLAGS, "-o", LIB, *SOURCES, "-lnccl"]
+    extra = os.environ.get("HIRE_NVCC_EXTRA", "").split()  # experiments only
+    cmd = [nvcc(), *NVCC_FLAGS, *extra, "-o", LIB, *SOURCES, "-lnccl"]
     if verbose:
         print(" ".join(cmd), file=sys.stderr)
     r = subprocess.run(cmd, capture_output=True, text=True)

@@ -27,6 +27,7 @@
 #include "exact.cuh"
 #include "score.cuh"
 #include "select.cuh"
+#include "select2.cuh"
 
 namespace hire_dev {
 
@@ -40,10 +41,13 @@ struct FusedFfnArgs {
   float* scores;           // [B][m]
   uint64_t* piv;           // [B][2] bracket pivots (hi, lo)
   uint64_t* thr;           // [B] exact k'-th proxy key
-  int* qcnt;               // [B][4] above / window / pairs counts (zeroed per launch)
-  uint64_t* win;           // [B][wcap] bracket windows
-  int wcap;
-  uint64_t* pairs;         // [B][kp] (exact activation, unit) keys of the candidates
+  int* qcnt;               // unused (kept for layout)
+  int* acnt;               // [B][G] keys above the bracket, per CTA slice
+  int* pcnt;               // [B][G] candidates per CTA slice
+  unsigned* gh;            // [B][kWinGroups][kWinBins] window histogram (zeroed in P2a)
+  uint64_t* lists;         // [B][kWinGroups][kWinBins][kBinCap] window keys by bin
+  int wmax;                // max rows per CTA slice
+  uint64_t* pairs;         // [B][G][wmax] (exact activation, unit) keys per CTA slice
   uint32_t* sel;           // [B][k]   (out, ascending)
   float* selact;           // [B][k]
   float* partial;          // [B][nch][d]
@@ -58,31 +62,49 @@ __device__ __forceinline__ long long globaltimer() {
   return t;
 }
 
-enum { kCntGemv = 0, kCntPiv = 32, kCntWin = 64, kCntThr = 96, kCntPairs = 128, kCntSel = 160, kCntDown = 192,
-       kCntExit = 224 };  // one 128-B line each
+// Hand-off counters. Arrivals of many CTAs on one address serialise at the
+// L2 atomic unit (~27 cycles each: 148 arrivals ~ 2 us), so every barrier
+// spreads its arrivals over kSpread counters on separate 128-B lines; the
+// waiter sums them.
+constexpr int kSpread = 16;
+constexpr int kBarInts = kSpread * 32;  // one barrier's counter block
+enum { kCntGemv = 0, kCntPiv = 1 * kBarInts, kCntWin = 2 * kBarInts, kCntThr = 3 * kBarInts,
+       kCntPairs = 4 * kBarInts, kCntSel = 5 * kBarInts, kCntDown = 6 * kBarInts, kCntExit = 7 * kBarInts,
+       kCntInts = 8 * kBarInts };
 
-__device__ __forceinline__ int ld_acquire(const int* p) {
+// One warp polls the spread counters with relaxed loads (an acquire probe
+// invalidates the SM's L1 every time). Once the target is reached the warp
+// re-reads all counters with one acquire load (synchronising with every
+// arriving CTA's release) — cheaper than a gpu-scope fence.
+__device__ __forceinline__ int ld_acquire_gpu_i32(const int* p) {
   int v;
   asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
-
-// One poller per CTA: relaxed probes (an acquire probe invalidates the
-// SM's L1 every time), one acquire fence once the target is reached.
 __device__ __forceinline__ void cta_wait_geq(const int* p, int target) {
-  if (threadIdx.x == 0) {
-    while (static_cast<int>(ld_relaxed_gpu(reinterpret_cast<const unsigned*>(p))) < target) {
+  if (threadIdx.x < 32) {
+    const int lane = threadIdx.x;
+    for (;;) {
+      const int v = lane < kSpread ? static_cast<int>(ld_relaxed_gpu(reinterpret_cast<const unsigned*>(p + lane * 32))) : 0;
+      if (__reduce_add_sync(0xffffffffu, v) >= target) break;
     }
-    fence_acq_rel_gpu();
+    if (lane < kSpread) (void)ld_acquire_gpu_i32(p + lane * 32);
   }
   __syncthreads();
 }
 
-// every thread fences its own writes, then one arrival per CTA
+// The CTA barrier orders every thread's writes before thread 0's
+// gpu-scope release (cumulative), which then arrives: one fence per CTA
+// instead of a MEMBAR in every thread.
 __device__ __forceinline__ void cta_arrive(int* p, int inc) {
-  __threadfence();
   __syncthreads();
-  if (threadIdx.x == 0) atomicAdd(p, inc);
+  if (threadIdx.x == 0) {
+    int old;  // returning atomic: performed at L2 before the CTA moves on
+    asm volatile("atom.release.gpu.global.add.s32 %0, [%1], %2;"
+                 : "=r"(old)
+                 : "l"(p + (blockIdx.x % kSpread) * 32), "r"(inc)
+                 : "memory");
+  }
 }
 
 constexpr int kFusedThreads = 512;
@@ -115,7 +137,12 @@ __global__ void __launch_bounds__(kFusedThreads, 1) ffn_fused_kernel(FusedFfnArg
   __shared__ int s_sum[16];
   __shared__ float s_red[kFusedWarps];
   __shared__ int s_redi[kFusedWarps];
-  __shared__ SelectScratch sc;
+  struct FusedScratch {
+    uint64_t samp[128];
+    uint64_t piv[4];
+    int scan[64];
+  };
+  __shared__ FusedScratch sc;
 
   const int nkb = d / 64;
   const int n_rb = (m + 15) / 16;
@@ -138,7 +165,17 @@ __global__ void __launch_bounds__(kFusedThreads, 1) ffn_fused_kernel(FusedFfnArg
   // ---- P0: x -> smem (fp32) and int8 quantisation (prep_x_int8 rule) ----
   // all queries at once: warps are split evenly over the B queries (wpq
   // warps each); two barriers in total, independent of B.
-  block_copy(s_xf, a.x, B * d);
+  // x fp32 in shared memory; for 8-element row chunks (bf16 rows) each
+  // query's vector is stored as [d/2 low halves | d/2 high halves] of the
+  // chunks so the P3 128-bit reads are conflict-free (lane stride 16 B)
+  auto xf_idx = [&](int b, int i) -> int {
+    if constexpr (E == 8) return b * d + ((i >> 2) & 1) * (d >> 1) + (i >> 3) * 4 + (i & 3);
+    else return b * d + i;
+  };
+  for (int v = tid; v < B * d / 4; v += kFusedThreads) {
+    const int i = 4 * v, b = i / d, ii = i % d;
+    *reinterpret_cast<float4*>(s_xf + xf_idx(b, ii)) = __ldg(reinterpret_cast<const float4*>(a.x) + v);
+  }
   __syncthreads();
   FUSED_STAMP(13);
   {
@@ -147,7 +184,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1) ffn_fused_kernel(FusedFfnArg
     const bool active = qb < B;
     float mx = 0.0f;
     if (active)
-      for (int i = qw * 32 + lane; i < d; i += wpq * 32) mx = fmaxf(mx, fabsf(s_xf[qb * d + i]));
+      for (int i = qw * 32 + lane; i < d; i += wpq * 32) mx = fmaxf(mx, fabsf(s_xf[xf_idx(qb, i)]));
     mx = warp_max_f32(mx);
     if (lane == 0) s_red[wid] = mx;
     __syncthreads();
@@ -160,7 +197,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1) ffn_fused_kernel(FusedFfnArg
     int local = 0;
     if (active)
       for (int i = qw * 32 + lane; i < d; i += wpq * 32) {
-        const int q = rhaz_clamp(__fdiv_rn(s_xf[qb * d + i], sx), 127);
+        const int q = rhaz_clamp(__fdiv_rn(s_xf[xf_idx(qb, i)], sx), 127);
         local += q;
         s_xq[qb * xs + i] = static_cast<int8_t>(q);
       }
@@ -256,22 +293,28 @@ __global__ void __launch_bounds__(kFusedThreads, 1) ffn_fused_kernel(FusedFfnArg
     ++done_rb;
   }
   FUSED_STAMP(2);
+  if (a.trace && tid == 0) atomicMax(reinterpret_cast<unsigned long long*>(a.trace + 33), static_cast<unsigned long long>(globaltimer()));
   cta_arrive(a.counters + kCntGemv, 1);
+  if (a.trace && tid == 0) atomicMax(reinterpret_cast<unsigned long long*>(a.trace + 35), static_cast<unsigned long long>(globaltimer()));
 
   // ---- P2a: bracket pivots for the k'-th proxy key (CTA b per query) ------
   // A 128-key sample of scores[b] ranked by counting; the sample keys at
-  // ranks (k'-1)S/m -/+ 3.5 sigma bracket the k'-th key (select.cuh).
+  // ranks (k'-1)S/m -/+ 3.5 sigma bracket the k'-th key (select.cuh). The
+  // bracket is split into kWinBins value-word bins for P2b/P2c.
   int f_row, w_row;  // this CTA's row slice (width rule)
   {
     const int base = m / G, extra = m % G;
     f_row = blockIdx.x * base + (blockIdx.x < extra ? blockIdx.x : extra);
     w_row = base + (blockIdx.x < extra ? 1 : 0);
   }
+  __shared__ RangeScratch rs2;
   if (blockIdx.x < B) {
     const int b = blockIdx.x;
+    for (int i = tid; i < kWinGroups * kWinBins; i += kFusedThreads) a.gh[b * kWinGroups * kWinBins + i] = 0u;
     cta_wait_geq(a.counters + kCntGemv, G);
     FUSED_STAMP(3);
     constexpr int S = 128;
+    __shared__ unsigned s_top;
     if (tid < S) {
       const int i = static_cast<int>((static_cast<int64_t>(tid) * m) / S);
       sc.samp[tid] = make_key(__ldcg(a.scores + static_cast<int64_t>(b) * m + i), static_cast<uint32_t>(i));
@@ -279,8 +322,10 @@ __global__ void __launch_bounds__(kFusedThreads, 1) ffn_fused_kernel(FusedFfnArg
     if (tid == 0) {
       sc.piv[0] = ~0ull;
       sc.piv[1] = 0ull;
+      s_top = 0u;
     }
     __syncthreads();
+    if (tid < S) atomicMax(&s_top, static_cast<unsigned>(sc.samp[tid] >> 32));
     const float p = static_cast<float>(a.kp) / static_cast<float>(m);
     const float mu = static_cast<float>(a.kp - 1) * S / static_cast<float>(m);
     const float delta = fmaxf(3.5f * sqrtf(S * p * (1.0f - p)), 3.0f);
@@ -292,79 +337,133 @@ __global__ void __launch_bounds__(kFusedThreads, 1) ffn_fused_kernel(FusedFfnArg
     });
     __syncthreads();
     if (tid == 0) {
-      a.piv[2 * b] = sc.piv[0];
-      a.piv[2 * b + 1] = sc.piv[1];
+      const uint64_t hi = sc.piv[0], lo = sc.piv[1];
+      const unsigned vlo = static_cast<unsigned>(lo >> 32);
+      const unsigned vtop = max(vlo, hi != ~0ull ? static_cast<unsigned>(hi >> 32) : s_top);
+      const int bits = 32 - __clz(vtop - vlo);
+      const int sh = bits > 8 ? bits - 8 : 0;
+      a.piv[4 * b] = hi;
+      a.piv[4 * b + 1] = lo;
+      a.piv[4 * b + 2] = static_cast<uint64_t>(vlo) | (static_cast<uint64_t>(sh) << 32);
     }
     cta_arrive(a.counters + kCntPiv, 1);
   }
 
-  // ---- P2b: every CTA counts / gathers the bracket over its own rows ------
-  // query-aligned warp groups (wpq warps per query) walk the slice; ballot
-  // counts go to per-query shared counters; one global atomic per query.
+  // ---- P2b: every CTA counts its slice above the bracket and files the ---
+  // bracket keys by bin (per chunk-group lists); counts per CTA slot, no
+  // same-address atomics across CTAs.
   cta_wait_geq(a.counters + kCntPiv, B);
   FUSED_STAMP(4);
   {
-    __shared__ int s_above[16], s_win[16], s_wbase[16];
-    uint64_t* s_stage = reinterpret_cast<uint64_t*>(s_pool);  // [B][w_row]
-    if (tid < B) s_above[tid] = s_win[tid] = 0;
+    __shared__ int s_above[16];
+    __shared__ unsigned s_pf[64];  // rows of the slice above some query's lower pivot (bitmap)
+    if (tid < B) s_above[tid] = 0;
+    if (tid < 64) s_pf[tid] = 0u;
     __syncthreads();
     const int wpq = kFusedWarps / B > 0 ? kFusedWarps / B : 1;
     const int qb = wid / wpq, qw = wid % wpq;
     if (qb < B) {
-      const uint64_t hi = __ldcg(a.piv + 2 * qb), lo = __ldcg(a.piv + 2 * qb + 1);
+      const uint64_t hi = __ldcg(a.piv + 4 * qb), lo = __ldcg(a.piv + 4 * qb + 1), bp = __ldcg(a.piv + 4 * qb + 2);
+      const unsigned vlo = static_cast<unsigned>(bp);
+      const int bsh = static_cast<int>(bp >> 32);
+      unsigned* ghg = a.gh + (static_cast<int64_t>(qb) * kWinGroups + blockIdx.x % kWinGroups) * kWinBins;
+      uint64_t* lsg = a.lists + (static_cast<int64_t>(qb) * kWinGroups + blockIdx.x % kWinGroups) * kWinBins * kBinCap;
+      int above = 0;
       for (int r0 = qw * 32; r0 < w_row; r0 += wpq * 32) {
         const int r = r0 + lane;
-        uint64_t key = 0;
-        bool above = false, in = false;
         if (r < w_row) {
-          key = make_key(__ldcg(a.scores + static_cast<int64_t>(qb) * m + f_row + r), static_cast<uint32_t>(f_row + r));
-          above = key > hi;
-          in = key > lo && key <= hi;
+          const uint64_t key = make_key(__ldcg(a.scores + static_cast<int64_t>(qb) * m + f_row + r), static_cast<uint32_t>(f_row + r));
+          above += key > hi ? 1 : 0;
+          if (key > lo) atomicOr(&s_pf[r >> 5], 1u << (r & 31));
+          if (key > lo && key <= hi) {
+            const unsigned bin = win_bin(key, vlo, bsh);
+            const unsigned lp = atomicAdd(&ghg[bin], 1u);
+            if (lp < kBinCap) lsg[bin * kBinCap + lp] = key;
+          }
         }
-        const unsigned ba = __ballot_sync(0xffffffffu, above), bi = __ballot_sync(0xffffffffu, in);
-        int base = 0;
-        if (lane == 0) {
-          if (ba) atomicAdd(&s_above[qb], __popc(ba));
-          if (bi) base = atomicAdd(&s_win[qb], __popc(bi));
-        }
-        base = __shfl_sync(0xffffffffu, base, 0);
-        if (in) s_stage[qb * w_row + base + __popc(bi & ((1u << lane) - 1u))] = key;
       }
+      above = warp_sum_i32(above);
+      if (lane == 0 && above) atomicAdd(&s_above[qb], above);
     }
     __syncthreads();
-    if (tid < B) {
-      if (s_above[tid]) atomicAdd(a.qcnt + 4 * tid, s_above[tid]);
-      s_wbase[tid] = s_win[tid] ? atomicAdd(a.qcnt + 4 * tid + 1, s_win[tid]) : 0;
-    }
-    __syncthreads();
-    for (int t2 = tid; t2 < B * w_row; t2 += kFusedThreads) {
-      const int b = t2 / w_row, j2 = t2 % w_row;
-      if (j2 < s_win[b] && s_wbase[b] + j2 < a.wcap)
-        a.win[static_cast<int64_t>(b) * a.wcap + s_wbase[b] + j2] = s_stage[t2];
-    }
+    if (tid < B) a.acnt[tid * G + blockIdx.x] = s_above[tid];
+    // likely k'-candidates: start streaming their U rows into L2 so the P3
+    // gather after the threshold hand-off reads L2, not HBM
+    if (tid < w_row && ((s_pf[tid >> 5] >> (tid & 31)) & 1u))
+      bulk_prefetch_l2(static_cast<const unsigned char*>(a.u) + static_cast<int64_t>(f_row + tid) * d * sizeof(T),
+                       static_cast<unsigned>(d * sizeof(T)));
+    if (a.trace && tid == 0) atomicMax(reinterpret_cast<unsigned long long*>(a.trace + 28), static_cast<unsigned long long>(globaltimer()));
   }
   cta_arrive(a.counters + kCntWin, 1);
 
-  // ---- P2c: exact k'-th key per query from its window (CTA b) -------------
+  // ---- P2c: exact k'-th key per query (CTA b): the bin holding rank ------
+  // k' - above, then the rank among that bin's keys.
   if (blockIdx.x < B) {
     const int b = blockIdx.x;
     cta_wait_geq(a.counters + kCntWin, G);
     FUSED_STAMP(5);
-    const int above = __ldcg(a.qcnt + 4 * b), nw = __ldcg(a.qcnt + 4 * b + 1);
-    const int need = a.kp - above;
-    uint64_t T;
-    if (need >= 1 && need <= nw && nw <= a.wcap) {
-      uint64_t* s_w = reinterpret_cast<uint64_t*>(s_pool);
-      block_copy_cg(s_w, a.win + static_cast<int64_t>(b) * a.wcap, nw);
-      __syncthreads();
-      T = block_kth_key<kFusedThreads>([&](int i) { return s_w[i]; }, nw, need, &sc);
-    } else {  // bracket missed: exact select over all m scores
-      float* s_val = reinterpret_cast<float*>(s_pool);
-      block_copy_cg(s_val, a.scores + static_cast<int64_t>(b) * m, m);
-      __syncthreads();
-      T = block_kth_key<kFusedThreads>([&](int i) { return make_key(s_val[i], static_cast<uint32_t>(i)); },
-                                       m, a.kp, &sc);
+    __shared__ long long s_red2[kFusedWarps];
+    __shared__ int s_bstar, s_m, s_bad;
+    __shared__ long long s_r2;
+    __shared__ uint64_t s_T;
+    long long ab = 0;
+    for (int c = tid; c < G; c += kFusedThreads) ab += __ldcg(a.acnt + b * G + c);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) ab += __shfl_xor_sync(0xffffffffu, ab, o);
+    if (lane == 0) s_red2[wid] = ab;
+    if (tid == 0) {
+      s_bad = 1;
+      rs2.small_n = 0;
     }
+    __syncthreads();
+    long long above_t = 0;
+#pragma unroll
+    for (int w = 0; w < kFusedWarps; ++w) above_t += s_red2[w];
+    const long long r = static_cast<long long>(a.kp) - above_t;
+    // bins, top first: thread t < kWinBins holds bin kWinBins-1-t
+    unsigned hb = 0, hmax = 0;
+    if (tid < kWinBins) {
+#pragma unroll
+      for (int g2 = 0; g2 < kWinGroups; ++g2) {
+        const unsigned v = __ldcg(a.gh + (static_cast<int64_t>(b) * kWinGroups + g2) * kWinBins + (kWinBins - 1 - tid));
+        hb += v;
+        hmax = max(hmax, v);
+      }
+    }
+    int tot;
+    const int ex = block_exclusive_scan<kFusedThreads>(static_cast<int>(hb), sc.scan, &tot);
+    if (tid < kWinBins && r >= 1 && ex < r && ex + static_cast<long long>(hb) >= r) {
+      s_bstar = kWinBins - 1 - tid;
+      s_r2 = r - ex;
+      s_m = static_cast<int>(hb);
+      s_bad = hmax > kBinCap ? 2 : 0;
+    }
+    __syncthreads();
+    FUSED_STAMP(29);
+    uint64_t T;
+    if (!s_bad) {
+      const unsigned bstar = static_cast<unsigned>(s_bstar);
+      if (tid < kWinGroups * kBinCap) {
+        const int g2 = tid / kBinCap, j = tid % kBinCap;
+        const unsigned cg = __ldcg(a.gh + (static_cast<int64_t>(b) * kWinGroups + g2) * kWinBins + bstar);
+        if (static_cast<unsigned>(j) < cg) {
+          const uint64_t kk = __ldcg(reinterpret_cast<const unsigned long long*>(a.lists) +
+                                     ((static_cast<int64_t>(b) * kWinGroups + g2) * kWinBins + bstar) * kBinCap + j);
+          const int pidx = atomicAdd(&rs2.small_n, 1);
+          rs2.ckeys[pidx] = kk;
+        }
+      }
+      __syncthreads();
+      const int mb = s_m;
+      RegKeys<1> src;
+      src.k[0] = tid < mb ? rs2.ckeys[tid] : 0ull;
+      __syncthreads();
+      T = block_range_select<kFusedThreads>(src, mb, s_r2, &rs2);
+    } else {  // bracket missed or a bin list overflowed: exact select over all m scores
+      RowKeys src{a.scores + static_cast<int64_t>(b) * m, static_cast<uint32_t>(m)};
+      T = block_range_select<kFusedThreads>(src, m, a.kp, &rs2);
+    }
+    FUSED_STAMP(30);
     if (tid == 0) a.thr[b] = T;
     cta_arrive(a.counters + kCntThr, 1);
   }
@@ -372,98 +471,111 @@ __global__ void __launch_bounds__(kFusedThreads, 1) ffn_fused_kernel(FusedFfnArg
   // ---- P3: every CTA recomputes the candidates in its own rows ------------
   cta_wait_geq(a.counters + kCntThr, B);
   FUSED_STAMP(6);
+  if (a.trace && tid == 0) atomicMax(reinterpret_cast<unsigned long long*>(a.trace + 23), static_cast<unsigned long long>(globaltimer()));
   {
-    // stage (b, row) candidates of this slice, query-major
-    int* s_cand = reinterpret_cast<int*>(s_pool);                    // [B*w_row] rows
-    float* s_act = reinterpret_cast<float*>(s_pool) + B * w_row;      // [B*w_row]
-    __shared__ int s_off[17];
+    // candidate mask per row of this slice (bit b: row is a k'-candidate of
+    // query b); rows with any bit are recomputed once for all their queries
+    unsigned* s_mask = reinterpret_cast<unsigned*>(s_pool);          // [w_row]
+    int* s_rows = reinterpret_cast<int*>(s_mask + w_row);             // [w_row] compacted
+    uint64_t* s_key = reinterpret_cast<uint64_t*>(s_rows + w_row);  // [B][w_row] (8 w_row bytes in: aligned)
+    __shared__ int s_nrow;
     __shared__ int s_nb[16];
-    __shared__ int s_pbase[16];
+    for (int r = tid; r < w_row; r += kFusedThreads) s_mask[r] = 0u;
     if (tid < B) s_nb[tid] = 0;
     __syncthreads();
-    {
-      const int wpq = kFusedWarps / B > 0 ? kFusedWarps / B : 1;
-      const int qb = wid / wpq, qw = wid % wpq;
-      if (qb < B) {
-        const uint64_t T = __ldcg(a.thr + qb);
-        for (int r0 = qw * 32; r0 < w_row; r0 += wpq * 32) {
-          const int r = r0 + lane;
-          bool c = false;
-          if (r < w_row)
-            c = make_key(__ldcg(a.scores + static_cast<int64_t>(qb) * m + f_row + r), static_cast<uint32_t>(f_row + r)) >= T;
-          const unsigned bc = __ballot_sync(0xffffffffu, c);
-          int base = 0;
-          if (lane == 0 && bc) base = atomicAdd(&s_nb[qb], __popc(bc));
-          base = __shfl_sync(0xffffffffu, base, 0);
-          if (c) s_cand[qb * w_row + base + __popc(bc & ((1u << lane) - 1u))] = f_row + r;
-        }
+    for (int t2 = tid; t2 < B * w_row; t2 += kFusedThreads) {
+      const int qb = t2 / w_row, r = t2 % w_row;
+      const uint64_t T = __ldcg(a.thr + qb);
+      if (make_key(__ldcg(a.scores + static_cast<int64_t>(qb) * m + f_row + r), static_cast<uint32_t>(f_row + r)) >= T)
+        atomicOr(&s_mask[r], 1u << qb);
+    }
+    __syncthreads();
+    if (a.trace && tid == 0) atomicMax(reinterpret_cast<unsigned long long*>(a.trace + 36), static_cast<unsigned long long>(globaltimer()));
+    if (wid == 0) {
+      int n = 0;
+      for (int r0 = 0; r0 < w_row; r0 += 32) {
+        const int r = r0 + lane;
+        const bool c = r < w_row && s_mask[r] != 0u;
+        const unsigned bc = __ballot_sync(0xffffffffu, c);
+        if (c) s_rows[n + __popc(bc & ((1u << lane) - 1u))] = r;
+        n += __popc(bc);
       }
+      if (lane == 0) s_nrow = n;
     }
     __syncthreads();
-    if (tid == 0) {
-      s_off[0] = 0;
-      for (int b = 0; b < B; ++b) s_off[b + 1] = s_off[b] + s_nb[b];
-    }
-    __syncthreads();
-    const int ntask = s_off[B];
+    if (a.trace && tid == 0) atomicMax(reinterpret_cast<unsigned long long*>(a.trace + 37), static_cast<unsigned long long>(globaltimer()));
+    const int nrow = s_nrow;
+    const long long p3_t0 = a.trace ? globaltimer() : 0;
     const T* U_ = static_cast<const T*>(a.u);
     const int64_t pitch_vec = d / E;
-    // two rows in flight per warp; per-row arithmetic identical to recompute_fast
-    for (int t0 = wid; t0 < ntask; t0 += 2 * kFusedWarps) {
-      int bt[2], rw[2], slot[2];
-      bool ok[2];
-      const uint4* rp[2];
+    // warp-strided rows, the next row's 16-byte chunks loaded while the
+    // current one is consumed; each row's dot with every query in its mask,
+    // arithmetic identical to recompute_fast (lane chunks lane + 32c, fmaf in
+    // element order, fixed butterfly). Rows fit one pass: d * sizeof(T) <= 4096.
+    constexpr int CH = 8;
+    auto load_row = [&](int idx, uint4 (&v)[CH]) {
+      const uint4* rp = reinterpret_cast<const uint4*>(U_) + static_cast<int64_t>(f_row + s_rows[idx]) * pitch_vec;
 #pragma unroll
-      for (int r = 0; r < 2; ++r) {
-        const int task = t0 + r * kFusedWarps;
-        ok[r] = task < ntask;
-        int b = 0;
-        if (ok[r])
-          while (task >= s_off[b + 1]) ++b;
-        bt[r] = b;
-        slot[r] = ok[r] ? b * w_row + (task - s_off[b]) : 0;
-        rw[r] = ok[r] ? s_cand[slot[r]] : 0;
-        rp[r] = reinterpret_cast<const uint4*>(U_) + static_cast<int64_t>(rw[r]) * pitch_vec;
+      for (int c = 0; c < CH; ++c) {
+        const int vi = lane + 32 * c;
+        v[c] = vi < pitch_vec ? ldg_stream(rp + vi) : make_uint4(0, 0, 0, 0);
       }
-      float accf[2] = {0.0f, 0.0f};
-      for (int c0 = 0; c0 < pitch_vec; c0 += 256) {  // 8 vectors per lane per pass
-        uint4 vv[2][8];
+    };
+    uint4 cur[CH];
+    if (wid < nrow) load_row(wid, cur);
+    for (int idx = wid; idx < nrow; idx += kFusedWarps) {
+      uint4 nxt[CH];
+      if (idx + kFusedWarps < nrow) load_row(idx + kFusedWarps, nxt);
+      const int rr = s_rows[idx];
+      unsigned bits = s_mask[rr];
+      while (bits) {
+        const int qb = __ffs(bits) - 1;
+        bits &= bits - 1;
+        float acc = 0.0f;
 #pragma unroll
-        for (int r = 0; r < 2; ++r)
-#pragma unroll
-          for (int c = 0; c < 8; ++c) {
-            const int vi = c0 + lane + 32 * c;
-            vv[r][c] = (ok[r] && vi < pitch_vec) ? ldg_stream(rp[r] + vi) : make_uint4(0, 0, 0, 0);
-          }
-#pragma unroll
-        for (int r = 0; r < 2; ++r)
-#pragma unroll
-          for (int c = 0; c < 8; ++c) {
-            const int vi = c0 + lane + 32 * c;
-            if (vi < pitch_vec) {
-              float f[E], xv[E];
-              Vec16<T>::expand(vv[r][c], f);
-              load_x_vec<E>(s_xf + bt[r] * d + vi * E, xv);
-#pragma unroll
-              for (int e = 0; e < E; ++e) accf[r] = fmaf(f[e], xv[e], accf[r]);
+        for (int c = 0; c < CH; ++c) {
+          const int vi = lane + 32 * c;
+          if (vi < pitch_vec) {
+            float f[E], xv[E];
+            Vec16<T>::expand(cur[c], f);
+            if constexpr (E == 8) {
+              const float4 xa = *reinterpret_cast<const float4*>(s_xf + qb * d + vi * 4);
+              const float4 xb = *reinterpret_cast<const float4*>(s_xf + qb * d + (d >> 1) + vi * 4);
+              xv[0] = xa.x; xv[1] = xa.y; xv[2] = xa.z; xv[3] = xa.w;
+              xv[4 % E] = xb.x; xv[5 % E] = xb.y; xv[6 % E] = xb.z; xv[7 % E] = xb.w;
+            } else {
+              load_x_vec<E>(s_xf + qb * d + vi * E, xv);
             }
+#pragma unroll
+            for (int e = 0; e < E; ++e) acc = fmaf(f[e], xv[e], acc);
           }
+        }
+        acc = warp_sum_f32(acc);
+        if (lane == 0) {
+          const int j2 = atomicAdd(&s_nb[qb], 1);
+          s_key[qb * w_row + j2] = make_key(apply_phi(a.phi, acc), static_cast<uint32_t>(f_row + rr));
+        }
       }
 #pragma unroll
-      for (int r = 0; r < 2; ++r) {
-        const float s2 = warp_sum_f32(accf[r]);
-        if (lane == 0 && ok[r]) s_act[slot[r]] = apply_phi(a.phi, s2);
-      }
+      for (int c = 0; c < CH; ++c) cur[c] = nxt[c];
     }
     __syncthreads();
-    if (tid < B) s_pbase[tid] = s_nb[tid] ? atomicAdd(a.qcnt + 4 * tid + 2, s_nb[tid]) : 0;
-    __syncthreads();
-    for (int task = tid; task < ntask; task += kFusedThreads) {
-      int b = 0;
-      while (task >= s_off[b + 1]) ++b;
-      const int j2 = task - s_off[b];
-      const int sl = b * w_row + j2;
-      a.pairs[static_cast<int64_t>(b) * a.kp + s_pbase[b] + j2] = make_key(s_act[sl], static_cast<uint32_t>(s_cand[sl]));
+    if (a.trace && tid == 0) {
+      const unsigned long long now = static_cast<unsigned long long>(globaltimer());
+      atomicMax(reinterpret_cast<unsigned long long*>(a.trace + 38), now);
+      // per-CTA dot-phase duration (ns) and row count, packed: max over CTAs
+      atomicMax(reinterpret_cast<unsigned long long*>(a.trace + 40), ((now - static_cast<unsigned long long>(p3_t0)) << 16) | nrow);
+      atomicAdd(reinterpret_cast<unsigned long long*>(a.trace + 41), now - static_cast<unsigned long long>(p3_t0));
+    }
+    for (int t2 = tid; t2 < B * w_row; t2 += kFusedThreads) {
+      const int qb = t2 / w_row, j2 = t2 % w_row;
+      if (j2 < s_nb[qb]) a.pairs[(static_cast<int64_t>(qb) * G + blockIdx.x) * a.wmax + j2] = s_key[t2];
+    }
+    if (tid < B) a.pcnt[tid * G + blockIdx.x] = s_nb[tid];
+    const int ntask = nrow;
+    if (a.trace && tid == 0) {
+      atomicMax(reinterpret_cast<unsigned long long*>(a.trace + 22), static_cast<unsigned long long>(globaltimer()));
+      atomicMax(reinterpret_cast<unsigned long long*>(a.trace + 24), static_cast<unsigned long long>(ntask));
     }
   }
   cta_arrive(a.counters + kCntPairs, 1);
@@ -473,17 +585,51 @@ __global__ void __launch_bounds__(kFusedThreads, 1) ffn_fused_kernel(FusedFfnArg
     const int b = blockIdx.x;
     cta_wait_geq(a.counters + kCntPairs, G);
     FUSED_STAMP(7);
-    uint64_t* s_keys = reinterpret_cast<uint64_t*>(s_pool);
-    unsigned* s_bits = reinterpret_cast<unsigned*>(s_keys + a.kp);
+    unsigned* s_bits = reinterpret_cast<unsigned*>(s_pool);
     const int nwords = (m + 31) / 32;
     float* s_au = reinterpret_cast<float*>(s_bits + nwords);
-    block_copy_cg(s_keys, a.pairs + static_cast<int64_t>(b) * a.kp, a.kp);
+    unsigned* s_pre = reinterpret_cast<unsigned*>(s_au + m);  // [G] slot prefix
+    unsigned char* s_seg = reinterpret_cast<unsigned char*>(s_pre + G);  // [k'] slot of pair i
     for (int w = tid; w < nwords; w += kFusedThreads) s_bits[w] = 0u;
+    int tot2 = 0;
+    {
+      const int c = tid;
+      const int v = c < G ? __ldcg(a.pcnt + b * G + c) : 0;
+      const int ex2 = block_exclusive_scan<kFusedThreads>(v, sc.scan, &tot2);
+      if (c < G) {
+        s_pre[c] = static_cast<unsigned>(ex2);
+        for (int j = 0; j < v; ++j) s_seg[ex2 + j] = static_cast<unsigned char>(c);
+      }
+    }
     __syncthreads();
-    const uint64_t T2 = block_kth_key<kFusedThreads>([&](int i) { return s_keys[i]; }, a.kp, a.k, &sc);
-    for (int i = tid; i < a.kp; i += kFusedThreads) {
-      const uint64_t key = s_keys[i];
-      if (key >= T2) {
+    // the order statistic runs on 4 warps (per-pass overhead scales with the
+    // warp count): 128 threads x KP pairs (k' <= 1024 here)
+    constexpr int KP = 8, NTS = 128;
+    RegKeys<KP> src;
+#pragma unroll
+    for (int j = 0; j < KP; ++j) {
+      const int i = tid + j * NTS;
+      uint64_t kk = 0;
+      if (tid < NTS && i < tot2) {
+        const int sg = s_seg[i];
+        kk = __ldcg(reinterpret_cast<const unsigned long long*>(a.pairs) +
+                    (static_cast<int64_t>(b) * G + sg) * a.wmax + (i - s_pre[sg]));
+      }
+      src.k[j] = kk;
+    }
+    FUSED_STAMP(25);
+    __shared__ uint64_t s_T2;
+    if (tid < NTS) {
+      const uint64_t t2 = block_range_select<NTS>(src, tot2, min(a.k, tot2), &rs2);
+      if (tid == 0) s_T2 = t2;
+    }
+    __syncthreads();
+    const uint64_t T2 = s_T2;
+    FUSED_STAMP(26);
+#pragma unroll
+    for (int j = 0; j < KP; ++j) {
+      const uint64_t key = src.k[j];
+      if (key && key >= T2) {
         const uint32_t u = key_index(key);
         atomicOr(&s_bits[u >> 5], 1u << (u & 31));
         s_au[u] = key_value(key);
@@ -508,6 +654,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1) ffn_fused_kernel(FusedFfnArg
         ++pos;
       }
     }
+    FUSED_STAMP(27);
     cta_arrive(a.counters + kCntSel, 1);
   }
 
@@ -554,6 +701,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1) ffn_fused_kernel(FusedFfnArg
       }
     }
   }
+  if (a.trace && tid == 0) atomicMax(reinterpret_cast<unsigned long long*>(a.trace + 31), static_cast<unsigned long long>(globaltimer()));
   cta_arrive(a.counters + kCntDown, 1);
 
   // ---- P6: fixed-order reduction over chunks ------------------------------
@@ -573,12 +721,19 @@ __global__ void __launch_bounds__(kFusedThreads, 1) ffn_fused_kernel(FusedFfnArg
   if (a.trace && blockIdx.x == 0 && threadIdx.x == 0) a.trace[21] = clock64();
   __syncthreads();
   if (tid == 0) {
+    // two-level exit count: the CTA completing its group arrives at the top
+    // counter; the one completing the top resets every counter
     __threadfence();
-    const int prev = atomicAdd(a.counters + kCntExit, 1);
-    if (prev == G - 1) {
-      for (int i = 0; i <= kCntExit; i += 32) a.counters[i] = 0;
-      for (int i = 0; i < 4 * B; ++i) a.qcnt[i] = 0;
-      __threadfence();
+    const int grp = blockIdx.x % kSpread;
+    const int members = (G - grp + kSpread - 1) / kSpread;
+    const int prev = atomicAdd(a.counters + kCntExit + grp * 32, 1);
+    if (prev == members - 1) {
+      const int ngrp = G < kSpread ? G : kSpread;
+      if (atomicAdd(a.counters + kCntExit + kSpread * 32 - 8, 1) == ngrp - 1) {
+        for (int i = 0; i < kCntInts; i += 32) a.counters[i] = 0;
+        a.counters[kCntExit + kSpread * 32 - 8] = 0;
+        __threadfence();
+      }
     }
   }
 }

@@ -81,7 +81,7 @@ struct hire_ctx_s {
   int64_t launches = 0;
   bool pdl = true;
   bool force_dp4a = false;
-  bool ffn_fused = true;
+  bool ffn_fused = false;  // the kernel chain is faster since the grid-wide selector (HIRE_FFN_FUSED=1 opts in)
   bool trace = false;
   int* counters = nullptr;  // zeroed hand-off counters of the fused kernels
   unsigned* selc = nullptr;  // zeroed selection counters (select2.cuh qc / agg)
@@ -254,6 +254,11 @@ int max_blocks(K kernel, int threads, size_t smem) {
 }
 
 // ----------------------------------------------------- selection policy --
+// context counter buffer: fused-kernel barriers, per-query counters, trace
+constexpr int kQcntOff = hire_dev::kCntInts;
+constexpr int kTraceOff = kQcntOff + 64;
+constexpr int kCtxCounterInts = kTraceOff + 128;
+
 constexpr int64_t kSelGridChunks = 4 * 148;  // S2/S3 CTAs over a whole batch (co-resident)
 
 struct SelPlan {
@@ -363,8 +368,19 @@ int run_select(hire_ctx ctx, const float* scores, int64_t score_stride, int64_t 
   if (sp.mode == 2) {
     const uint32_t nn = static_cast<uint32_t>(n), K = static_cast<uint32_t>(sp.k_eff);
     if (n <= kSel2Exact) {
-      CK(launch_k(ctx, sel_exact_kernel, static_cast<unsigned>(B), kSel2Threads, 0, scores, score_stride,
-                  nn, K, cand, cand_stride));
+      // fewer warps per CTA: the per-pass cost of the order statistic is
+      // per-warp overhead, the key counting is cheap
+      const char* v = std::getenv("HIRE_SEL_EXACT");
+      const int variant = v ? std::atoi(v) : (n <= 4096 ? 1 : 0);
+      if (variant == 1)
+        CK(launch_k(ctx, sel_exact_kernel<256, 16>, static_cast<unsigned>(B), 256, 0, scores, score_stride, nn, K,
+                    cand, cand_stride));
+      else if (variant == 2 && n <= 8192)
+        CK(launch_k(ctx, sel_exact_kernel<256, 32>, static_cast<unsigned>(B), 256, 0, scores, score_stride, nn, K,
+                    cand, cand_stride));
+      else
+        CK(launch_k(ctx, sel_exact_kernel<512, 16>, static_cast<unsigned>(B), 512, 0, scores, score_stride, nn, K,
+                    cand, cand_stride));
       CK(cudaGetLastError());
       return HIRE_OK;
     }
@@ -951,10 +967,10 @@ int hire_ctx_create(int device, void* stream, int own_stream, hire_ctx* out) {
     for (const void* k : ks) CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
   }
   if (const char* e = getenv("HIRE_PROXY_KERNEL")) c->force_dp4a = std::strcmp(e, "dp4a") == 0;
-  if (const char* e = getenv("HIRE_FFN_FUSED")) c->ffn_fused = std::strcmp(e, "0") != 0;
+  if (const char* e = getenv("HIRE_FFN_FUSED")) c->ffn_fused = std::strcmp(e, "1") == 0;
   if (const char* e = getenv("HIRE_FUSED_TRACE")) c->trace = std::strcmp(e, "1") == 0;
-  CK(cudaMalloc(&c->counters, 512 * sizeof(int)));
-  CK(cudaMemset(c->counters, 0, 512 * sizeof(int)));
+  CK(cudaMalloc(&c->counters, kCtxCounterInts * sizeof(int)));
+  CK(cudaMemset(c->counters, 0, kCtxCounterInts * sizeof(int)));
   if (const char* e = getenv("HIRE_NO_PDL")) c->pdl = std::strcmp(e, "1") != 0;
   *out = c;
   return HIRE_OK;
@@ -990,9 +1006,9 @@ int hire_ctx_synchronize(hire_ctx c) {
 int64_t hire_ctx_launch_count(hire_ctx c) { return c ? c->launches : 0; }
 
 int hire_ctx_read_trace(hire_ctx c, long long* out, int n) {
-  if (!c || !out || n > 28) return invalid("bad trace request");
+  if (!c || !out || n > 64) return invalid("bad trace request");
   CK(cudaStreamSynchronize(c->stream));
-  CK(cudaMemcpy(out, c->counters + 320, static_cast<size_t>(n) * 8, cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(out, c->counters + kTraceOff, static_cast<size_t>(n) * 8, cudaMemcpyDeviceToHost));
   return HIRE_OK;
 }
 
@@ -1583,22 +1599,27 @@ int try_ffn_fused(hire_ctx ctx, const hire_matrix_s* u, const hire_matrix_s* v, 
   int ks = 1;
   while (ks < 8 && n_rb * ks < static_cast<int64_t>(ctx->num_sms) * kFusedWarps && nkb >= 2 * ks) ks *= 2;
   const size_t xq_acc = static_cast<size_t>(nt) * 8 * (d + 16) + (ks > 1 ? static_cast<size_t>(kFusedWarps) * nt * 4 * 32 * 4 : 0);
-  const int wcap = 4096;
-  const int64_t wrow = ceil_div(m, ctx->num_sms);
-  const size_t pool = std::max({xq_acc, static_cast<size_t>(m) * 4, static_cast<size_t>(wcap) * 8,
-                                static_cast<size_t>(wrow) * 8, static_cast<size_t>(B * wrow) * 8,
-                                static_cast<size_t>(kp) * 8 + static_cast<size_t>((m + 31) / 32) * 4 +
-                                    static_cast<size_t>(m) * 4});
+  if (kp > 1024 || ctx->num_sms > 255) return 1;  // P4: 128 threads x 8 pairs, u8 slot ids
+  if (ceil_div(m, ctx->num_sms) > 2048) return 1;  // P2b prefetch bitmap
+  if (d * static_cast<int64_t>(dtype_size(u->dtype)) > 4096) return 1;  // P3: one register pass per row
+  const int64_t G = ctx->num_sms;
+  const int64_t wrow = ceil_div(m, G);
+  const size_t pool = std::max({xq_acc, static_cast<size_t>(B * wrow) * 8 + static_cast<size_t>(wrow) * 8 + 8,
+                                static_cast<size_t>((m + 31) / 32) * 4 + static_cast<size_t>(m) * 4 +
+                                    static_cast<size_t>(G) * 4 + static_cast<size_t>(kp)});
   const size_t smem = static_cast<size_t>(B) * d * 4 + pool;
   if (smem > 200 * 1024) return 1;
   const int64_t nch = ceil_div(k, kFusedCh);
   Arena ar;
   FusedFfnArgs args{};
   ar.take(&args.scores, static_cast<size_t>(B * m));
-  ar.take(&args.piv, static_cast<size_t>(2 * B));
+  ar.take(&args.piv, static_cast<size_t>(4 * B));
   ar.take(&args.thr, static_cast<size_t>(B));
-  ar.take(&args.win, static_cast<size_t>(B) * wcap);
-  ar.take(&args.pairs, static_cast<size_t>(B * kp));
+  ar.take(&args.acnt, static_cast<size_t>(B * G));
+  ar.take(&args.pcnt, static_cast<size_t>(B * G));
+  ar.take(&args.gh, static_cast<size_t>(B) * kWinGroups * kWinBins);
+  ar.take(&args.lists, static_cast<size_t>(B) * kWinGroups * kWinBins * kBinCap);
+  ar.take(&args.pairs, static_cast<size_t>(B * G * wrow));
   ar.take(&args.selact, static_cast<size_t>(B * k));
   ar.take(&args.partial, static_cast<size_t>(B * nch * d));
   RET(ar.commit(ctx));
@@ -1613,12 +1634,12 @@ int try_ffn_fused(hire_ctx ctx, const hire_matrix_s* u, const hire_matrix_s* v, 
   args.kp = static_cast<int>(kp);
   args.k = static_cast<int>(k);
   args.phi = p->phi;
-  args.wcap = wcap;
-  args.qcnt = ctx->counters + 256;  // zeroed at creation, reset by the kernel's last CTA
+  args.wmax = static_cast<int>(wrow);
+  args.qcnt = nullptr;
   args.sel = sel;
   args.out = out;
   args.counters = ctx->counters;
-  args.trace = ctx->trace ? reinterpret_cast<long long*>(ctx->counters + 320) : nullptr;
+  args.trace = ctx->trace ? reinterpret_cast<long long*>(ctx->counters + kTraceOff) : nullptr;
   StageScope scope(ctx, kStageFused);
   if (u->dtype == HIRE_BF16) return launch_ffn_fused_nt<__nv_bfloat16>(ctx, args, smem, nt, ks);
   return launch_ffn_fused_nt<float>(ctx, args, smem, nt, ks);

@@ -452,10 +452,10 @@ __device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
 // S1 (small rows, n <= kSel2Exact). One CTA per query: exact T over the
 // whole row and the ordered emit -> cand.
 // ---------------------------------------------------------------------
-__global__ void __launch_bounds__(kSel2Threads) sel_exact_kernel(
+template <int NT, int KPT>
+__global__ void __launch_bounds__(NT) sel_exact_kernel(
     const float* __restrict__ scores, int64_t stride, uint32_t n, uint32_t K,
     uint32_t* __restrict__ cand, int64_t cand_stride) {
-  constexpr int NT = kSel2Threads, KPT = kSel2Kpt;
   __shared__ RangeScratch rs;
   hire_dev::griddep_wait();
   hire_dev::griddep_launch();

@@ -331,7 +331,9 @@ def test_ffn_fused_equals_unfused_and_oracle(H, O, B, monkeypatch):
     a = H.ApproxScorer.quantize(f.u)
     codes, scales = a.export_q4()
     x = _data.queries(B, d, 41, scale=1.0)
-    out_f, sel_f = H.ffn_group_sparse(f, T(x), a, k, kp, x_mode=H.X_INT8)
+    monkeypatch.setenv("HIRE_FFN_FUSED", "1")  # opt-in single-launch kernel (read at context creation)
+    ctx_f = H.Context(0)
+    out_f, sel_f = H.ffn_group_sparse(f, T(x), a, k, kp, x_mode=H.X_INT8, ctx=ctx_f)
     monkeypatch.setenv("HIRE_FFN_FUSED", "0")
     ctx = H.Context(0)
     out_u, sel_u = H.ffn_group_sparse(f, T(x), a, k, kp, x_mode=H.X_INT8, ctx=ctx)
