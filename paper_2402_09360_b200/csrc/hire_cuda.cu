@@ -187,6 +187,27 @@ cudaError_t launch_k(hire_ctx ctx, void (*kernel)(KArgs...), dim3 grid, dim3 blo
   return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
 }
 
+// launch_k with a thread-block cluster of cluster_x CTAs along x
+template <typename... KArgs, typename... Args>
+cudaError_t launch_k_cluster(hire_ctx ctx, void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                             unsigned cluster_x, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = ctx->stream;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = cluster_x;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = ctx->pdl ? 2 : 1;
+  ++ctx->launches;
+  return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
+}
 
 int ensure(void** buf, size_t* cap, size_t need, cudaStream_t s) {
   if (need <= *cap) return HIRE_OK;
@@ -367,6 +388,21 @@ int run_select(hire_ctx ctx, const float* scores, int64_t score_stride, int64_t 
   StageScope scope(ctx, kStageSelect);
   if (sp.mode == 2) {
     const uint32_t nn = static_cast<uint32_t>(n), K = static_cast<uint32_t>(sp.k_eff);
+    // opt-in: one thread-block cluster per query (select2.cuh
+    // sel_cluster_kernel). Measured slower than the paths below on B200
+    // (a cluster barrier per pass costs more than the counting it splits).
+    if (std::getenv("HIRE_SEL_CLUSTER")) {
+#define HIRE_SC(NT_, KPT_)                                                                                    \
+      if (n <= 16 * NT_ * KPT_) {                                                                             \
+        const unsigned cl = static_cast<unsigned>(std::max<int64_t>(1, ceil_div(n, NT_ * KPT_)));           \
+        CK(launch_k_cluster(ctx, sel_cluster_kernel<NT_, KPT_>, dim3(cl, static_cast<unsigned>(B)), NT_, 0, cl, \
+                            scores, score_stride, nn, K, cand, cand_stride));                                 \
+        CK(cudaGetLastError());                                                                               \
+        return HIRE_OK;                                                                                       \
+      }
+      HIRE_SC(256, 4) HIRE_SC(256, 8) HIRE_SC(256, 16) HIRE_SC(512, 16) HIRE_SC(512, 32)
+#undef HIRE_SC
+    }
     if (n <= kSel2Exact) {
       // fewer warps per CTA: the per-pass cost of the order statistic is
       // per-warp overhead, the key counting is cheap
@@ -931,6 +967,10 @@ int hire_ctx_create(int device, void* stream, int own_stream, hire_ctx* out) {
   // opt-in shared memory for the selectors
   CK(cudaFuncSetAttribute(select_candidates_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                           kPoolKeys * 8));
+  for (const void* kf : {(const void*)sel_cluster_kernel<256, 4>, (const void*)sel_cluster_kernel<256, 8>,
+                         (const void*)sel_cluster_kernel<256, 16>, (const void*)sel_cluster_kernel<512, 16>,
+                         (const void*)sel_cluster_kernel<512, 32>})
+    CK(cudaFuncSetAttribute(kf, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
   {
     const int f2 = kFinalMax * 8;
     CK(cudaFuncSetAttribute(final2_kernel<128, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, f2));

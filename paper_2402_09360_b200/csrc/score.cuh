@@ -37,8 +37,19 @@ __global__ void __launch_bounds__(256) prep_x_int8_kernel(
   const float* xb = x + static_cast<int64_t>(b) * d;
   __shared__ float s_red[8];
   __shared__ int s_sum[8];
+  // x stays in registers between the two passes (d <= 256 * kXR on the fast
+  // path; longer vectors stream the remainder)
+  constexpr int kXR = 32;
+  float xr[kXR];
   float m = 0.0f;
-  for (int i = threadIdx.x; i < d; i += blockDim.x) m = fmaxf(m, fabsf(xb[i]));
+#pragma unroll
+  for (int r = 0; r < kXR; ++r) {
+    const int i = threadIdx.x + r * 256;
+    xr[r] = i < d ? xb[i] : 0.0f;
+  }
+#pragma unroll
+  for (int r = 0; r < kXR; ++r) m = fmaxf(m, fabsf(xr[r]));
+  for (int i = threadIdx.x + kXR * 256; i < d; i += blockDim.x) m = fmaxf(m, fabsf(xb[i]));
   m = warp_max_f32(m);
   if ((threadIdx.x & 31) == 0) s_red[threadIdx.x >> 5] = m;
   __syncthreads();
@@ -51,7 +62,18 @@ __global__ void __launch_bounds__(256) prep_x_int8_kernel(
   const float maxabs = s_red[0];
   const float sx = maxabs > 0.0f ? __fdiv_rn(maxabs, 127.0f) : 1.0f;
   int local = 0;
-  for (int i = threadIdx.x; i < d; i += blockDim.x) {
+#pragma unroll
+  for (int r = 0; r < kXR; ++r) {
+    const int i = threadIdx.x + r * 256;
+    if (i >= d) break;
+    const int q = rhaz_clamp(__fdiv_rn(xr[r], sx), 127);
+    local += q;
+    xq[static_cast<int64_t>(b) * d + i] = static_cast<int8_t>(q);
+    const int g = i & ~7, j = i & 7;
+    const int pos = g + ((j & 1) ? 4 : 0) + (j >> 1);
+    xperm[static_cast<int64_t>(b) * d + pos] = static_cast<int8_t>(q);
+  }
+  for (int i = threadIdx.x + kXR * 256; i < d; i += blockDim.x) {
     const int q = rhaz_clamp(__fdiv_rn(xb[i], sx), 127);
     local += q;
     xq[static_cast<int64_t>(b) * d + i] = static_cast<int8_t>(q);
@@ -702,9 +724,6 @@ __global__ void __launch_bounds__(256) q4_score_mma(
     const uint4* __restrict__ wmma, int64_t rows, int d, const float* __restrict__ scales,
     const int8_t* __restrict__ xq, const float* __restrict__ sx, const int* __restrict__ sumxq,
     int B, int phi, float* __restrict__ scores, int64_t score_stride) {
-  hire_dev::griddep_wait();
-  hire_dev::griddep_launch();
-  KTrace kt_(kKtProxy);
   extern __shared__ __align__(16) unsigned char smem[];
   constexpr int RB_PER_CTA = 8 / KS;
   const int xs = d + 16;  // padded query stride (bank spread)
@@ -729,6 +748,7 @@ __global__ void __launch_bounds__(256) q4_score_mma(
   }
   griddep_wait();  // x quantisation (prep_x_int8_kernel) is complete
   griddep_launch();
+  KTrace kt_(kKtProxy);
   for (int i = threadIdx.x; i < NT * 8 * (d / 16); i += blockDim.x) {
     const int n = i / (d / 16), c = i % (d / 16);
     int4 v = make_int4(0, 0, 0, 0);

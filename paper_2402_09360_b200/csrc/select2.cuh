@@ -46,7 +46,7 @@ constexpr int kSel2Sample = kSel2Threads * kSel2SampleKpt;    // 2048 sampled ke
 constexpr int kSel2WinRegs = kSel2Threads * kSel2Kpt;         // window handled in registers
 constexpr int kSel2Qc = 8;                                    // u32 counters per query
 
-constexpr int kRsCompact = 2 * 512;  // survivors moved to registers after a pass
+constexpr int kRsCompact = 1024;  // survivors moved to registers after a pass
 
 struct RangeScratch {
   unsigned cnt[2][32][16];    // per-pass-parity, per-warp bin counts (packed: words 0..7)
@@ -318,8 +318,12 @@ __device__ uint64_t rs_loop(const Src& src, RangeState st, RangeScratch* rs) {
       return st.phase == 0 ? ((static_cast<uint64_t>(st.hi) << 32) | 0xFFFFFFFFull)
                            : ((static_cast<uint64_t>(st.vstar) << 32) | st.hi);
     }
-    if constexpr (Src::kFixed > 2) {
-      if (st.cnt > 32 && st.cnt <= 2 * NT && st.lo != st.hi) {
+    // survivors per thread after compaction: a quarter of the keys per
+    // thread, bounded by the shared staging buffer
+    constexpr int CK0 = Src::kFixed / 4 > 2 ? Src::kFixed / 4 : 2;
+    constexpr int CK = CK0 < kRsCompact / NT ? CK0 : kRsCompact / NT;
+    if constexpr (Src::kFixed > CK && CK >= 2) {
+      if (st.cnt > 32 && st.cnt <= CK * NT && st.lo != st.hi) {
         // compact the survivors (this warp's slice starts after the
         // lower warps' counts of bin bs), continue on 2 keys per thread
         unsigned wc = lane < NW ? bin_count(lane, bs) : 0u;
@@ -339,10 +343,10 @@ __device__ uint64_t rs_loop(const Src& src, RangeState st, RangeScratch* rs) {
           pos += __popc(bl);
         });
         rs_sync<NT>();
-        RegKeys<2> c;
+        RegKeys<CK> c;
         const int t = threadIdx.x;
-        c.k[0] = t < st.cnt ? rs->ckeys[t] : 0ull;
-        c.k[1] = t + NT < st.cnt ? rs->ckeys[t + NT] : 0ull;
+#pragma unroll
+        for (int j = 0; j < CK; ++j) c.k[j] = t + j * NT < st.cnt ? rs->ckeys[t + j * NT] : 0ull;
         return rs_loop<NT>(c, st, rs);
       }
     }
@@ -465,10 +469,21 @@ __global__ void __launch_bounds__(NT) sel_exact_kernel(
   // blocked layout: thread t owns indices [t*KPT, t*KPT+KPT) -> ordered emit
   RegKeys<KPT> src;
   const uint32_t i0 = threadIdx.x * KPT;
+  if ((reinterpret_cast<uintptr_t>(row) & 15) == 0 && i0 + KPT <= n) {
 #pragma unroll
-  for (int j = 0; j < KPT; ++j) {
-    const uint32_t i = i0 + j;
-    src.k[j] = i < n ? make_key(row[i], i) : 0ull;
+    for (int j = 0; j < KPT; j += 4) {
+      const float4 v = *reinterpret_cast<const float4*>(row + i0 + j);
+      src.k[j] = make_key(v.x, i0 + j);
+      src.k[j + 1] = make_key(v.y, i0 + j + 1);
+      src.k[j + 2] = make_key(v.z, i0 + j + 2);
+      src.k[j + 3] = make_key(v.w, i0 + j + 3);
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < KPT; ++j) {
+      const uint32_t i = i0 + j;
+      src.k[j] = i < n ? make_key(row[i], i) : 0ull;
+    }
   }
   const uint64_t T = block_range_select<NT>(src, n, K, &rs);
   int c = 0;
@@ -1034,6 +1049,286 @@ __global__ void __launch_bounds__(NT) final2_kernel(
       out_prob[b * out_stride + j] = static_cast<float>(static_cast<double>(pj) / sum);
     }
   }
+}
+
+}  // namespace hire_dev
+
+namespace hire_dev {
+
+// ---------------------------------------------------------------------
+// Cluster selection: one thread-block cluster (CS <= 16 CTAs) per query.
+// CTA r of the cluster owns the contiguous chunk r of the score row (keys
+// in registers, blocked per thread). Every pass of the 16-way range split
+// counts locally, publishes the CTA's 16 bin totals in its shared memory and
+// crosses ONE cluster barrier; then each CTA reads the cluster's totals
+// through distributed shared memory (mapa + ld.shared::cluster) and takes
+// the same decision. The <= 32 survivors are ranked by every CTA from the
+// cluster's lists; the ordered emit takes its offset from the lower ranks'
+// counts. Rows up to CS * NT * KPT keys in one launch, no global atomics.
+// ---------------------------------------------------------------------
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ unsigned cluster_rank() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ unsigned cluster_size() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%cluster_nctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ uint32_t dsmem_addr(const void* p, unsigned rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_u32(p)), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ unsigned dsmem_ld_u32(const void* p, unsigned rank) {
+  unsigned v;
+  asm volatile("ld.shared::cluster.u32 %0, [%1];" : "=r"(v) : "r"(dsmem_addr(p, rank)) : "memory");
+  return v;
+}
+__device__ __forceinline__ uint64_t dsmem_ld_u64(const void* p, unsigned rank) {
+  unsigned long long v;
+  asm volatile("ld.shared::cluster.u64 %0, [%1];" : "=l"(v) : "r"(dsmem_addr(p, rank)) : "memory");
+  return static_cast<uint64_t>(v);
+}
+
+struct ClusterScratch {
+  unsigned tot[2][16];   // this CTA's bin totals, by pass parity
+  unsigned mm[2][2];     // this CTA's min / max of the projected word, by minmax parity
+  uint64_t small[32];    // this CTA's survivors at the finish
+  int nsmall;
+  unsigned emit;         // this CTA's selected count
+  unsigned st_lo, st_hi;  // decision broadcast inside the CTA
+  long long st_rr, st_cnt;
+  uint64_t result;
+};
+
+template <int NT, int KPT>
+__global__ void __launch_bounds__(NT) sel_cluster_kernel(const float* __restrict__ scores, int64_t stride,
+                                                         uint32_t n, uint32_t K, uint32_t* __restrict__ cand,
+                                                         int64_t cand_stride) {
+  constexpr int NW = NT / 32;
+  __shared__ RangeScratch rs;
+  __shared__ ClusterScratch cs;
+  hire_dev::griddep_wait();
+  hire_dev::griddep_launch();
+  KTrace kt_(kKtPivot);
+  const int b = blockIdx.y;
+  const unsigned rank = cluster_rank(), CS = cluster_size();
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const uint64_t base_n = n / CS, extra = n % CS;
+  const uint32_t first = static_cast<uint32_t>(rank * base_n + (rank < extra ? rank : extra));
+  const uint32_t width = static_cast<uint32_t>(base_n + (rank < extra ? 1 : 0));
+  const float* row = scores + b * stride;
+  RegKeys<KPT> src;
+  const uint32_t i0 = threadIdx.x * KPT;
+#pragma unroll
+  for (int j = 0; j < KPT; ++j) {
+    const uint32_t i = i0 + j;
+    src.k[j] = i < width ? make_key(row[first + i], first + i) : 0ull;
+  }
+  if (threadIdx.x == 0) cs.nsmall = 0;
+  RangeState st;
+  st.phase = 0;
+  st.vstar = 0;
+  st.rr = K;
+  st.cnt = n;
+  st.par = 0;
+  st.above = 0;
+  st.bracket = 0;
+  st.stop = 0;
+  int mpar = 0;
+  // cluster min / max of the projected word
+  auto cluster_minmax = [&]() {
+    unsigned mn = 0xFFFFFFFFu, mx = 0u;
+    src.each([&](uint64_t k, int) {
+      unsigned x;
+      const bool ok = rs_project(st, k, &x);
+      mn = ok ? min(mn, x) : mn;
+      mx = ok ? max(mx, x) : mx;
+    });
+    __syncwarp();
+    mn = __reduce_min_sync(0xffffffffu, mn);
+    mx = __reduce_max_sync(0xffffffffu, mx);
+    if (lane == 0) {
+      rs.red[0][wid] = mn;
+      rs.red[1][wid] = mx;
+    }
+    __syncthreads();
+    if (wid == 0) {
+      unsigned a = lane < NW ? rs.red[0][lane] : 0xFFFFFFFFu, c = lane < NW ? rs.red[1][lane] : 0u;
+      a = __reduce_min_sync(0xffffffffu, a);
+      c = __reduce_max_sync(0xffffffffu, c);
+      if (lane == 0) {
+        cs.mm[mpar][0] = a;
+        cs.mm[mpar][1] = c;
+      }
+    }
+    cluster_sync_all();
+    unsigned a = 0xFFFFFFFFu, c = 0u;
+    if (lane < static_cast<int>(CS)) {
+      a = dsmem_ld_u32(&cs.mm[mpar][0], lane);
+      c = dsmem_ld_u32(&cs.mm[mpar][1], lane);
+    }
+    st.lo = __reduce_min_sync(0xffffffffu, a);
+    st.hi = __reduce_max_sync(0xffffffffu, c);
+    mpar ^= 1;
+  };
+  cluster_minmax();
+  for (;;) {
+    if (st.lo == st.hi) {
+      if (st.phase == 1) break;  // index words are unique: T = (vstar, lo)
+      if (st.cnt > 32) {
+        st.phase = 1;
+        st.vstar = st.lo;
+        cluster_minmax();
+        continue;
+      }
+    }
+    if (st.cnt <= 32) break;
+    const unsigned lo = st.lo, hi = st.hi, range = hi - lo;
+    int sh = 32 - __clz(range) - 4;
+    if (sh < 0) sh = 0;
+    const int pp = st.par;
+    unsigned w[8];
+#pragma unroll
+    for (int m = 0; m < 8; ++m) w[m] = 0;
+    if (st.phase == 0 && lo != 0) {
+      src.count_value_bins(lo, range, sh, w);
+    } else {
+      unsigned a = 0, c = 0;
+      src.each([&](uint64_t k, int j) {
+        unsigned x;
+        const bool ok = rs_project(st, k, &x);
+        const unsigned dlt = x - lo;
+        const unsigned bin = dlt >> sh;
+        const unsigned inc = (ok && dlt <= range) ? (1u << ((bin & 7u) << 2)) : 0u;
+        a += (bin & 8u) ? 0u : inc;
+        c += (bin & 8u) ? inc : 0u;
+        if (j % 15 == 14) {
+          widen_bins(a, c, w);
+          a = 0;
+          c = 0;
+        }
+      });
+      widen_bins(a, c, w);
+    }
+    __syncwarp();
+    unsigned a4[4], a2[2];
+    {
+      const bool h = lane & 4;
+#pragma unroll
+      for (int m = 0; m < 4; ++m)
+        a4[m] = (h ? w[m + 4] : w[m]) + __shfl_xor_sync(0xffffffffu, h ? w[m] : w[m + 4], 4);
+    }
+    {
+      const bool h = lane & 2;
+#pragma unroll
+      for (int m = 0; m < 2; ++m)
+        a2[m] = (h ? a4[m + 2] : a4[m]) + __shfl_xor_sync(0xffffffffu, h ? a4[m] : a4[m + 2], 2);
+    }
+    const bool h1 = lane & 1;
+    unsigned mine = (h1 ? a2[1] : a2[0]) + __shfl_xor_sync(0xffffffffu, h1 ? a2[0] : a2[1], 1);
+    mine += __shfl_xor_sync(0xffffffffu, mine, 8);
+    mine += __shfl_xor_sync(0xffffffffu, mine, 16);
+    if (lane < 8) rs.cnt[pp][wid][lane] = mine;
+    __syncthreads();
+    if (wid == 0) {  // CTA totals of the 16 bins -> shared, for the cluster
+      unsigned t = 0;
+      if (lane < 16) {
+#pragma unroll
+        for (int v = 0; v < NW; ++v) t += rs.cnt[pp][v][lane >> 1];
+        t = (lane & 1) ? (t >> 16) : (t & 0xFFFFu);
+        cs.tot[pp][lane] = t;
+      }
+    }
+    cluster_sync_all();
+    // every warp: the cluster's totals, the same decision everywhere
+    unsigned tot = 0;
+    if (lane < 16)
+      for (unsigned r2 = 0; r2 < CS; ++r2) tot += dsmem_ld_u32(&cs.tot[pp][lane], r2);
+    st.par ^= 1;
+    __syncwarp();
+    unsigned cum = tot;
+#pragma unroll
+    for (int o = 1; o < 16; o <<= 1) {
+      const unsigned t = __shfl_down_sync(0xffffffffu, cum, o);
+      if (lane + o < 16) cum += t;
+    }
+    const unsigned bal = __ballot_sync(0xffffffffu, lane < 16 && static_cast<long long>(cum) >= st.rr);
+    const int bs = 31 - __clz(bal & 0xFFFFu);
+    const unsigned cum_next = __shfl_sync(0xffffffffu, cum, bs + 1);
+    const unsigned tb = __shfl_sync(0xffffffffu, tot, bs);
+    const unsigned nlo = lo + (static_cast<unsigned>(bs) << sh);
+    const unsigned span = (1u << sh) - 1u;
+    st.hi = (hi - nlo > span) ? nlo + span : hi;
+    st.lo = nlo;
+    st.rr -= static_cast<long long>(cum_next);
+    st.cnt = tb;
+  }
+  uint64_t T;
+  if (st.phase == 1 && st.lo == st.hi) {
+    T = (static_cast<uint64_t>(st.vstar) << 32) | st.lo;
+  } else {
+    // <= 32 survivors over the cluster: each CTA lists its own, every CTA
+    // ranks the union
+    const unsigned lo = st.lo, hi = st.hi;
+    src.each([&](uint64_t k, int) {
+      unsigned x;
+      if (rs_project(st, k, &x) && x - lo <= hi - lo) {
+        const int p = atomicAdd(&cs.nsmall, 1);
+        if (p < 32) cs.small[p] = k;
+      }
+    });
+    cluster_sync_all();
+    if (wid == 0) {
+      // lane l gathers the l-th survivor of the union
+      int cnt_r = lane < static_cast<int>(CS) ? static_cast<int>(dsmem_ld_u32(&cs.nsmall, lane)) : 0;
+      cnt_r = min(cnt_r, 32);
+      int incl = cnt_r;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int t = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += t;
+      }
+      const int total = min(__shfl_sync(0xffffffffu, incl, 31), 32);
+      if (lane < 16) rs.scan[lane] = incl;  // inclusive prefix by rank
+      __syncwarp();
+      uint64_t mine = 0;
+      if (lane < total) {
+        int r2 = 0;
+        while (rs.scan[r2] <= lane) ++r2;
+        const int before = r2 > 0 ? rs.scan[r2 - 1] : 0;
+        mine = dsmem_ld_u64(&cs.small[lane - before], static_cast<unsigned>(r2));
+      }
+      int g = 0;
+      for (int j = 0; j < total; ++j)
+        g += static_cast<uint64_t>(__shfl_sync(0xffffffffu, static_cast<unsigned long long>(mine), j)) > mine ? 1 : 0;
+      if (lane < total && g == st.rr - 1) cs.result = mine;
+    }
+    __syncthreads();
+    T = cs.result;
+  }
+  // ordered emit: offset of this CTA = selected keys of the lower ranks
+  int c = 0;
+#pragma unroll
+  for (int j = 0; j < KPT; ++j) c += (src.k[j] && src.k[j] >= T) ? 1 : 0;
+  int total;
+  int pos = block_scan_excl<NT>(c, rs.scan, &total);
+  if (threadIdx.x == 0) cs.emit = static_cast<unsigned>(total);
+  cluster_sync_all();
+  unsigned off = 0;
+  if (lane < static_cast<int>(rank)) off = dsmem_ld_u32(&cs.emit, lane);
+  off = __reduce_add_sync(0xffffffffu, off);
+  uint32_t* out = cand + b * cand_stride;
+  pos += static_cast<int>(off);
+#pragma unroll
+  for (int j = 0; j < KPT; ++j)
+    if (src.k[j] && src.k[j] >= T) out[pos++] = first + i0 + j;
+  cluster_sync_all();  // no CTA leaves while its shared memory may still be read
 }
 
 }  // namespace hire_dev
