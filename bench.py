@@ -545,6 +545,23 @@ def make_workload(H, args, world=1, rank=0):
     return FfnWorkload(H, args.batch or 8)
 
 
+def B_default(args):
+    return args.batch or {"cfg2": 8, "cfg3": 1, "cfg1": 1, "cfg4": 16}[args.workload]
+
+
+def measured_traffic(wl, batch):
+    """DRAM bytes per launch of the roofline kernel from one committed
+    `ncu --set full` capture (profiles/traffic.json), for the workload and
+    batch it was captured at; None otherwise."""
+    try:
+        t = json.load(open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "traffic.json")))
+    except (OSError, ValueError):
+        return None
+    e = t.get(wl.name)
+    default_b = {"cfg2": 8, "cfg3": 1, "cfg1": 1, "cfg4": 16}.get(wl.name)
+    return e["bytes"] if e and batch == default_b else None
+
+
 def run_ours(args):
     world, rank, local = dist_env()
     torch.cuda.set_device(local)
@@ -669,7 +686,7 @@ def run_ours(args):
         "recall_at_k": round(rec, 5) if rec is not None else None,
         "roofline": {"bound": "hbm", "kernel": kname,
                      "achieved": round(achieved, 1), "peak": peaks["hbm_gbs"], "unit": "GB/s",
-                     "frac": round(achieved / peaks["hbm_gbs"], 4), "traffic": None,
+                     "frac": round(achieved / peaks["hbm_gbs"], 4), "traffic": measured_traffic(wl, B_default(args)),
                      "bytes_per_launch": pb, "avg_launch_us": round(k_us, 3),
                      "peak_src": peaks["src"]},
         "step_roofline": {"bytes": step_b, "unique_u_rows": nu, "unique_v_rows": nv,

@@ -555,7 +555,9 @@ int launch_q4_mma_t(hire_ctx ctx, const hire_scorer_s* a, const ScoreWs& w, int6
   }
   const int64_t n_rb = ceil_div(a->rows, 16);
   const int64_t want = ceil_div(n_rb, 8 / KS);
-  const int grid = static_cast<int>(std::min<int64_t>(want, static_cast<int64_t>(bps) * ctx->num_sms));
+  static const int mult = std::getenv("HIRE_MMA_CTAS_PER_SM") ? std::atoi(std::getenv("HIRE_MMA_CTAS_PER_SM")) : 0;
+  const int per_sm = mult > 0 ? std::min(mult, bps) : bps;
+  const int grid = static_cast<int>(std::min<int64_t>(want, static_cast<int64_t>(per_sm) * ctx->num_sms));
   CK(launch_k(ctx, k, grid, 256, smem, a->mma, a->rows, d, a->scales, w.xq + b0 * d, w.sx + b0,
               w.sumxq + b0, static_cast<int>(nb), phi, out + b0 * stride, stride));
   return HIRE_OK;
