@@ -9,7 +9,7 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libhire_cuda.so")
+LIB_PATH = os.path.join(HERE, os.environ.get("HIRE_LIB_VARIANT", "libhire_cuda.so"))  # variant: A/B experiments only
 
 OK, ERR_INVALID, ERR_IO, ERR_RUNTIME = 0, 1, 2, 3
 F32, BF16 = 0, 1

@@ -86,9 +86,29 @@ class Context:
             if buf[48]:
                 spans["ws_gather"] = (buf[47], buf[48])
                 spans["ws_select"] = (buf[48], buf[49])
-                spans["ws_m"] = (0, buf[50] * 1000)
-        return {k: (round((a - t0) / 1e3, 2), round((b - t0) / 1e3, 2)) for k, (a, b) in
-                sorted(spans.items(), key=lambda t: t[1][0])}
+        if buf[52] or buf[55]:
+            # fused proxy/filter kernel (fsel.cuh): sample arrivals, bracket
+            # published, first/last CTA done streaming, last CTA done filtering
+            if buf[52]:
+                spans["fsel_sampled_bracket"] = (buf[52], buf[53] or buf[52])
+            spans["proxy_cta_end_first_last"] = (buf[54], buf[55])
+            if buf[56]:
+                spans["fsel_filter_end"] = (buf[55], buf[56])
+            if buf[63]:
+                spans["fsel_bounds_seen"] = (buf[63], buf[63])
+        if buf[57]:
+            spans["fin_counts_to_gather"] = (buf[57], buf[58] or buf[57])
+            spans["fin_select"] = (buf[58] or buf[57], buf[59] or buf[57])
+            spans["fin_emit"] = (buf[59] or buf[57], buf[60] or buf[57])
+        counts = {"fin_listed": int(buf[61]), "fin_fallback": int(buf[62])} if buf[57] else {}
+        for nm, base in (("fin_fastsel", 24), ("bracket_fastsel", 32)):
+            st = [buf[base + i] for i in range(8) if buf[base + i]]
+            if st:
+                counts[nm + "_phase_us"] = [round((b - a) / 1e3, 2) for a, b in zip(st, st[1:])]
+        out = {k: (round((a - t0) / 1e3, 2), round((b - t0) / 1e3, 2)) for k, (a, b) in
+               sorted(spans.items(), key=lambda t: t[1][0])}
+        out.update(counts)
+        return out
 
     def profile_read(self) -> dict:
         """{stage: (total_ms, intervals)} since the last read (syncs)."""

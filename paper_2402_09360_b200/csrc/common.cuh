@@ -143,11 +143,24 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned phase) {
 }
 
 // --------------------------------------------------------------- loads --
+// Weight streams (proxy codes, gathered rows): no L1 allocation.
+// HIRE_L2_HINT=1 adds an L2 evict-first policy (measured slower on B200).
+#ifndef HIRE_L2_HINT
+#define HIRE_L2_HINT 0  // measured: slower proxy stream, no downstream gain (kept opt-in)
+#endif
 __device__ __forceinline__ uint4 ldg_stream(const void* p) {
   uint4 r;
+#if HIRE_L2_HINT
+  asm("{\n\t.reg .b64 pol;\n\t"
+      "createpolicy.fractional.L2::evict_first.b64 pol, 1.0;\n\t"
+      "ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], pol;\n\t}"
+      : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+      : "l"(p));
+#else
   asm("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
                : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
                : "l"(p));
+#endif
   return r;
 }
 

@@ -28,6 +28,7 @@
 #include "score.cuh"
 #include "select.cuh"
 #include "select2.cuh"
+#include "fsel.cuh"
 
 using namespace hire_dev;
 
@@ -86,6 +87,8 @@ struct hire_ctx_s {
   int* counters = nullptr;  // zeroed hand-off counters of the fused kernels
   unsigned* selc = nullptr;  // zeroed selection counters (select2.cuh qc / agg)
   size_t selc_cap = 0;
+  void* fzero = nullptr;     // zero-at-rest sample slots + bounds of the fused selector (fsel.cuh)
+  size_t fzero_cap = 0;
   // stage profiling (hire_ctx_set_profiling): event pairs around each stage
   bool prof = false;
   std::vector<cudaEvent_t> ev_pool;
@@ -245,7 +248,7 @@ int ensure_selc(hire_ctx ctx, size_t words) {
   }
   const size_t n = std::max<size_t>(words, 4096);
   CK(cudaMalloc(&ctx->selc, n * sizeof(unsigned)));
-  CK(cudaMemset(ctx->selc, 0, n * sizeof(unsigned)));
+  CK(cudaMemsetAsync(ctx->selc, 0, n * sizeof(unsigned), ctx->stream));
   ctx->selc_cap = n;
   return HIRE_OK;
 }
@@ -914,6 +917,92 @@ int validate_topk(const hire_matrix_s* w, const hire_scorer_s* a, int64_t B, con
 }
 
 // The local stage of hire_topk: scores -> candidates -> exact values.
+// ------------------------------------------- proxy + fused selection --
+// fsel.cuh: the int4 tensor-core proxy kernel filters its own scores against
+// a sampled lower bound; sel_fin_kernel finishes the exact top-k'.
+struct FselPlan {
+  bool on = false;
+  int nt = 1, ks = 1, G = 0, nbrk = 1, samp_step = 1, n_samp = 0, r_lo = 0;
+  size_t smem = 0;
+};
+
+template <int NT, int KS>
+size_t fsel_smem(int d) {
+  return static_cast<size_t>(NT) * 8 * (d + 16) + (KS > 1 ? static_cast<size_t>(8) * NT * 4 * 32 * 4 : 0);
+}
+
+template <int NT, int KS>
+int fsel_bps(size_t smem) {
+  static size_t last = ~size_t(0);
+  static int bps = 0;
+  if (smem != last) {
+    auto k = q4_score_mma_sel<NT, KS>;
+    if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024) != cudaSuccess) return 0;
+    bps = max_blocks(k, 256, smem);
+    last = smem;
+  }
+  return bps;
+}
+
+template <int NT>
+int fsel_bps_ks(int ks, int d, size_t* smem) {
+  if (ks == 1) { *smem = fsel_smem<NT, 1>(d); return fsel_bps<NT, 1>(*smem); }
+  *smem = fsel_smem<NT, 2>(d);
+  return fsel_bps<NT, 2>(*smem);
+}
+
+// Decide whether the fused path applies and size it: one full wave of
+// streaming CTAs (same count on every SM) + bracket CTAs, list capacity,
+// sample rank of the bracket.
+void plan_fsel(hire_ctx ctx, const hire_scorer_s* a, int64_t B, const hire_topk_params* p, const SelPlan& sp,
+               FselPlan* f) {
+  f->on = false;
+  const char* env = std::getenv("HIRE_FSEL");
+  if (env && env[0] == '0') return;
+  if (sp.mode != 2 || a->rows <= kSel2Exact || a->kind != HIRE_SCORER_Q4 || p->x_mode != HIRE_X_INT8) return;
+  // B <= 8 (one MMA n-tile): at larger batches the in-flight filter's
+  // registers spill and the fused kernel loses to the unfused chain (measured)
+  if (a->d % 64 != 0 || ctx->force_dp4a || B < 1 || B > 8) return;
+  const int64_t n = a->rows, K = sp.k_eff, n_rb = ceil_div(n, 16);
+  f->nt = B <= 8 ? 1 : B <= 16 ? 2 : B <= 32 ? 4 : 8;
+  f->ks = n_rb < 32LL * ctx->num_sms ? 2 : 1;
+  int bps = 0;
+  switch (f->nt) {
+    case 1: bps = fsel_bps_ks<1>(f->ks, static_cast<int>(a->d), &f->smem); break;
+    case 2: bps = fsel_bps_ks<2>(f->ks, static_cast<int>(a->d), &f->smem); break;
+    case 4: bps = fsel_bps_ks<4>(f->ks, static_cast<int>(a->d), &f->smem); break;
+    default: bps = fsel_bps_ks<8>(f->ks, static_cast<int>(a->d), &f->smem); break;
+  }
+  if (bps < 1) return;
+  const int64_t resident = static_cast<int64_t>(bps) * ctx->num_sms;
+  f->nbrk = static_cast<int>(std::min<int64_t>(B, 8));
+  const int64_t rpc = 8 / f->ks;
+  const int64_t G = std::min<int64_t>(resident - f->nbrk, ceil_div(n_rb, rpc));
+  if (G < 1 || n > kFinMaxRows) return;
+  // sample: round-0 row-blocks of every samp_step-th CTA (rpc * 16 keys each)
+  const int64_t per = rpc * 16;
+  const int64_t want = std::min<int64_t>(G, kFselSampleMax / per);
+  f->samp_step = static_cast<int>(ceil_div(G, want));
+  f->n_samp = static_cast<int>(std::min<int64_t>(ceil_div(G, f->samp_step) * per, std::min<int64_t>(n, kFselSampleMax)));
+  // bracket: sample rank ~ mean + 4 sigma
+  const double S = f->n_samp, pr = static_cast<double>(K) / static_cast<double>(n);
+  const double mu = pr * S, sd = std::sqrt(S * pr * (1.0 - pr));
+  f->r_lo = static_cast<int>(std::ceil(mu + 4.0 * sd + 1.0));
+  if (f->r_lo > S / 2) return;
+  const double listed = f->r_lo / S * static_cast<double>(n) + 4.0 * std::sqrt(static_cast<double>(f->r_lo) / S * n);
+  if (listed > 0.9 * kFinCap) return;
+  f->G = static_cast<int>(G);
+  f->on = true;
+}
+
+template <int NT, int KS>
+int launch_fsel_t(hire_ctx ctx, const hire_scorer_s* a, const ScoreWs& w, int64_t B, int phi, float* out,
+                  const FselPlan& f, const FuseSel& fs) {
+  CK(launch_k(ctx, q4_score_mma_sel<NT, KS>, f.G + f.nbrk, 256, f.smem, a->mma, a->rows, static_cast<int>(a->d), a->scales,
+              w.xq, w.sx, w.sumxq, static_cast<int>(B), phi, out, a->rows, fs));
+  return HIRE_OK;
+}
+
 struct TopkWs {
   ScoreWs sw;
   float* scores = nullptr;
@@ -921,23 +1010,90 @@ struct TopkWs {
   uint32_t* cand = nullptr;
   float* vals = nullptr;
   int* status = nullptr;
+  FselPlan fz;
+  uint64_t* fz_lists = nullptr;
 };
 
 void take_topk_ws(Arena& ar, TopkWs* t, const hire_scorer_s* a, int64_t B, const SelPlan& sp,
-                  bool need_cand) {
+                  bool need_cand, hire_ctx ctx = nullptr, const hire_topk_params* p = nullptr) {
   take_score_ws(ar, &t->sw, a, B);
   ar.take(&t->scores, static_cast<size_t>(B * a->rows));
-  ar.take(&t->surv, static_cast<size_t>(sp.surv_words(B)));
+  if (ctx && p) plan_fsel(ctx, a, B, p, sp, &t->fz);
+  if (t->fz.on) {
+    ar.take(&t->fz_lists, static_cast<size_t>(B) * kFinCap);
+  } else {
+    ar.take(&t->surv, static_cast<size_t>(sp.surv_words(B)));
+  }
   if (need_cand) ar.take(&t->cand, static_cast<size_t>(B * sp.k_eff));
   ar.take(&t->vals, static_cast<size_t>(B * sp.k_eff));
   ar.take(&t->status, 1);
 }
 
+// prep_x -> fused proxy/filter kernel -> sel_fin_kernel
+int run_scores_fsel(hire_ctx ctx, const hire_scorer_s* a, const float* x, int64_t B, int phi, const SelPlan& sp,
+                    const TopkWs& t, uint32_t* cand) {
+  const FselPlan& f = t.fz;
+  const int d = static_cast<int>(a->d);
+  RET(ensure_mma_layout(ctx, const_cast<hire_scorer_s*>(a)));
+  {
+    StageScope pscope(ctx, kStagePrep);
+    CK(launch_k(ctx, prep_x_int8_kernel, static_cast<unsigned>(B), 256, 0, x, d, t.sw.xq, t.sw.xperm, t.sw.sx,
+                t.sw.sumxq));
+  }
+  FuseSel fs;
+  fs.n = static_cast<uint32_t>(a->rows);
+  fs.K = static_cast<uint32_t>(sp.k_eff);
+  fs.g_stream = f.G;
+  fs.nbrk = f.nbrk;
+  fs.samp_step = f.samp_step;
+  fs.n_samp = f.n_samp;
+  fs.r_lo = f.r_lo;
+  {  // dedicated zero-at-rest buffer (the arena is shared with other ops)
+    const size_t need = static_cast<size_t>(B) * (kFselSampleMax + 2) * 8;
+    if (need > ctx->fzero_cap) {
+      if (ctx->fzero) {
+        CK(cudaStreamSynchronize(ctx->stream));
+        CK(cudaFree(ctx->fzero));
+        ctx->fzero = nullptr;
+      }
+      const size_t nb = std::max(need, ctx->fzero_cap * 2);
+      CK(cudaMalloc(&ctx->fzero, nb));
+      CK(cudaMemsetAsync(ctx->fzero, 0, nb, ctx->stream));
+      ctx->fzero_cap = nb;
+    }
+  }
+  fs.samp = static_cast<uint64_t*>(ctx->fzero);
+  fs.lo = static_cast<unsigned long long*>(ctx->fzero) + static_cast<size_t>(B) * kFselSampleMax;
+  fs.cnt = reinterpret_cast<unsigned*>(fs.lo + B);
+  fs.lists = t.fz_lists;
+  {
+    StageScope scope(ctx, kStageProxy);
+#define HIRE_FS(NT_)                                                                   \
+    if (f.nt == NT_) {                                                                 \
+      if (f.ks == 1) RET((launch_fsel_t<NT_, 1>(ctx, a, t.sw, B, phi, t.scores, f, fs))); \
+      else RET((launch_fsel_t<NT_, 2>(ctx, a, t.sw, B, phi, t.scores, f, fs)));           \
+    }
+    HIRE_FS(1) else HIRE_FS(2) else HIRE_FS(4) else HIRE_FS(8)
+#undef HIRE_FS
+  }
+  {
+    StageScope scope(ctx, kStageSelect);
+    CK(launch_k(ctx, sel_fin_kernel, static_cast<unsigned>(B), kFinThreads, static_cast<size_t>((a->rows + 31) / 32) * 4, static_cast<const float*>(t.scores),
+                a->rows, fs, cand, sp.k_eff, t.status));
+  }
+  CK(cudaGetLastError());
+  return HIRE_OK;
+}
+
 int local_candidates(hire_ctx ctx, const hire_matrix_s* w, const hire_scorer_s* a, const float* x,
                      int64_t B, const hire_topk_params* p, const SelPlan& sp, const TopkWs& t,
                      uint32_t* cand) {
-  RET(run_scores(ctx, a, x, B, p->phi, p->x_mode, p->strict, t.sw, t.scores, a->rows));
-  RET(run_select(ctx, t.scores, a->rows, a->rows, B, sp, t.surv, cand, sp.k_eff, t.status));
+  if (t.fz.on) {
+    RET(run_scores_fsel(ctx, a, x, B, p->phi, sp, t, cand));
+  } else {
+    RET(run_scores(ctx, a, x, B, p->phi, p->x_mode, p->strict, t.sw, t.scores, a->rows));
+    RET(run_select(ctx, t.scores, a->rows, a->rows, B, sp, t.surv, cand, sp.k_eff, t.status));
+  }
   RET(run_recompute(ctx, w, cand, sp.k_eff, sp.k_eff, x, B, p->phi, p->strict, t.vals, sp.k_eff));
   return HIRE_OK;
 }
@@ -986,6 +1142,7 @@ int hire_ctx_create(int device, void* stream, int own_stream, hire_ctx* out) {
   }
   CK(cudaFuncSetAttribute(final_select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                           kFinalMax * 8));
+  CK(cudaFuncSetAttribute(sel_fin_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kFinMaxRows / 8));
   CK(cudaFuncSetAttribute(bucket_topt_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                           kBucketMaxWidth * 8));
   // every other kernel with dynamic shared memory: allow up to 200 KB once,
@@ -1024,6 +1181,7 @@ int hire_ctx_destroy(hire_ctx c) {
   if (c->ws) cudaFree(c->ws);
   if (c->counters) cudaFree(c->counters);
   if (c->selc) cudaFree(c->selc);
+  if (c->fzero) cudaFree(c->fzero);
   if (c->io_dev) cudaFree(c->io_dev);
   if (c->io_host) cudaFreeHost(c->io_host);
   for (auto& m : c->marks) { cudaEventDestroy(m.second.first); cudaEventDestroy(m.second.second); }
@@ -1063,7 +1221,7 @@ int hire_debug_ktrace(hire_ctx c, int op, unsigned long long* out, int n) {
   if (op == 1) {
     if (!buf) CK(cudaMalloc(&buf, kWords * sizeof(unsigned long long)));
     unsigned long long init[kWords];
-    for (int i = 0; i < kWords; ++i) init[i] = (i & 1) || i >= 39 ? 0ull : ~0ull;
+    for (int i = 0; i < kWords; ++i) init[i] = ((i & 1) || i >= 24) && i != 54 ? 0ull : ~0ull;
     CK(cudaMemcpy(buf, init, sizeof(init), cudaMemcpyHostToDevice));
     CK(cudaMemcpyToSymbol(hire_dev::g_ktrace, &buf, sizeof(buf)));
   } else if (op == 2) {
@@ -1431,7 +1589,7 @@ int hire_topk_run(hire_ctx ctx, hire_matrix w, hire_scorer a, const float* x, in
   RET(plan_select(w->rows, p->k_prime, p->select, p->n_buckets, p->bucket_t, &sp));
   Arena ar;
   TopkWs t;
-  take_topk_ws(ar, &t, a, B, sp, true);
+  take_topk_ws(ar, &t, a, B, sp, true, ctx, p);
   RET(ar.commit(ctx));
   RET(local_candidates(ctx, w, a, x, B, p, sp, t, t.cand));
   const int64_t take = std::min<int64_t>(p->k, sp.k_eff);
@@ -1818,7 +1976,7 @@ int da_local(hire_ctx ctx, const hire_matrix_s* w, const hire_scorer_s* a, int64
              uint64_t* send) {
   Arena ar;
   TopkWs t;
-  take_topk_ws(ar, &t, a, B, dp.sp, true);
+  take_topk_ws(ar, &t, a, B, dp.sp, true, ctx, p);
   RET(ar.commit(ctx));
   RET(local_candidates(ctx, w, a, x, B, p, dp.sp, t, t.cand));
   if (offset) {

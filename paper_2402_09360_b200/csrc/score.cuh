@@ -672,8 +672,10 @@ namespace hire_dev {
 // ---------------------------------------------------------------------
 __global__ void q4_to_mma_layout(const uint8_t* __restrict__ wq, int64_t pitch, int64_t rows,
                                  int d, uint32_t* __restrict__ out, int64_t n_words) {
+  // No early launch_dependents: the proxy kernels that follow stream their
+  // first weight tiles BEFORE their griddepcontrol.wait (independent
+  // prologue), so the layout they read must be complete when they start.
   hire_dev::griddep_wait();
-  hire_dev::griddep_launch();
   const int64_t id = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (id >= n_words) return;
   const int nkb = d / 64;
@@ -830,6 +832,13 @@ __global__ void __launch_bounds__(256) q4_score_mma(
                 apply_phi(phi, __fmul_rn(static_cast<float>(aint), cs));
           }
         }
+    }
+  }
+  if (g_ktrace) {  // spread of CTA end times (debug timeline)
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      atomicMin(&g_ktrace[54], gtimer());
+      atomicMax(&g_ktrace[55], gtimer());
     }
   }
 }

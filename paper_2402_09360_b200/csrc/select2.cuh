@@ -35,6 +35,7 @@
 // pipeline without re-initialisation.
 #pragma once
 #include "common.cuh"
+#include "fastsel.cuh"
 
 namespace hire_dev {
 
@@ -940,6 +941,7 @@ __global__ void __launch_bounds__(NT) final2_kernel(
     float* __restrict__ out_prob, uint64_t* __restrict__ out_keys, int64_t out_stride) {
   __shared__ RangeScratch rs;
   __shared__ double s_red[NT / 32];
+  int* const s_scan = rs.scan;
   extern __shared__ __align__(16) unsigned char smem_f2[];
   uint64_t* s_sel = reinterpret_cast<uint64_t*>(smem_f2);
   hire_dev::griddep_wait();
@@ -962,11 +964,11 @@ __global__ void __launch_bounds__(NT) final2_kernel(
 #pragma unroll
   for (int j = 0; j < KPT; ++j) nv += src.k[j] != 0;
   nv = __reduce_add_sync(0xffffffffu, nv);
-  if ((threadIdx.x & 31) == 0) rs.scan[threadIdx.x >> 5] = nv;
+  if ((threadIdx.x & 31) == 0) s_scan[threadIdx.x >> 5] = nv;
   __syncthreads();
   int n_valid = 0;
 #pragma unroll
-  for (int v = 0; v < NT / 32; ++v) n_valid += rs.scan[v];
+  for (int v = 0; v < NT / 32; ++v) n_valid += s_scan[v];
   __syncthreads();
   const int Kq = min(K, n_valid);
   // K >= pool: everything is selected (no order statistic needed)
@@ -975,7 +977,7 @@ __global__ void __launch_bounds__(NT) final2_kernel(
 #pragma unroll
   for (int j = 0; j < KPT; ++j) c += (src.k[j] && src.k[j] >= T) ? 1 : 0;
   int total;
-  int pos = block_scan_excl<NT>(c, rs.scan, &total);
+  int pos = block_scan_excl<NT>(c, s_scan, &total);
   if (out_mode == 1) {
 #pragma unroll
     for (int j = 0; j < KPT; ++j)
