@@ -89,6 +89,21 @@ struct hire_ctx_s {
   size_t selc_cap = 0;
   void* fzero = nullptr;     // zero-at-rest sample slots + bounds of the fused selector (fsel.cuh)
   size_t fzero_cap = 0;
+  // host-buffer calls (*_host): after one eager call per shape, the whole
+  // call — H2D copy, kernel chain, D2H copy — replays as one CUDA graph on
+  // gstream. An entry is valid while every buffer it captured is unchanged.
+  struct HostGraph {
+    std::vector<int64_t> key;
+    std::vector<const void*> bufs;
+    cudaGraphExec_t exec = nullptr;
+    int64_t out[4] = {0, 0, 0, 0};
+  };
+  std::vector<HostGraph> hgraphs;
+  std::vector<std::vector<int64_t>> hseen;
+  bool host_graphs = true;
+  cudaStream_t gstream = nullptr;
+  cudaEvent_t gev = nullptr;
+  std::vector<const void*> buf_snapshot() const { return {ws, io_dev, io_host, selc, fzero, counters}; }
   // stage profiling (hire_ctx_set_profiling): event pairs around each stage
   bool prof = false;
   std::vector<cudaEvent_t> ev_pool;
@@ -1100,6 +1115,75 @@ int local_candidates(hire_ctx ctx, const hire_matrix_s* w, const hire_scorer_s* 
 
 }  // namespace
 
+namespace {
+// ------------------------------------------------------- host-call graphs --
+// body(stream) issues the whole host call (copies + kernels) on ctx->stream
+// and fills out[4]. First call per key: eager. Second: captured on gstream,
+// instantiated, launched. Later: launched. The caller synchronises.
+template <class Body>
+int run_host_graph(hire_ctx ctx, const std::vector<int64_t>& key, int64_t* out, Body body) {
+  if (!ctx->host_graphs || ctx->prof) return body(out);
+  const auto bufs = ctx->buf_snapshot();
+  for (auto& g : ctx->hgraphs)
+    if (g.key == key && g.bufs == bufs) {
+      CK(cudaEventRecord(ctx->gev, ctx->stream));
+      CK(cudaStreamWaitEvent(ctx->gstream, ctx->gev, 0));
+      CK(cudaGraphLaunch(g.exec, ctx->gstream));
+      CK(cudaEventRecord(ctx->gev, ctx->gstream));
+      CK(cudaStreamWaitEvent(ctx->stream, ctx->gev, 0));
+      for (int i = 0; i < 4; ++i) out[i] = g.out[i];
+      return HIRE_OK;
+    }
+  bool seen = false;
+  for (auto& k : ctx->hseen) seen |= k == key;
+  if (!seen) {  // eager first call: allocations, lazy layouts, static state
+    ctx->hseen.push_back(key);
+    return body(out);
+  }
+  if (!ctx->gstream) {
+    CK(cudaStreamCreateWithFlags(&ctx->gstream, cudaStreamNonBlocking));
+    CK(cudaEventCreateWithFlags(&ctx->gev, cudaEventDisableTiming));
+  }
+  // drop stale entries of this key (a buffer moved)
+  for (size_t i = 0; i < ctx->hgraphs.size();)
+    if (ctx->hgraphs[i].key == key) {
+      cudaGraphExecDestroy(ctx->hgraphs[i].exec);
+      ctx->hgraphs.erase(ctx->hgraphs.begin() + static_cast<long>(i));
+    } else {
+      ++i;
+    }
+  CK(cudaStreamSynchronize(ctx->stream));
+  cudaStream_t user = ctx->stream;
+  ctx->stream = ctx->gstream;
+  CK(cudaStreamBeginCapture(ctx->gstream, cudaStreamCaptureModeThreadLocal));
+  const int64_t launches0 = ctx->launches;
+  const int rc = body(out);
+  cudaGraph_t graph = nullptr;
+  const cudaError_t ec = cudaStreamEndCapture(ctx->gstream, &graph);
+  ctx->stream = user;
+  ctx->launches = launches0;
+  if (rc != HIRE_OK) {
+    if (graph) cudaGraphDestroy(graph);
+    return rc;
+  }
+  if (ec != cudaSuccess || ctx->buf_snapshot() != bufs) {  // not capturable as is: stay eager
+    if (graph) cudaGraphDestroy(graph);
+    cudaGetLastError();
+    ctx->host_graphs = ec == cudaSuccess;
+    return body(out);
+  }
+  cudaGraphExec_t exec = nullptr;
+  const cudaError_t ei = cudaGraphInstantiate(&exec, graph, 0);
+  cudaGraphDestroy(graph);
+  CK(ei);
+  ctx->hgraphs.push_back({key, bufs, exec, {out[0], out[1], out[2], out[3]}});
+  CK(cudaGraphLaunch(exec, ctx->gstream));
+  CK(cudaEventRecord(ctx->gev, ctx->gstream));
+  CK(cudaStreamWaitEvent(ctx->stream, ctx->gev, 0));
+  return HIRE_OK;
+}
+}  // namespace
+
 // ====================================================================== ABI
 extern "C" {
 
@@ -1171,6 +1255,7 @@ int hire_ctx_create(int device, void* stream, int own_stream, hire_ctx* out) {
   CK(cudaMalloc(&c->counters, kCtxCounterInts * sizeof(int)));
   CK(cudaMemset(c->counters, 0, kCtxCounterInts * sizeof(int)));
   if (const char* e = getenv("HIRE_NO_PDL")) c->pdl = std::strcmp(e, "1") != 0;
+  if (const char* e = getenv("HIRE_HOST_GRAPHS")) c->host_graphs = std::strcmp(e, "0") != 0;
   *out = c;
   return HIRE_OK;
 }
@@ -1184,6 +1269,9 @@ int hire_ctx_destroy(hire_ctx c) {
   if (c->fzero) cudaFree(c->fzero);
   if (c->io_dev) cudaFree(c->io_dev);
   if (c->io_host) cudaFreeHost(c->io_host);
+  for (auto& g : c->hgraphs) cudaGraphExecDestroy(g.exec);
+  if (c->gstream) cudaStreamDestroy(c->gstream);
+  if (c->gev) cudaEventDestroy(c->gev);
   for (auto& m : c->marks) { cudaEventDestroy(m.second.first); cudaEventDestroy(m.second.second); }
   for (auto e : c->ev_pool) cudaEventDestroy(e);
   if (c->own_stream) cudaStreamDestroy(c->stream);
@@ -1578,6 +1666,7 @@ int hire_topk_select(hire_ctx ctx, const float* v, int64_t B, int64_t n, int64_t
   return HIRE_OK;
 }
 
+
 // ------------------------------------------------------------ hire_topk --
 int hire_topk_run(hire_ctx ctx, hire_matrix w, hire_scorer a, const float* x, int64_t B,
                   const hire_topk_params* p, uint32_t* cand, uint32_t* top_idx, float* top_val,
@@ -1623,18 +1712,30 @@ int hire_topk_host(hire_ctx ctx, hire_matrix w, hire_scorer a, const float* x_ho
   char* dv = static_cast<char*>(ctx->io_dev);
   char* hs = static_cast<char*>(ctx->io_host);
   std::memcpy(hs, x_host, xb);
-  CK(cudaMemcpyAsync(dv, hs, xb, cudaMemcpyHostToDevice, ctx->stream));
-  char* o = dv + in_bytes;
-  uint32_t* dcand = cb ? reinterpret_cast<uint32_t*>(o) : nullptr;
-  o += align_up(cb);
-  uint32_t* didx = reinterpret_cast<uint32_t*>(o);
-  o += align_up(tb);
-  float* dval = reinterpret_cast<float*>(o);
-  o += align_up(tb);
-  float* dprob = pb ? reinterpret_cast<float*>(o) : nullptr;
-  RET(hire_topk_run(ctx, w, a, reinterpret_cast<const float*>(dv), B, p, dcand, didx, dval, dprob,
-                    n_cand, n_top, clamped));
-  CK(cudaMemcpyAsync(hs + in_bytes, dv + in_bytes, out_bytes, cudaMemcpyDeviceToHost, ctx->stream));
+  const std::vector<int64_t> key = {1, reinterpret_cast<int64_t>(w), reinterpret_cast<int64_t>(a), B, p->k, p->k_prime,
+                                    p->phi, p->x_mode, p->select, p->strict, p->n_buckets, p->bucket_t,
+                                    cb ? 1 : 0, pb ? 1 : 0};
+  int64_t res[4];
+  RET(run_host_graph(ctx, key, res, [&](int64_t* r) -> int {
+    CK(cudaMemcpyAsync(dv, hs, xb, cudaMemcpyHostToDevice, ctx->stream));
+    char* o = dv + in_bytes;
+    uint32_t* dcand = cb ? reinterpret_cast<uint32_t*>(o) : nullptr;
+    o += align_up(cb);
+    uint32_t* didx = reinterpret_cast<uint32_t*>(o);
+    o += align_up(tb);
+    float* dval = reinterpret_cast<float*>(o);
+    o += align_up(tb);
+    float* dprob = pb ? reinterpret_cast<float*>(o) : nullptr;
+    int cl = 0;
+    RET(hire_topk_run(ctx, w, a, reinterpret_cast<const float*>(dv), B, p, dcand, didx, dval, dprob, &r[0], &r[1],
+                      &cl));
+    r[2] = cl;
+    CK(cudaMemcpyAsync(hs + in_bytes, dv + in_bytes, out_bytes, cudaMemcpyDeviceToHost, ctx->stream));
+    return HIRE_OK;
+  }));
+  if (n_cand) *n_cand = res[0];
+  if (n_top) *n_top = res[1];
+  if (clamped) *clamped = static_cast<int>(res[2]);
   CK(cudaStreamSynchronize(ctx->stream));
   const char* ho = hs + in_bytes;
   (void)take;
@@ -1883,11 +1984,17 @@ int hire_ffn_host(hire_ctx ctx, hire_matrix u, hire_matrix v, hire_scorer a, con
   char* dv = static_cast<char*>(ctx->io_dev);
   char* hs = static_cast<char*>(ctx->io_host);
   std::memcpy(hs, x_host, xb);
-  CK(cudaMemcpyAsync(dv, hs, xb, cudaMemcpyHostToDevice, ctx->stream));
   uint32_t* dsel = reinterpret_cast<uint32_t*>(dv + in_bytes);
   float* dout = reinterpret_cast<float*>(dv + in_bytes + align_up(sb));
-  RET(hire_ffn_run(ctx, u, v, a, reinterpret_cast<const float*>(dv), B, p, dsel, dout));
-  CK(cudaMemcpyAsync(hs + in_bytes, dv + in_bytes, out_bytes, cudaMemcpyDeviceToHost, ctx->stream));
+  const std::vector<int64_t> key = {2, reinterpret_cast<int64_t>(u), reinterpret_cast<int64_t>(v), reinterpret_cast<int64_t>(a),
+                                    B, p->k, p->k_prime, p->group_size, p->phi, p->x_mode, p->strict};
+  int64_t res[4];
+  RET(run_host_graph(ctx, key, res, [&](int64_t*) -> int {
+    CK(cudaMemcpyAsync(dv, hs, xb, cudaMemcpyHostToDevice, ctx->stream));
+    RET(hire_ffn_run(ctx, u, v, a, reinterpret_cast<const float*>(dv), B, p, dsel, dout));
+    CK(cudaMemcpyAsync(hs + in_bytes, dv + in_bytes, out_bytes, cudaMemcpyDeviceToHost, ctx->stream));
+    return HIRE_OK;
+  }));
   CK(cudaStreamSynchronize(ctx->stream));
   if (sel_host) std::memcpy(sel_host, hs + in_bytes, sb);
   std::memcpy(out_host, hs + in_bytes + align_up(sb), ob);

@@ -1,0 +1,79 @@
+"""GPU: the host-buffer C ABI calls (hire_topk_host / hire_ffn_host — the
+calls a reference-side binding makes with plain host pointers). After one
+eager call per shape they replay as one captured CUDA graph (H2D copy, the
+kernel chain, D2H copy); every call must equal the device-pointer path on
+the same inputs, across eager / capture / replay calls, changing inputs,
+other ops in between (workspace reuse), and with graphs disabled."""
+import ctypes as C
+
+import numpy as np
+import pytest
+import torch
+
+from tests import _data
+
+pytestmark = pytest.mark.gpu
+
+
+def T(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+def _topk_host(H, ctx, z, a, x, cfg):
+    B = x.shape[0]
+    p = cfg.params()
+    cand = np.zeros((B, cfg.k_prime), np.uint32)
+    idx = np.zeros((B, cfg.k), np.uint32)
+    val = np.zeros((B, cfg.k), np.float32)
+    prob = np.zeros((B, cfg.k), np.float32)
+    nc, nt, cl = C.c_int64(), C.c_int64(), C.c_int()
+    xx = np.ascontiguousarray(x, np.float32)
+    H._lib.check(H.lib().hire_topk_host(ctx.h, z.h, a.h, xx.ctypes.data_as(C.c_void_p), B, C.byref(p),
+                                        cand.ctypes.data_as(C.c_void_p), idx.ctypes.data_as(C.c_void_p),
+                                        val.ctypes.data_as(C.c_void_p), prob.ctypes.data_as(C.c_void_p),
+                                        C.byref(nc), C.byref(nt), C.byref(cl)))
+    return cand[:, :nc.value], idx[:, :nt.value], val[:, :nt.value], prob[:, :nt.value], bool(cl.value)
+
+
+@pytest.mark.parametrize("V,d,k,kp,B", [(20000, 256, 16, 256, 2), (6000, 128, 8, 64, 1)])
+def test_topk_host_replays_equal_device_path(H, O, V, d, k, kp, B):
+    w = _data.lowrank_plus_noise(V, d, 16, V)
+    codes, scales = O.quantize_int4(w)
+    z = H.ScoreMatrix(T(w))
+    a = H.ApproxScorer.quantized(codes, scales)
+    cfg = H.HireConfig(k=k, k_prime=kp, x_mode=H.X_INT8)
+    ctx = H.Context(0)
+    g = np.random.default_rng(1)
+    for it in range(6):
+        x = (g.standard_normal((B, d)) / np.sqrt(d)).astype(np.float32)
+        if it == 3:  # another op on the same context in between (workspace reuse)
+            H.topk_select(T(g.standard_normal((3, 50000)).astype(np.float32)), 100, ctx=ctx)
+        cand, idx, val, prob, cl = _topk_host(H, ctx, z, a, x, cfg)
+        r = H.hire_topk(T(x), z, a, cfg)
+        _, pr = H.softmax_topk(z, T(x), a, cfg)
+        assert np.array_equal(cand, r.cand.cpu().numpy().astype(np.uint32)), it
+        assert np.array_equal(idx, r.top_idx.cpu().numpy().astype(np.uint32)), it
+        assert np.array_equal(val.view(np.uint32), r.top_val.cpu().numpy().view(np.uint32)), it
+        np.testing.assert_allclose(prob, pr.cpu().numpy(), rtol=1e-6)
+        assert cl == r.clamped
+
+
+def test_ffn_host_replays_equal_device_path(H, O, monkeypatch):
+    m, d, k, kp, B = 2048, 256, 102, 204, 3
+    u, v = _data.ffn_family(m, d, 5, r=16)
+    f = H.GroupedFFN(H.ScoreMatrix(T(u)), H.ScoreMatrix(T(v)))
+    a = H.ApproxScorer.quantize(f.u)
+    g = np.random.default_rng(2)
+    for graphs in ("1", "0"):
+        monkeypatch.setenv("HIRE_HOST_GRAPHS", graphs)
+        ctx = H.Context(0)
+        p = H._lib.FfnParams(k, kp, 1, 1, H.X_INT8, 0, 0)
+        for it in range(5):
+            x = g.standard_normal((B, d)).astype(np.float32)
+            sel = np.zeros((B, k), np.uint32)
+            out = np.zeros((B, d), np.float32)
+            H._lib.check(H.lib().hire_ffn_host(ctx.h, f.u.h, f.v.h, a.h, x.ctypes.data_as(C.c_void_p), B, C.byref(p),
+                                               sel.ctypes.data_as(C.c_void_p), out.ctypes.data_as(C.c_void_p)))
+            want, wsel = H.ffn_group_sparse(f, T(x), a, k, kp, x_mode=H.X_INT8)
+            assert np.array_equal(sel, wsel.cpu().numpy().astype(np.uint32)), (graphs, it)
+            assert np.array_equal(out.view(np.uint32), want.cpu().numpy().view(np.uint32)), (graphs, it)
