@@ -50,6 +50,8 @@ constexpr int kFinThreads = 1024;
 constexpr int kFinKpt = 8;
 constexpr int kFinCap = kFinThreads * kFinKpt; // listed keys handled on chip
 constexpr int kFinMaxRows = 1 << 19;           // emit bitmap: rows per query
+constexpr int kFselCtr = 16;                   // claim counters (128 B apart)
+constexpr int kFselDynLog = 16;                // claimed row-blocks remembered per warp before the bounds
 constexpr int kFselMaxB = 64;
 constexpr unsigned long long kFselTimeoutNs = 20000000ull;  // 20 ms
 
@@ -64,6 +66,9 @@ struct FuseSel {
   uint64_t* samp;    // [B][kFselSampleMax], zero at rest
   unsigned long long* lo;  // [B], zero at rest; 0 = not yet known
   unsigned* cnt;     // [B] listed keys (bit 31: a bound never arrived), zero at rest
+  unsigned* ctr;     // [kFselCtr * 32] row-block claim counters (dynamic tail), zero at rest
+  int n_static;      // rounds scheduled statically (>= 1; the rest is claimed, KS == 1)
+  const float* xf;   // non-null: quantise x here (prep_x_int8_kernel folded in; small B)
   uint64_t* lists;   // [B][kFinCap] listed keys (unordered)
 };
 
@@ -172,11 +177,56 @@ __global__ void __launch_bounds__(256, HIRE_FSEL_MINB) q4_score_mma_sel(
     return;
   }
 
-  for (int i = threadIdx.x; i < NT * 8 * (d / 16); i += blockDim.x) {
-    const int n = i / (d / 16), cc = i % (d / 16);
-    int4 v = make_int4(0, 0, 0, 0);
-    if (n < B) v = *reinterpret_cast<const int4*>(xq + static_cast<int64_t>(n) * d + cc * 16);
-    *reinterpret_cast<int4*>(s_x + n * xs + cc * 16) = v;
+  __shared__ float s_sx[8];
+  __shared__ int s_sumq[8];
+  __shared__ float s_red[8];
+  __shared__ int s_redi[8];
+  if (fs.xf) {
+    // prep_x_int8_kernel folded in (B <= 2): every CTA quantises x itself,
+    // with the same arithmetic (bit-identical sx, codes and code sums)
+    for (int n = 0; n < NT * 8; ++n) {
+      if (n >= B) {
+        for (int i = threadIdx.x; i < d / 16; i += blockDim.x) *reinterpret_cast<int4*>(s_x + n * xs + i * 16) = make_int4(0, 0, 0, 0);
+        continue;
+      }
+      const float* xb = fs.xf + static_cast<int64_t>(n) * d;
+      float m = 0.0f;
+      for (int i = threadIdx.x; i < d; i += blockDim.x) m = fmaxf(m, fabsf(__ldg(xb + i)));
+      m = warp_max_f32(m);
+      if (lane == 0) s_red[wid] = m;
+      __syncthreads();
+      float mx = 0.0f;
+#pragma unroll
+      for (int w = 0; w < 8; ++w) mx = fmaxf(mx, s_red[w]);
+      const float sxv = mx > 0.0f ? __fdiv_rn(mx, 127.0f) : 1.0f;
+      int sum = 0;
+      for (int i = threadIdx.x; i < d; i += blockDim.x) {
+        const int qv = rhaz_clamp(__fdiv_rn(__ldg(xb + i), sxv), 127);
+        sum += qv;
+        s_x[n * xs + i] = static_cast<int8_t>(qv);
+      }
+      sum = warp_sum_i32(sum);
+      if (lane == 0) s_redi[wid] = sum;
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        int t2 = 0;
+        for (int w = 0; w < 8; ++w) t2 += s_redi[w];
+        s_sumq[n] = t2;
+        s_sx[n] = sxv;
+      }
+      __syncthreads();
+    }
+  } else {
+    for (int i = threadIdx.x; i < NT * 8 * (d / 16); i += blockDim.x) {
+      const int n = i / (d / 16), cc = i % (d / 16);
+      int4 v = make_int4(0, 0, 0, 0);
+      if (n < B) v = *reinterpret_cast<const int4*>(xq + static_cast<int64_t>(n) * d + cc * 16);
+      *reinterpret_cast<int4*>(s_x + n * xs + cc * 16) = v;
+    }
+    if (threadIdx.x < B && threadIdx.x < 8) {
+      s_sx[threadIdx.x] = sx[threadIdx.x];
+      s_sumq[threadIdx.x] = sumxq[threadIdx.x];
+    }
   }
   __syncthreads();
 
@@ -222,30 +272,32 @@ __global__ void __launch_bounds__(256, HIRE_FSEL_MINB) q4_score_mma_sel(
     base = __shfl_sync(0xffffffffu, base, 0);
     if (in && base + rank < static_cast<unsigned>(kFinCap)) fs.lists[static_cast<int64_t>(n) * kFinCap + base + rank] = key;
   };
-  // backlog: this warp's row-blocks of rounds [q0, q1) re-read from L2
-  // (its own scores), loads of all backlog rounds in flight at once (an L2
-  // round trip costs microseconds while HBM is saturated)
-  auto filter_from_l2 = [&](int q0, int q1, unsigned long long la, unsigned long long lb) {
+  // backlog: row-blocks this warp scored before the bounds were known,
+  // re-read from L2 (its own scores); nrb of them, rb_of(i) gives the i-th.
+  // Loads of all of them in flight at once (an L2 round trip costs
+  // microseconds while HBM is saturated); lanes 0-15 / 16-31 take two
+  // row-blocks per load, lane order = row order.
+  auto filter_from_l2 = [&](int nrb, auto rb_of, unsigned long long la, unsigned long long lb) {
     if (ks != 0) return;
     constexpr int RB = 8;
     for (int n = 0; n < B; ++n) {
       const uint64_t lo = __shfl_sync(0xffffffffu, n < 32 ? la : lb, n & 31);
       const float* srow = scores + static_cast<int64_t>(n) * score_stride;
-      for (int r0 = q0; r0 < q1; r0 += RB) {
+      for (int i0 = 0; i0 < nrb; i0 += RB) {
         float v[RB / 2];
+        int64_t rbs[RB / 2];
 #pragma unroll
-        for (int j = 0; j < RB / 2; ++j) {  // two rounds per load: lanes 0-15 / 16-31
-          const int rr = r0 + 2 * j + (lane >> 4);
-          const int64_t row = (static_cast<int64_t>(rr) * U + static_cast<int64_t>(c) * RPC + rb_local) * 16 + (lane & 15);
-          v[j] = (rr < q1 && row < rows) ? __ldcg(srow + row) : 0.0f;
+        for (int j = 0; j < RB / 2; ++j) {
+          const int i = i0 + 2 * j + (lane >> 4);
+          rbs[j] = i < nrb ? rb_of(i) : n_rb;
+          const int64_t row = rbs[j] * 16 + (lane & 15);
+          v[j] = (rbs[j] < n_rb && row < rows) ? __ldcg(srow + row) : 0.0f;
         }
 #pragma unroll
         for (int j = 0; j < RB / 2; ++j) {
-          const int rr = r0 + 2 * j + (lane >> 4);
-          const int64_t rbi = static_cast<int64_t>(rr) * U + static_cast<int64_t>(c) * RPC + rb_local;
-          const int64_t row = rbi * 16 + (lane & 15);
+          const int64_t row = rbs[j] * 16 + (lane & 15);
           const uint64_t key = make_key(v[j], static_cast<uint32_t>(row));
-          const bool in = rr < q1 && rbi < n_rb && row < rows && key >= lo;
+          const bool in = rbs[j] < n_rb && row < rows && key >= lo;
           const unsigned bal = __ballot_sync(0xffffffffu, in);
           append(n, in, key, bal, __popc(bal & ((1u << lane) - 1u)));
         }
@@ -256,8 +308,22 @@ __global__ void __launch_bounds__(256, HIRE_FSEL_MINB) q4_score_mma_sel(
   const bool sampler = c % fs.samp_step == 0;
   bool ready = false;
   unsigned long long lo_a = 0, lo_b = 0;  // lane l: lo[l], lo[l + 32]
-  for (int rd = 0; rd < rounds; ++rd) {
-    const int64_t rb = static_cast<int64_t>(rd) * U + static_cast<int64_t>(c) * RPC + rb_local;
+  // schedule: rounds [0, n_static) static (round-robin row-blocks as in the
+  // unfused kernel); KS == 1: the remaining row-blocks are claimed one at a
+  // time from kFselCtr interleaved counters (claim issued one row-block
+  // ahead), so warps on slower SMs take fewer and all finish together
+  const int n_static = KS == 1 ? min(fs.n_static, rounds) : rounds;
+  const int64_t s_rb = static_cast<int64_t>(n_static) * U;
+  const int q = (c * 8 + wid) & (kFselCtr - 1);
+  __shared__ int64_t s_dyn[8][kFselDynLog];
+  int n_dyn = 0;        // claimed row-blocks scored before the bounds (logged)
+  bool dyn_over = false;
+  unsigned claim = 0;
+  int64_t rb = static_cast<int64_t>(c) * RPC + rb_local;
+  for (int rd = 0;; ++rd) {
+    if (KS == 1 ? rb >= n_rb : rd >= rounds) break;
+    const bool next_static = rd + 1 < n_static;
+    if (KS == 1 && !next_static && lane == 0) claim = atomicAdd(fs.ctr + q * 32, 1u);
     // issue the bound poll now, look at it after the row-block
     unsigned long long pa = 0, pb = 0;
     if (!ready) {
@@ -271,7 +337,9 @@ __global__ void __launch_bounds__(256, HIRE_FSEL_MINB) q4_score_mma_sel(
 #pragma unroll
       for (int nt = 0; nt < NT; ++nt) acc[nt][0] = acc[nt][1] = acc[nt][2] = acc[nt][3] = 0;
     }
-    const int64_t rbn = rb + U;
+    const int64_t rbn = (KS > 1 || next_static)
+                            ? rb + U
+                            : s_rb + q + static_cast<int64_t>(kFselCtr) * __shfl_sync(0xffffffffu, claim, 0);
     if (rbn < n_rb) {
 #pragma unroll
       for (int u = 0; u < UL; ++u)
@@ -306,8 +374,8 @@ __global__ void __launch_bounds__(256, HIRE_FSEL_MINB) q4_score_mma_sel(
         const int n = nt * 8 + 2 * t + (e & 1);
         key[nt][e] = 0ull;
         if (own && row < rows && n < B) {
-          const int aint = acc[nt][e] - 8 * sumxq[n];
-          const float cs = __fmul_rn(scales[row], sx[n]);
+          const int aint = acc[nt][e] - 8 * s_sumq[n];
+          const float cs = __fmul_rn(scales[row], s_sx[n]);
           const float sc = apply_phi(phi, __fmul_rn(static_cast<float>(aint), cs));
           scores[static_cast<int64_t>(n) * score_stride + row] = sc;
           key[nt][e] = make_key(sc, static_cast<uint32_t>(row));
@@ -332,7 +400,23 @@ __global__ void __launch_bounds__(256, HIRE_FSEL_MINB) q4_score_mma_sel(
         lo_a = pa;
         lo_b = pb;
         if (g_ktrace && threadIdx.x == 0) atomicMax(&g_ktrace[63], gtimer());
-        filter_from_l2(0, rd, lo_a, lo_b);  // backlog
+        // backlog: static rounds before this one, then the logged claims
+        const int ns = min(rd, n_static);
+        filter_from_l2(ns, [&](int i) { return static_cast<int64_t>(i) * U + static_cast<int64_t>(c) * RPC + rb_local; },
+                       lo_a, lo_b);
+        filter_from_l2(n_dyn, [&](int i) { return s_dyn[wid][i]; }, lo_a, lo_b);
+        if (dyn_over && ks == 0 && lane < B) {
+          atomicOr(fs.cnt + lane, 0x80000000u);  // claims not logged: exact fallback
+          if (lane + 32 < B) atomicOr(fs.cnt + lane + 32, 0x80000000u);
+        }
+      } else if (rd >= n_static && rb < n_rb) {  // log this claimed row-block
+        if (n_dyn < kFselDynLog) {
+          if (lane == 0) s_dyn[wid][n_dyn] = rb;
+          __syncwarp();
+          ++n_dyn;
+        } else {
+          dyn_over = true;
+        }
       }
     }
     if (ready && own) {
@@ -363,6 +447,7 @@ __global__ void __launch_bounds__(256, HIRE_FSEL_MINB) q4_score_mma_sel(
           if (in1 && c0 + __popc(bb1 & below) < lim) Lk[c0 + __popc(bb1 & below)] = k1;
         }
     }
+    rb = rbn;
   }
   if (g_ktrace && lane == 0) {
     atomicMin(&g_ktrace[54], gtimer());
@@ -384,7 +469,13 @@ __global__ void __launch_bounds__(256, HIRE_FSEL_MINB) q4_score_mma_sel(
       __nanosleep(128);
     }
     if (ready) {
-      filter_from_l2(0, rounds, pa, pb);
+      filter_from_l2(n_static, [&](int i) { return static_cast<int64_t>(i) * U + static_cast<int64_t>(c) * RPC + rb_local; },
+                     pa, pb);
+      filter_from_l2(n_dyn, [&](int i) { return s_dyn[wid][i]; }, pa, pb);
+      if (dyn_over && ks == 0 && lane < B) {
+        atomicOr(fs.cnt + lane, 0x80000000u);
+        if (lane + 32 < B) atomicOr(fs.cnt + lane + 32, 0x80000000u);
+      }
     } else if (ks == 0 && lane < B) {
       atomicOr(fs.cnt + lane, 0x80000000u);  // no bound: sel_fin_kernel falls back
       if (lane + 32 < B) atomicOr(fs.cnt + lane + 32, 0x80000000u);
@@ -402,7 +493,7 @@ __global__ void __launch_bounds__(256, HIRE_FSEL_MINB) q4_score_mma_sel(
 // ---------------------------------------------------------------------
 __global__ void __launch_bounds__(kFinThreads) sel_fin_kernel(
     const float* __restrict__ scores, int64_t stride, FuseSel fs, uint32_t* __restrict__ cand,
-    int64_t cand_stride, int* __restrict__ status) {
+    int64_t cand_stride, int ordered, int* __restrict__ status) {
   constexpr int NT = kFinThreads, KPT = kFinKpt;
   __shared__ union {
     RangeScratch rs;
@@ -427,6 +518,7 @@ __global__ void __launch_bounds__(kFinThreads) sel_fin_kernel(
       fs.lo[b] = 0ull;
       fs.cnt[b] = 0u;
     }
+    if (b == 0 && threadIdx.x < kFselCtr) fs.ctr[threadIdx.x * 32] = 0u;
   }
   uint32_t* out = cand + static_cast<int64_t>(b) * cand_stride;
   const int total = static_cast<int>(total_raw & 0x7FFFFFFFu);
@@ -443,6 +535,20 @@ __global__ void __launch_bounds__(kFinThreads) sel_fin_kernel(
     if (dbg) g_ktrace[58] = gtimer();
     const uint64_t T = block_fast_select<NT, KPT>(k, K, &u.fss, (g_ktrace && b == 0) ? g_ktrace + 24 : nullptr);
     if (dbg) { g_ktrace[59] = gtimer(); g_ktrace[61] = total; }
+    if (!ordered) {
+      // the caller does not return the candidate list: any order will do
+      // (the exact recompute and the final top-k are order-independent)
+      int c = 0;
+#pragma unroll
+      for (int j = 0; j < KPT; ++j) c += (k[j] != 0 && k[j] >= T) ? 1 : 0;
+      int tot2;
+      int pos = block_scan_excl<NT>(c, u.fss.scan, &tot2);
+#pragma unroll
+      for (int j = 0; j < KPT; ++j)
+        if (k[j] != 0 && k[j] >= T) out[pos++] = key_index(k[j]);
+      if (dbg) g_ktrace[60] = gtimer();
+      return;
+    }
 #pragma unroll
     for (int j = 0; j < KPT; ++j)
       if (k[j] != 0 && k[j] >= T) {

@@ -1046,16 +1046,19 @@ void take_topk_ws(Arena& ar, TopkWs* t, const hire_scorer_s* a, int64_t B, const
 
 // prep_x -> fused proxy/filter kernel -> sel_fin_kernel
 int run_scores_fsel(hire_ctx ctx, const hire_scorer_s* a, const float* x, int64_t B, int phi, const SelPlan& sp,
-                    const TopkWs& t, uint32_t* cand) {
+                    const TopkWs& t, uint32_t* cand, bool ordered) {
   const FselPlan& f = t.fz;
   const int d = static_cast<int>(a->d);
   RET(ensure_mma_layout(ctx, const_cast<hire_scorer_s*>(a)));
-  {
+  // B <= 2: the proxy kernel quantises x itself (one launch fewer)
+  const bool fold = B <= 2 && !std::getenv("HIRE_FSEL_NOFOLD");
+  if (!fold) {
     StageScope pscope(ctx, kStagePrep);
     CK(launch_k(ctx, prep_x_int8_kernel, static_cast<unsigned>(B), 256, 0, x, d, t.sw.xq, t.sw.xperm, t.sw.sx,
                 t.sw.sumxq));
   }
   FuseSel fs;
+  fs.xf = fold ? x : nullptr;
   fs.n = static_cast<uint32_t>(a->rows);
   fs.K = static_cast<uint32_t>(sp.k_eff);
   fs.g_stream = f.G;
@@ -1064,7 +1067,7 @@ int run_scores_fsel(hire_ctx ctx, const hire_scorer_s* a, const float* x, int64_
   fs.n_samp = f.n_samp;
   fs.r_lo = f.r_lo;
   {  // dedicated zero-at-rest buffer (the arena is shared with other ops)
-    const size_t need = static_cast<size_t>(B) * (kFselSampleMax + 2) * 8;
+    const size_t need = static_cast<size_t>(B) * (kFselSampleMax + 2) * 8 + kFselCtr * 32 * 4;
     if (need > ctx->fzero_cap) {
       if (ctx->fzero) {
         CK(cudaStreamSynchronize(ctx->stream));
@@ -1080,6 +1083,17 @@ int run_scores_fsel(hire_ctx ctx, const hire_scorer_s* a, const float* x, int64_
   fs.samp = static_cast<uint64_t*>(ctx->fzero);
   fs.lo = static_cast<unsigned long long*>(ctx->fzero) + static_cast<size_t>(B) * kFselSampleMax;
   fs.cnt = reinterpret_cast<unsigned*>(fs.lo + B);
+  fs.ctr = reinterpret_cast<unsigned*>(fs.lo + 2 * B);
+  {
+    const int64_t U = static_cast<int64_t>(f.G) * (8 / f.ks);
+    const int64_t full = a->rows / 16 / U;  // complete rounds
+    // static round-robin for every round by default; HIRE_FSEL_STATIC=k
+    // claims the row-blocks after round k dynamically (measured: no gain —
+    // the proxy stream is bandwidth-bound to the end)
+    fs.n_static = 1 << 30;
+    (void)full;
+    if (const char* e = std::getenv("HIRE_FSEL_STATIC")) fs.n_static = std::max(1, std::atoi(e));
+  }
   fs.lists = t.fz_lists;
   {
     StageScope scope(ctx, kStageProxy);
@@ -1094,17 +1108,19 @@ int run_scores_fsel(hire_ctx ctx, const hire_scorer_s* a, const float* x, int64_
   {
     StageScope scope(ctx, kStageSelect);
     CK(launch_k(ctx, sel_fin_kernel, static_cast<unsigned>(B), kFinThreads, static_cast<size_t>((a->rows + 31) / 32) * 4, static_cast<const float*>(t.scores),
-                a->rows, fs, cand, sp.k_eff, t.status));
+                a->rows, fs, cand, sp.k_eff, ordered ? 1 : 0, t.status));
   }
   CK(cudaGetLastError());
   return HIRE_OK;
 }
 
+// ordered: the candidate list is returned to the caller (ascending indices,
+// hire.hpp:65-67); otherwise any order (recompute and final top-k do not care)
 int local_candidates(hire_ctx ctx, const hire_matrix_s* w, const hire_scorer_s* a, const float* x,
                      int64_t B, const hire_topk_params* p, const SelPlan& sp, const TopkWs& t,
-                     uint32_t* cand) {
+                     uint32_t* cand, bool ordered = true) {
   if (t.fz.on) {
-    RET(run_scores_fsel(ctx, a, x, B, p->phi, sp, t, cand));
+    RET(run_scores_fsel(ctx, a, x, B, p->phi, sp, t, cand, ordered));
   } else {
     RET(run_scores(ctx, a, x, B, p->phi, p->x_mode, p->strict, t.sw, t.scores, a->rows));
     RET(run_select(ctx, t.scores, a->rows, a->rows, B, sp, t.surv, cand, sp.k_eff, t.status));
@@ -1680,7 +1696,7 @@ int hire_topk_run(hire_ctx ctx, hire_matrix w, hire_scorer a, const float* x, in
   TopkWs t;
   take_topk_ws(ar, &t, a, B, sp, true, ctx, p);
   RET(ar.commit(ctx));
-  RET(local_candidates(ctx, w, a, x, B, p, sp, t, t.cand));
+  RET(local_candidates(ctx, w, a, x, B, p, sp, t, t.cand, cand != nullptr));
   const int64_t take = std::min<int64_t>(p->k, sp.k_eff);
   RET(run_final(ctx, t.vals, sp.k_eff, t.cand, sp.k_eff, nullptr, 0, 0, sp.k_eff, take, B, 0, top_idx,
                 top_val, top_prob, nullptr, p->k));
@@ -2085,7 +2101,7 @@ int da_local(hire_ctx ctx, const hire_matrix_s* w, const hire_scorer_s* a, int64
   TopkWs t;
   take_topk_ws(ar, &t, a, B, dp.sp, true, ctx, p);
   RET(ar.commit(ctx));
-  RET(local_candidates(ctx, w, a, x, B, p, dp.sp, t, t.cand));
+  RET(local_candidates(ctx, w, a, x, B, p, dp.sp, t, t.cand, false));
   if (offset) {
     CK(launch_k(ctx, add_offset_kernel, static_cast<unsigned>(ceil_div(B * dp.sp.k_eff, 256)), 256, 0, t.cand, B * dp.sp.k_eff, static_cast<uint32_t>(offset)));
     CK(cudaGetLastError());

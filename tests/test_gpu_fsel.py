@@ -121,3 +121,19 @@ def test_fused_topk_values_strict(H, O):
         assert np.array_equal(N(r.cand[b]).astype(np.uint32), o["cand"])
         assert np.array_equal(N(r.top_idx[b]).astype(np.uint32), o["top_idx"])
         assert np.array_equal(N(r.top_val[b]).view(np.uint32), o["top_val"].view(np.uint32))
+
+
+def test_fused_unordered_candidates_same_topk(H, O):
+    # want_candidates=False: the fused selector emits candidates in any order;
+    # the exact top-k (values, ties by index) must not change
+    V, d, k, kp, B = 150000, 128, 64, 1024, 4
+    w, z, a, codes, scales = _instance(H, O, V, d, 21)
+    x = _data.queries(B, d, 22)
+    cfg = H.HireConfig(k=k, k_prime=kp, x_mode=H.X_INT8)
+    r1 = H.hire_topk(T(x), z, a, cfg)
+    r0 = H.hire_topk(T(x), z, a, cfg, want_candidates=False)
+    assert torch.equal(r1.top_idx, r0.top_idx)
+    assert torch.equal(r1.top_val, r0.top_val)
+    for b in range(B):
+        want, _ = _want_cand(O, codes, scales, x[b], kp)
+        assert np.array_equal(N(r1.cand[b]).astype(np.uint32), want)
