@@ -42,6 +42,7 @@
 #include "common.cuh"
 #include "select2.cuh"
 #include "fastsel.cuh"
+#include "exact.cuh"
 
 namespace hire_dev {
 
@@ -491,21 +492,18 @@ __global__ void __launch_bounds__(256, HIRE_FSEL_MINB) q4_score_mma_sel(
 // in shared memory (set bits, popcount prefix, ordered write) — no sort.
 // Dynamic shared memory: ceil(n / 32) words.
 // ---------------------------------------------------------------------
-__global__ void __launch_bounds__(kFinThreads) sel_fin_kernel(
-    const float* __restrict__ scores, int64_t stride, FuseSel fs, uint32_t* __restrict__ cand,
-    int64_t cand_stride, int ordered, int* __restrict__ status) {
+union FinShared {
+  RangeScratch rs;
+  FastSelScratch fss;
+};
+
+// The finisher for query b (one 1024-thread CTA); s_bm: ceil(n/32) words of
+// shared memory for the ordered emit.
+__device__ __noinline__ void fin_select_emit(const float* __restrict__ scores, int64_t stride, const FuseSel& fs,
+                                             uint32_t* __restrict__ cand, int64_t cand_stride, int ordered,
+                                             int* __restrict__ status, int b, FinShared& u, unsigned* s_bm) {
   constexpr int NT = kFinThreads, KPT = kFinKpt;
-  __shared__ union {
-    RangeScratch rs;
-    FastSelScratch fss;
-  } u;
   RangeScratch& rs = u.rs;
-  extern __shared__ __align__(16) unsigned char fin_smem[];
-  unsigned* s_bm = reinterpret_cast<unsigned*>(fin_smem);
-  griddep_wait();
-  griddep_launch();
-  KTrace kt_(kKtEmit);
-  const int b = blockIdx.x;
   const uint32_t n = fs.n, K = fs.K;
   const unsigned total_raw = __ldcg(fs.cnt + b);
   const bool dbg = g_ktrace && threadIdx.x == 0 && b == 0;
@@ -599,6 +597,170 @@ __global__ void __launch_bounds__(kFinThreads) sel_fin_kernel(
     for (int j = 0; j < KPT; ++j)
       if (k[j] != 0 && k[j] >= T) out[pos++] = key_index(k[j]);
     base += tot2;
+  }
+}
+
+
+__global__ void __launch_bounds__(kFinThreads) sel_fin_kernel(
+    const float* __restrict__ scores, int64_t stride, FuseSel fs, uint32_t* __restrict__ cand,
+    int64_t cand_stride, int ordered, int* __restrict__ status) {
+  __shared__ FinShared u;
+  extern __shared__ __align__(16) unsigned char fin_smem[];
+  griddep_wait();
+  griddep_launch();
+  KTrace kt_(kKtEmit);
+  fin_select_emit(scores, stride, fs, cand, cand_stride, ordered, status, blockIdx.x, u,
+                  reinterpret_cast<unsigned*>(fin_smem));
+}
+
+// ---------------------------------------------------------------------
+// One launch for everything after the fused proxy kernel (hire_topk):
+//   CTAs [0, B)   : the finisher of query b (fin_select_emit), then flag[b]
+//   CTAs [B, B+R) : recompute workers — for each query in turn, wait for its
+//                   flag, gather + score its candidate rows (the arithmetic
+//                   of recompute_fast: lane chunks in order, fmaf, fixed
+//                   butterfly -> bit-identical values), then take a ticket;
+//                   the last worker of query b runs the final top-k +
+//                   softmax (hire.hpp:74-80, 135-142) and clears flag/ticket.
+// Two kernel boundaries and two cold starts fewer than fin -> K4 -> K5.
+// post: [2B] zero-at-rest words (flags, tickets). All CTAs co-resident (one
+// per SM, B + R <= SMs).
+// ---------------------------------------------------------------------
+constexpr int kPostMaxK = 256;
+
+template <typename T, int CPL>
+__device__ __forceinline__ float post_row_dot(const T* __restrict__ w, int64_t pitch_vec, int64_t row,
+                                              const float* s_x, int lane) {
+  constexpr int E = Vec16<T>::kElems;
+  const uint4* rp = reinterpret_cast<const uint4*>(w) + row * pitch_vec;
+  float acc = 0.0f;
+#pragma unroll
+  for (int c0 = 0; c0 < CPL; c0 += 4) {
+    uint4 v[4];
+#pragma unroll
+    for (int c = 0; c < 4; ++c)
+      if (c0 + c < CPL) v[c] = ldg_stream(rp + lane + 32 * (c0 + c));
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      if (c0 + c >= CPL) break;
+      float f[E], xv[E];
+      Vec16<T>::expand(v[c], f);
+      load_x_vec<E>(s_x + (lane + 32 * (c0 + c)) * E, xv);
+#pragma unroll
+      for (int e = 0; e < E; ++e) acc = fmaf(f[e], xv[e], acc);
+    }
+  }
+  return warp_sum_f32(acc);
+}
+
+template <typename T, int CPL>
+__global__ void __launch_bounds__(kFinThreads, 1) fsel_post_kernel(
+    const float* __restrict__ scores, int64_t stride, FuseSel fs, uint32_t* __restrict__ cand, int64_t cand_stride,
+    int ordered, int* __restrict__ status, const T* __restrict__ w, int d, const float* __restrict__ x, int phi,
+    float* __restrict__ vals, int kp, int K, uint32_t* __restrict__ out_idx, float* __restrict__ out_val,
+    float* __restrict__ out_prob, int64_t out_stride, unsigned* __restrict__ post, int R) {
+  constexpr int NT = kFinThreads;
+  __shared__ FinShared u;
+  __shared__ uint64_t s_sel[kPostMaxK];
+  __shared__ double s_red[NT / 32];
+  __shared__ unsigned s_last;
+  extern __shared__ __align__(16) unsigned char post_smem[];
+  griddep_wait();
+  griddep_launch();
+  const int B = static_cast<int>(gridDim.x) - R;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  if (static_cast<int>(blockIdx.x) < B) {
+    KTrace kt_(kKtEmit);
+    const int b = blockIdx.x;
+    fin_select_emit(scores, stride, fs, cand, cand_stride, ordered, status, b, u,
+                    reinterpret_cast<unsigned*>(post_smem));
+    __syncthreads();
+    if (tid == 0) {
+      __threadfence();
+      atomicExch(post + b, 1u);
+    }
+    return;
+  }
+  KTrace kt_(kKtRecompute);
+  const int j = blockIdx.x - B;
+  float* s_x = reinterpret_cast<float*>(post_smem);
+  constexpr int E = Vec16<T>::kElems;
+  const int64_t pitch_vec = static_cast<int64_t>(d) / E;
+  for (int b = 0; b < B; ++b) {
+    if (tid == 0) {
+      const unsigned long long t0 = gtimer();
+      while (ld_relaxed_gpu(post + b) == 0u && gtimer() - t0 < kFselTimeoutNs) __nanosleep(64);
+      fence_acq_rel_gpu();
+    }
+    block_copy(s_x, x + static_cast<int64_t>(b) * d, d);
+    __syncthreads();
+    for (int i = j * 32 + wid; i < kp; i += R * 32) {
+      const int64_t row = __ldcg(cand + static_cast<int64_t>(b) * cand_stride + i);
+      const float acc = post_row_dot<T, CPL>(w, pitch_vec, row, s_x, lane);
+      if (lane == 0) vals[static_cast<int64_t>(b) * kp + i] = apply_phi(phi, acc);
+    }
+    __syncthreads();
+    if (tid == 0) {
+      __threadfence();
+      s_last = atomicAdd(post + B + b, 1u) == static_cast<unsigned>(R - 1) ? 1u : 0u;
+      if (s_last) fence_acq_rel_gpu();
+    }
+    __syncthreads();
+    if (s_last) {
+      // final top-K of the kp exact values (ties by index), rank order
+      constexpr int KPT = kFinKpt;
+      RegKeys<KPT> src;
+#pragma unroll
+      for (int q = 0; q < KPT; ++q) {
+        const int i = tid * KPT + q;
+        src.k[q] = i < kp ? make_key(__ldcg(vals + static_cast<int64_t>(b) * kp + i),
+                                     __ldcg(cand + static_cast<int64_t>(b) * cand_stride + i))
+                          : 0ull;
+      }
+      const int Kq = min(K, kp);
+      const uint64_t T2 = Kq >= kp ? 1ull : block_range_select<NT>(src, kp, Kq, &u.rs);
+      int c = 0;
+#pragma unroll
+      for (int q = 0; q < KPT; ++q) c += (src.k[q] && src.k[q] >= T2) ? 1 : 0;
+      int total;
+      int pos = block_scan_excl<NT>(c, u.rs.scan, &total);
+#pragma unroll
+      for (int q = 0; q < KPT; ++q)
+        if (src.k[q] && src.k[q] >= T2) s_sel[pos++] = src.k[q];
+      __syncthreads();
+      const uint64_t mine = tid < Kq ? s_sel[tid] : 0ull;
+      int rank = 0;
+      for (int q = 0; q < Kq; ++q) rank += s_sel[q] > mine ? 1 : 0;
+      __syncthreads();
+      if (tid < Kq) s_sel[rank] = mine;
+      __syncthreads();
+      if (tid < Kq) {
+        out_idx[b * out_stride + tid] = key_index(s_sel[tid]);
+        out_val[b * out_stride + tid] = key_value(s_sel[tid]);
+      }
+      if (out_prob) {
+        // hire.hpp:135-142: p_i = float(exp(double(v_i) - v_max)) / double sum
+        const double vmax = static_cast<double>(key_value(s_sel[0]));
+        double local = 0.0;
+        for (int q = tid; q < Kq; q += NT) local += exp(static_cast<double>(key_value(s_sel[q])) - vmax);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) local += __shfl_xor_sync(0xffffffffu, local, o);
+        if (lane == 0) s_red[wid] = local;
+        __syncthreads();
+        double sum = 0.0;
+#pragma unroll
+        for (int v = 0; v < NT / 32; ++v) sum += s_red[v];
+        for (int q = tid; q < Kq; q += NT) {
+          const float pj = static_cast<float>(exp(static_cast<double>(key_value(s_sel[q])) - vmax));
+          out_prob[b * out_stride + q] = static_cast<float>(static_cast<double>(pj) / sum);
+        }
+      }
+      if (tid == 0) {
+        post[b] = 0u;
+        post[B + b] = 0u;
+      }
+    }
+    __syncthreads();  // s_x / s_sel reuse
   }
 }
 

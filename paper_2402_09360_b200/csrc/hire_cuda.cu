@@ -1045,8 +1045,49 @@ void take_topk_ws(Arena& ar, TopkWs* t, const hire_scorer_s* a, int64_t B, const
 }
 
 // prep_x -> fused proxy/filter kernel -> sel_fin_kernel
+// Everything after the proxy kernel in one launch (fsel_post_kernel): the
+// finisher, the exact recompute and the final top-k + softmax.
+struct FselPost {
+  const hire_matrix_s* w = nullptr;  // non-null: use the post kernel
+  int64_t k = 0;
+  uint32_t* top_idx = nullptr;
+  float* top_val = nullptr;
+  float* top_prob = nullptr;
+  int64_t out_stride = 0;
+};
+
+bool fsel_post_ok(const hire_matrix_s* w, const hire_topk_params* p, const SelPlan& sp, int64_t B, int num_sms) {
+  // opt-in (HIRE_FSEL_POST=1): measured slower than fin -> K4 -> K5 on B200
+  // (the recompute workers are latency-bound at 1024 threads / 64 registers)
+  const char* e = std::getenv("HIRE_FSEL_POST");
+  if (!e || e[0] != '1' || p->strict) return false;
+  const int64_t es = w->dtype == HIRE_BF16 ? 2 : 4;
+  const int64_t bytes = w->d * es;
+  if (bytes % 512 != 0) return false;
+  const int64_t cpl = bytes / 512;
+  if (cpl != 4 && cpl != 8 && cpl != 16) return false;
+  if (p->k > kPostMaxK || sp.k_eff > kFinCap || w->d * 4 > 64 * 1024) return false;
+  return B + 8 <= num_sms;
+}
+
+template <typename T, int CPL>
+int launch_post_t(hire_ctx ctx, const float* scores, int64_t stride, const FuseSel& fs, uint32_t* cand,
+                  int64_t cand_stride, int ordered, int* status, const void* w, int d, const float* x, int phi,
+                  float* vals, int kp, int K, const FselPost& po, unsigned* post, int B, int R, size_t smem) {
+  auto k = fsel_post_kernel<T, CPL>;
+  static size_t set = 0;
+  if (smem > set) {
+    CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    set = smem;
+  }
+  CK(launch_k(ctx, k, static_cast<unsigned>(B + R), kFinThreads, smem, scores, stride, fs, cand, cand_stride, ordered,
+              status, static_cast<const T*>(w), d, x, phi, vals, kp, K, po.top_idx, po.top_val, po.top_prob,
+              po.out_stride, post, R));
+  return HIRE_OK;
+}
+
 int run_scores_fsel(hire_ctx ctx, const hire_scorer_s* a, const float* x, int64_t B, int phi, const SelPlan& sp,
-                    const TopkWs& t, uint32_t* cand, bool ordered) {
+                    const TopkWs& t, uint32_t* cand, bool ordered, const FselPost* po = nullptr) {
   const FselPlan& f = t.fz;
   const int d = static_cast<int>(a->d);
   RET(ensure_mma_layout(ctx, const_cast<hire_scorer_s*>(a)));
@@ -1067,7 +1108,7 @@ int run_scores_fsel(hire_ctx ctx, const hire_scorer_s* a, const float* x, int64_
   fs.n_samp = f.n_samp;
   fs.r_lo = f.r_lo;
   {  // dedicated zero-at-rest buffer (the arena is shared with other ops)
-    const size_t need = static_cast<size_t>(B) * (kFselSampleMax + 2) * 8 + kFselCtr * 32 * 4;
+    const size_t need = static_cast<size_t>(B) * (kFselSampleMax + 2) * 8 + kFselCtr * 32 * 4 + static_cast<size_t>(B) * 8;
     if (need > ctx->fzero_cap) {
       if (ctx->fzero) {
         CK(cudaStreamSynchronize(ctx->stream));
@@ -1105,9 +1146,29 @@ int run_scores_fsel(hire_ctx ctx, const hire_scorer_s* a, const float* x, int64_
     HIRE_FS(1) else HIRE_FS(2) else HIRE_FS(4) else HIRE_FS(8)
 #undef HIRE_FS
   }
-  {
+  const size_t bm = static_cast<size_t>((a->rows + 31) / 32) * 4;
+  if (po && po->w) {
     StageScope scope(ctx, kStageSelect);
-    CK(launch_k(ctx, sel_fin_kernel, static_cast<unsigned>(B), kFinThreads, static_cast<size_t>((a->rows + 31) / 32) * 4, static_cast<const float*>(t.scores),
+    const hire_matrix_s* w = po->w;
+    const int dd = static_cast<int>(w->d);
+    const int64_t kp = sp.k_eff;
+    const int R = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(ctx->num_sms - B, ceil_div(B * kp, 32))));
+    const size_t smem = std::max(bm, static_cast<size_t>(dd) * 4);
+    unsigned* post = fs.ctr + kFselCtr * 32;
+    const int cpl = static_cast<int>(dd * (w->dtype == HIRE_BF16 ? 2 : 4) / 512);
+    const int K = static_cast<int>(std::min<int64_t>(po->k, kp));
+#define HIRE_PO(TT, C)                                                                                           \
+    RET((launch_post_t<TT, C>(ctx, t.scores, a->rows, fs, cand, kp, ordered ? 1 : 0, t.status, w->ptr, dd, x, phi, \
+                              t.vals, static_cast<int>(kp), K, *po, post, static_cast<int>(B), R, smem)))
+    if (w->dtype == HIRE_BF16) {
+      if (cpl == 4) HIRE_PO(__nv_bfloat16, 4); else if (cpl == 8) HIRE_PO(__nv_bfloat16, 8); else HIRE_PO(__nv_bfloat16, 16);
+    } else {
+      if (cpl == 4) HIRE_PO(float, 4); else if (cpl == 8) HIRE_PO(float, 8); else HIRE_PO(float, 16);
+    }
+#undef HIRE_PO
+  } else {
+    StageScope scope(ctx, kStageSelect);
+    CK(launch_k(ctx, sel_fin_kernel, static_cast<unsigned>(B), kFinThreads, bm, static_cast<const float*>(t.scores),
                 a->rows, fs, cand, sp.k_eff, ordered ? 1 : 0, t.status));
   }
   CK(cudaGetLastError());
@@ -1696,10 +1757,22 @@ int hire_topk_run(hire_ctx ctx, hire_matrix w, hire_scorer a, const float* x, in
   TopkWs t;
   take_topk_ws(ar, &t, a, B, sp, true, ctx, p);
   RET(ar.commit(ctx));
-  RET(local_candidates(ctx, w, a, x, B, p, sp, t, t.cand, cand != nullptr));
   const int64_t take = std::min<int64_t>(p->k, sp.k_eff);
-  RET(run_final(ctx, t.vals, sp.k_eff, t.cand, sp.k_eff, nullptr, 0, 0, sp.k_eff, take, B, 0, top_idx,
-                top_val, top_prob, nullptr, p->k));
+  if (t.fz.on && fsel_post_ok(w, p, sp, B, ctx->num_sms)) {
+    // one launch after the proxy kernel: finisher + recompute + final top-k
+    FselPost po;
+    po.w = w;
+    po.k = p->k;
+    po.top_idx = top_idx;
+    po.top_val = top_val;
+    po.top_prob = top_prob;
+    po.out_stride = p->k;
+    RET(run_scores_fsel(ctx, a, x, B, p->phi, sp, t, t.cand, cand != nullptr, &po));
+  } else {
+    RET(local_candidates(ctx, w, a, x, B, p, sp, t, t.cand, cand != nullptr));
+    RET(run_final(ctx, t.vals, sp.k_eff, t.cand, sp.k_eff, nullptr, 0, 0, sp.k_eff, take, B, 0, top_idx,
+                  top_val, top_prob, nullptr, p->k));
+  }
   if (cand) CK(cudaMemcpy2DAsync(cand, p->k_prime * 4, t.cand, sp.k_eff * 4, sp.k_eff * 4, B,
                                  cudaMemcpyDeviceToDevice, ctx->stream));
   if (n_cand) *n_cand = sp.k_eff;

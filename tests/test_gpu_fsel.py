@@ -137,3 +137,22 @@ def test_fused_unordered_candidates_same_topk(H, O):
     for b in range(B):
         want, _ = _want_cand(O, codes, scales, x[b], kp)
         assert np.array_equal(N(r1.cand[b]).astype(np.uint32), want)
+
+
+def test_fused_post_kernel_equals_chain(H, O, monkeypatch):
+    # opt-in single post-proxy launch (finisher + recompute + final top-k)
+    V, d, k, kp, B = 60000, 256, 32, 512, 3
+    w, z, a, codes, scales = _instance(H, O, V, d, 31)
+    x = _data.queries(B, d, 32)
+    cfg = H.HireConfig(k=k, k_prime=kp, x_mode=H.X_INT8)
+    r0 = H.hire_topk(T(x), z, a, cfg)
+    i0, p0 = H.softmax_topk(z, T(x), a, cfg)
+    monkeypatch.setenv("HIRE_FSEL_POST", "1")
+    for _ in range(2):
+        r1 = H.hire_topk(T(x), z, a, cfg)
+        i1, p1 = H.softmax_topk(z, T(x), a, cfg)
+        assert torch.equal(r0.cand, r1.cand)
+        assert torch.equal(r0.top_idx, r1.top_idx)
+        assert torch.equal(r0.top_val, r1.top_val)
+        assert torch.equal(i0, i1)
+        torch.testing.assert_close(p0, p1, rtol=1e-6, atol=0)
