@@ -58,9 +58,12 @@ __device__ __forceinline__ int fs_scan_excl(int v, int* s_tmp, int* total) {
 
 // K-th largest (1 <= K <= number of non-zero keys) of the CTA's keys.
 // Block-uniform result. Every thread of the CTA (NT of them) must call it.
+// sf != nullptr: the keys are make_key(sf[i], i) for i < nf, read from
+// shared memory (rows too long for registers); keys[] is then unused.
 template <int NT, int KPT>
 __device__ __forceinline__ uint64_t block_fast_select(const uint64_t (&keys)[KPT], long long K, FastSelScratch* s,
-                                                      unsigned long long* tr = nullptr) {
+                                                      unsigned long long* tr = nullptr, const float* sf = nullptr,
+                                                      unsigned nf = 0) {
   int trn = 0;  // debug timeline: tr[0..7] = %globaltimer after each phase (thread 0)
   auto stamp = [&]() {
     if (tr && threadIdx.x == 0 && trn < 8) tr[trn] = gtimer();
@@ -80,8 +83,14 @@ __device__ __forceinline__ uint64_t block_fast_select(const uint64_t (&keys)[KPT
     *x = phase == 0 ? hi32 : static_cast<unsigned>(k);
     return k != 0 && (phase == 0 || hi32 == vstar);
   };
+  if (sf) src = -2;
   auto each = [&](auto f) {
-    if (src < 0) {
+    if (src == -2) {  // shared-memory scores, uniform trip count
+      for (unsigned i0 = 0; i0 < nf; i0 += NT) {
+        const unsigned i = i0 + tid;
+        f(i < nf ? make_key(sf[i], i) : 0ull);
+      }
+    } else if (src < 0) {
 #pragma unroll
       for (int j = 0; j < KPT; ++j) f(keys[j]);
     } else {  // uniform trip count: f may use warp collectives

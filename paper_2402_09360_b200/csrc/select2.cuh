@@ -499,6 +499,60 @@ __global__ void __launch_bounds__(NT) sel_exact_kernel(
 }
 
 // ---------------------------------------------------------------------
+// Mid-size rows (kSel2Exact < n <= kSmemRowMax): one 1024-thread CTA per
+// query holds the whole score row in shared memory; T = the K-th largest
+// key by block_fast_select over the shared-memory row; ordered emit with
+// warp-owned contiguous slices (count pass -> warp prefix -> write pass).
+// One launch instead of the grid-wide pivot / window / window-select / emit.
+// ---------------------------------------------------------------------
+constexpr int kSmemRowMax = 49152;  // 192 KB of fp32 scores
+
+__global__ void __launch_bounds__(1024, 1) sel_smem_kernel(
+    const float* __restrict__ scores, int64_t stride, uint32_t n, uint32_t K,
+    uint32_t* __restrict__ cand, int64_t cand_stride) {
+  constexpr int NT = 1024, NW = NT / 32;
+  __shared__ FastSelScratch fss;
+  __shared__ unsigned s_wc[NW];
+  extern __shared__ __align__(16) unsigned char row_smem[];
+  float* sr = reinterpret_cast<float*>(row_smem);
+  hire_dev::griddep_wait();
+  hire_dev::griddep_launch();
+  KTrace kt_(kKtPivot);
+  const int b = blockIdx.x;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const float* row = scores + b * stride;
+  if ((reinterpret_cast<uintptr_t>(row) & 15) == 0 && (n & 3) == 0) {
+    block_copy_tf<8, float4>(reinterpret_cast<float4*>(sr), static_cast<int>(n / 4),
+                             [&](int i) { return __ldcg(reinterpret_cast<const float4*>(row) + i); });
+  } else {
+    block_copy_tf<8, float>(sr, static_cast<int>(n), [&](int i) { return __ldcg(row + i); });
+  }
+  __syncthreads();
+  const uint64_t dummy[1] = {0ull};
+  const uint64_t T = block_fast_select<NT, 1>(dummy, K, &fss, nullptr, sr, n);
+  // warp w owns [w*span, (w+1)*span), 32 elements per step (lane = element)
+  const uint32_t span = ((n + NW - 1) / NW + 31) / 32 * 32;
+  const uint32_t w0 = wid * span, w1 = min(n, w0 + span);
+  unsigned c = 0;
+  for (uint32_t i0 = w0; i0 < w1; i0 += 32) {
+    const uint32_t i = i0 + lane;
+    c += __popc(__ballot_sync(0xffffffffu, i < w1 && make_key(sr[i], i) >= T));
+  }
+  if (lane == 0) s_wc[wid] = c;
+  __syncthreads();
+  unsigned pos = 0;
+  for (int v = 0; v < wid; ++v) pos += s_wc[v];
+  uint32_t* out = cand + b * cand_stride;
+  for (uint32_t i0 = w0; i0 < w1; i0 += 32) {
+    const uint32_t i = i0 + lane;
+    const bool in = i < w1 && make_key(sr[i], i) >= T;
+    const unsigned bal = __ballot_sync(0xffffffffu, in);
+    if (in) out[pos + __popc(bal & ((1u << lane) - 1u))] = i;
+    pos += __popc(bal);
+  }
+}
+
+// ---------------------------------------------------------------------
 // S1 (large rows). One 128-thread CTA per query: 2048 sampled keys (512
 // blocks of 4 consecutive rows, block ids s * perm mod nblk), pivots from
 // two sample order statistics -> piv[b] = {lo, hi}.
