@@ -248,7 +248,9 @@ int ensure_host(void** buf, size_t* cap, size_t need, cudaStream_t s) {
     *buf = nullptr;
   }
   size_t n = std::max(need, *cap * 2);
-  CK(cudaMallocHost(buf, n));
+  // mapped: the kernels read the inputs and write the results straight
+  // through PCIe (a copy-engine transfer costs ~10 us of setup latency)
+  CK(cudaHostAlloc(buf, n, cudaHostAllocMapped | cudaHostAllocPortable));
   *cap = n;
   return HIRE_OK;
 }
@@ -835,6 +837,31 @@ int run_final(hire_ctx ctx, const float* vals, int64_t vs, const uint32_t* idx, 
   return HIRE_OK;
 }
 
+// Host-call inputs: pinned (mapped) host memory -> device, 16 B per thread,
+// read straight over PCIe (no copy-engine transfer in the call's graph).
+__global__ void fetch_host_kernel(const uint4* __restrict__ src, uint4* __restrict__ dst, int64_t n16) {
+  hire_dev::griddep_wait();
+  hire_dev::griddep_launch();
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n16;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    dst[i] = src[i];
+}
+
+// H2D of a host call's inputs: the fetch kernel when aligned, else a copy.
+int fetch_inputs(hire_ctx ctx, void* dst, const void* host_src, size_t bytes) {
+  void* dsrc = nullptr;
+  if (bytes % 16 == 0 && (reinterpret_cast<uintptr_t>(host_src) & 15) == 0 &&
+      cudaHostGetDevicePointer(&dsrc, const_cast<void*>(host_src), 0) == cudaSuccess && dsrc) {
+    const int64_t n16 = static_cast<int64_t>(bytes / 16);
+    const unsigned grid = static_cast<unsigned>(std::min<int64_t>(ceil_div(n16, 256), 64));
+    CK(launch_k(ctx, fetch_host_kernel, grid, 256, 0, static_cast<const uint4*>(dsrc), static_cast<uint4*>(dst), n16));
+    return HIRE_OK;
+  }
+  cudaGetLastError();
+  CK(cudaMemcpyAsync(dst, host_src, bytes, cudaMemcpyHostToDevice, ctx->stream));
+  return HIRE_OK;
+}
+
 __global__ void add_offset_kernel(uint32_t* idx, int64_t n, uint32_t off) {
   hire_dev::griddep_wait();
   hire_dev::griddep_launch();
@@ -1206,17 +1233,22 @@ namespace {
 // body(stream) issues the whole host call (copies + kernels) on ctx->stream
 // and fills out[4]. First call per key: eager. Second: captured on gstream,
 // instantiated, launched. Later: launched. The caller synchronises.
+// *done_on = the stream the caller synchronises on.
 template <class Body>
-int run_host_graph(hire_ctx ctx, const std::vector<int64_t>& key, int64_t* out, Body body) {
+int run_host_graph(hire_ctx ctx, const std::vector<int64_t>& key, int64_t* out, cudaStream_t* done_on, Body body) {
+  *done_on = ctx->stream;
   if (!ctx->host_graphs || ctx->prof) return body(out);
   const auto bufs = ctx->buf_snapshot();
   for (auto& g : ctx->hgraphs)
     if (g.key == key && g.bufs == bufs) {
-      CK(cudaEventRecord(ctx->gev, ctx->stream));
-      CK(cudaStreamWaitEvent(ctx->gstream, ctx->gev, 0));
+      // order after earlier work on the context stream only if there is any
+      if (cudaStreamQuery(ctx->stream) != cudaSuccess) {
+        cudaGetLastError();
+        CK(cudaEventRecord(ctx->gev, ctx->stream));
+        CK(cudaStreamWaitEvent(ctx->gstream, ctx->gev, 0));
+      }
       CK(cudaGraphLaunch(g.exec, ctx->gstream));
-      CK(cudaEventRecord(ctx->gev, ctx->gstream));
-      CK(cudaStreamWaitEvent(ctx->stream, ctx->gev, 0));
+      *done_on = ctx->gstream;  // the host call blocks on it: no event back
       for (int i = 0; i < 4; ++i) out[i] = g.out[i];
       return HIRE_OK;
     }
@@ -1264,8 +1296,7 @@ int run_host_graph(hire_ctx ctx, const std::vector<int64_t>& key, int64_t* out, 
   CK(ei);
   ctx->hgraphs.push_back({key, bufs, exec, {out[0], out[1], out[2], out[3]}});
   CK(cudaGraphLaunch(exec, ctx->gstream));
-  CK(cudaEventRecord(ctx->gev, ctx->gstream));
-  CK(cudaStreamWaitEvent(ctx->stream, ctx->gev, 0));
+  *done_on = ctx->gstream;
   return HIRE_OK;
 }
 }  // namespace
@@ -1784,7 +1815,7 @@ int hire_topk_run(hire_ctx ctx, hire_matrix w, hire_scorer a, const float* x, in
                   top_val, top_prob, nullptr, p->k));
   }
   if (cand) CK(cudaMemcpy2DAsync(cand, p->k_prime * 4, t.cand, sp.k_eff * 4, sp.k_eff * 4, B,
-                                 cudaMemcpyDeviceToDevice, ctx->stream));
+                                 cudaMemcpyDefault, ctx->stream));
   if (n_cand) *n_cand = sp.k_eff;
   if (n_top) *n_top = take;
   if (clamped) *clamped = sp.clamped || take < p->k;
@@ -1815,9 +1846,10 @@ int hire_topk_host(hire_ctx ctx, hire_matrix w, hire_scorer a, const float* x_ho
                                     p->phi, p->x_mode, p->select, p->strict, p->n_buckets, p->bucket_t,
                                     cb ? 1 : 0, pb ? 1 : 0};
   int64_t res[4];
-  RET(run_host_graph(ctx, key, res, [&](int64_t* r) -> int {
-    CK(cudaMemcpyAsync(dv, hs, xb, cudaMemcpyHostToDevice, ctx->stream));
-    char* o = dv + in_bytes;
+  cudaStream_t done_on = nullptr;
+  RET(run_host_graph(ctx, key, res, &done_on, [&](int64_t* r) -> int {
+    RET(fetch_inputs(ctx, dv, hs, xb));
+    char* o = hs + in_bytes;  // results are written straight into mapped host memory
     uint32_t* dcand = cb ? reinterpret_cast<uint32_t*>(o) : nullptr;
     o += align_up(cb);
     uint32_t* didx = reinterpret_cast<uint32_t*>(o);
@@ -1829,13 +1861,12 @@ int hire_topk_host(hire_ctx ctx, hire_matrix w, hire_scorer a, const float* x_ho
     RET(hire_topk_run(ctx, w, a, reinterpret_cast<const float*>(dv), B, p, dcand, didx, dval, dprob, &r[0], &r[1],
                       &cl));
     r[2] = cl;
-    CK(cudaMemcpyAsync(hs + in_bytes, dv + in_bytes, out_bytes, cudaMemcpyDeviceToHost, ctx->stream));
     return HIRE_OK;
   }));
   if (n_cand) *n_cand = res[0];
   if (n_top) *n_top = res[1];
   if (clamped) *clamped = static_cast<int>(res[2]);
-  CK(cudaStreamSynchronize(ctx->stream));
+  CK(cudaStreamSynchronize(done_on));
   const char* ho = hs + in_bytes;
   (void)take;
   if (cb) std::memcpy(cand_host, ho, cb);
@@ -2083,18 +2114,31 @@ int hire_ffn_host(hire_ctx ctx, hire_matrix u, hire_matrix v, hire_scorer a, con
   char* dv = static_cast<char*>(ctx->io_dev);
   char* hs = static_cast<char*>(ctx->io_host);
   std::memcpy(hs, x_host, xb);
+  // the output rows are written straight into mapped host memory; the unit
+  // ids stay on the device (the down-projection reads them) and are stored
+  // to the host by a small kernel at the end
   uint32_t* dsel = reinterpret_cast<uint32_t*>(dv + in_bytes);
-  float* dout = reinterpret_cast<float*>(dv + in_bytes + align_up(sb));
+  uint32_t* hsel = reinterpret_cast<uint32_t*>(hs + in_bytes);
+  float* dout = reinterpret_cast<float*>(hs + in_bytes + align_up(sb));
   const std::vector<int64_t> key = {2, reinterpret_cast<int64_t>(u), reinterpret_cast<int64_t>(v), reinterpret_cast<int64_t>(a),
                                     B, p->k, p->k_prime, p->group_size, p->phi, p->x_mode, p->strict};
   int64_t res[4];
-  RET(run_host_graph(ctx, key, res, [&](int64_t*) -> int {
-    CK(cudaMemcpyAsync(dv, hs, xb, cudaMemcpyHostToDevice, ctx->stream));
+  cudaStream_t done_on = nullptr;
+  RET(run_host_graph(ctx, key, res, &done_on, [&](int64_t*) -> int {
+    RET(fetch_inputs(ctx, dv, hs, xb));
     RET(hire_ffn_run(ctx, u, v, a, reinterpret_cast<const float*>(dv), B, p, dsel, dout));
-    CK(cudaMemcpyAsync(hs + in_bytes, dv + in_bytes, out_bytes, cudaMemcpyDeviceToHost, ctx->stream));
+    if (sel_host) {
+      if (sb % 16 == 0) {
+        const int64_t n16 = static_cast<int64_t>(sb / 16);
+        CK(launch_k(ctx, fetch_host_kernel, static_cast<unsigned>(std::min<int64_t>(ceil_div(n16, 256), 64)), 256, 0,
+                    reinterpret_cast<const uint4*>(dsel), reinterpret_cast<uint4*>(hsel), n16));
+      } else {
+        CK(cudaMemcpyAsync(hsel, dsel, sb, cudaMemcpyDefault, ctx->stream));
+      }
+    }
     return HIRE_OK;
   }));
-  CK(cudaStreamSynchronize(ctx->stream));
+  CK(cudaStreamSynchronize(done_on));
   if (sel_host) std::memcpy(sel_host, hs + in_bytes, sb);
   std::memcpy(out_host, hs + in_bytes + align_up(sb), ob);
   return HIRE_OK;
