@@ -185,6 +185,11 @@ class FfnWorkload:
     def proxy_bytes(self):
         return self.m * (self.d // 2 + 4)  # int4 codes + fp32 scale per row
 
+    def kernel_bytes(self):
+        """Bytes each gather kernel reads per step (per query, no union):
+        K4 recompute reads B*k' U rows, K6 the B*k selected V rows."""
+        return {"recompute": self.B * self.kp * self.d * 2, "down": self.B * self.k * self.d * 2}
+
     def step_bytes(self, x):
         """Roofline bytes for one step: proxy + unique gathered U rows (k'
         candidates, union over the batch) + unique V rows (k selected)."""
@@ -261,6 +266,9 @@ class SoftmaxWorkload:
 
     def proxy_bytes(self):
         return self.V * (self.d // 2 + 4)
+
+    def kernel_bytes(self):
+        return {"recompute": self.B * self.kp * self.d * 2}
 
     def step_bytes(self, x):
         r = self.H.hire_topk(x, self.W, self.A, self.cfg)
@@ -340,6 +348,9 @@ class LowRankSoftmaxWorkload:
 
     def proxy_bytes(self):
         return (self.V + self.d) * self.r * 4
+
+    def kernel_bytes(self):
+        return {"recompute": self.B * self.kp * self.d * 4}
 
     def step_bytes(self, x):
         z, a = self.copies[0]
@@ -422,6 +433,9 @@ class DaSoftmaxWorkload:
 
     def proxy_bytes(self):
         return (self.width + self.d) * self.r * 2
+
+    def kernel_bytes(self):
+        return {"recompute": self.B * self.P.quota(self.kp, self.world, self.rank) * self.d * 2}
 
     def step_bytes(self, x):
         # local candidates of this shard: union over the batch of k'/D rows
@@ -728,6 +742,11 @@ def run_ours(args):
                      "frac_device_span": round(pb / (dspan * 1e-6) / 1e9 / peaks["hbm_gbs"], 4) if dspan else None,
                      "peak_src": peaks["src"]},
         "step_timeline_us": {k: v for k, v in (spans or {}).items() if isinstance(v, tuple)},
+        "kernel_roofline": {k: {"bytes": b, "span_us": round(spans[k][1] - spans[k][0], 3),
+                                "gbs": round(b / ((spans[k][1] - spans[k][0]) * 1e-6) / 1e9, 1),
+                                "frac": round(b / ((spans[k][1] - spans[k][0]) * 1e-6) / 1e9 / peaks["hbm_gbs"], 4)}
+                            for k, b in (wl.kernel_bytes().items() if hasattr(wl, "kernel_bytes") else [])
+                            if spans and k in spans and spans[k][1] > spans[k][0]},
         "step_roofline": {"bytes": step_b, "unique_u_rows": nu, "unique_v_rows": nv,
                           "achieved_gbs": round(step_b / (ms_step * 1e-3) / 1e9, 1),
                           "frac": round(step_b / (ms_step * 1e-3) / 1e9 / peaks["hbm_gbs"], 4)},

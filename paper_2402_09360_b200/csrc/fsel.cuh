@@ -117,14 +117,16 @@ __global__ void __launch_bounds__(256, HIRE_FSEL_MINB) q4_score_mma_sel(
   const int64_t n_rb = (rows + 15) / 16;
   const int rb_local = wid / KS, ks = wid % KS;
   const int kb0 = ks * nkb / KS, kb1 = (ks + 1) * nkb / KS;
-  const int G = fs.g_stream, c = blockIdx.x;
+  // the bracket CTAs take the lowest block ids (scheduled first even when a
+  // predecessor kernel still holds a few slots); streaming CTA c = id - nbrk
+  const int G = fs.g_stream, c = static_cast<int>(blockIdx.x) - fs.nbrk;
   const int64_t U = static_cast<int64_t>(G) * RPC;
   const int rounds = static_cast<int>((n_rb + U - 1) / U);
 
   constexpr int UL = 4;
   uint4 a[UL];
   // prologue independent of the producer kernel: first weight loads
-  if (c < G) {
+  if (c >= 0) {
     const int64_t rb = static_cast<int64_t>(c) * RPC + rb_local;
     if (rb < n_rb) {
 #pragma unroll
@@ -137,10 +139,10 @@ __global__ void __launch_bounds__(256, HIRE_FSEL_MINB) q4_score_mma_sel(
   KTrace kt_(kKtProxy);
 
   // ---- B: bracket CTAs ----
-  if (c >= G) {
+  if (c < 0) {
     constexpr int KPT = kFselSampleMax / 256;
     const int S = fs.n_samp;
-    for (int b = c - G; b < B; b += fs.nbrk) {
+    for (int b = static_cast<int>(blockIdx.x); b < B; b += fs.nbrk) {
       const unsigned long long* sp = reinterpret_cast<const unsigned long long*>(fs.samp) +
                                      static_cast<int64_t>(b) * kFselSampleMax;
       const unsigned long long t0 = gtimer();

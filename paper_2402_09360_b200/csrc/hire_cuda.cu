@@ -434,6 +434,9 @@ int run_select(hire_ctx ctx, const float* scores, int64_t score_stride, int64_t 
       else if (variant == 2 && n <= 8192)
         CK(launch_k(ctx, sel_exact_kernel<256, 32>, static_cast<unsigned>(B), 256, 0, scores, score_stride, nn, K,
                     cand, cand_stride));
+      else if (variant == 3 && n <= 8192)
+        CK(launch_k(ctx, sel_exact_kernel<1024, 8>, static_cast<unsigned>(B), 1024, 0, scores, score_stride, nn, K,
+                    cand, cand_stride));
       else
         CK(launch_k(ctx, sel_exact_kernel<512, 16>, static_cast<unsigned>(B), 512, 0, scores, score_stride, nn, K,
                     cand, cand_stride));
