@@ -628,7 +628,10 @@ __device__ __forceinline__ unsigned win_bin(uint64_t k, unsigned vlo, int sh) {
 // aggregate agg[b][c] for S3.
 // ---------------------------------------------------------------------
 constexpr int kWinThreads = 256;
-constexpr int kScanBatch = 8;
+#ifndef HIRE_SCAN_BATCH
+#define HIRE_SCAN_BATCH 8
+#endif
+constexpr int kScanBatch = HIRE_SCAN_BATCH;  // score loads in flight per thread (S2 / S3)
 
 __global__ void __launch_bounds__(kWinThreads) sel_window_kernel(
     const float* __restrict__ scores, int64_t stride, uint32_t n, const uint64_t* __restrict__ piv,
