@@ -775,9 +775,11 @@ int run_recompute(hire_ctx ctx, const hire_matrix_s* m, const uint32_t* cand, in
   const int d = static_cast<int>(m->d);
   const size_t es = dtype_size(m->dtype);
   const int64_t bytes = static_cast<int64_t>(d) * static_cast<int64_t>(es);
-  // bulk-copy ring for large gathers (many rows per SM); the register
-  // version has less set-up latency for a few thousand rows
-  if (!strict && bytes % 512 == 0 && n_cand * B >= 8192 && !std::getenv("HIRE_RECOMPUTE_REGS")) {
+  // bulk-copy ring: opt-in (HIRE_RECOMPUTE_TMA=1). Measured on B200 the
+  // register path is faster at every batch (cfg3 B=8: 8.0 vs 12.6 us, B=32:
+  // 23 vs 46 us; cfg4: 61 vs 63 us)
+  const bool tma = std::getenv("HIRE_RECOMPUTE_TMA") != nullptr;
+  if (!strict && bytes % 512 == 0 && n_cand * B >= 8192 && tma) {
     bool done = false;
     if (m->dtype == HIRE_BF16)
       RET(launch_recompute_tma<__nv_bfloat16>(ctx, m->ptr, d, cand, cand_stride, n_cand, x, B, phi, out, out_stride, &done));

@@ -347,3 +347,16 @@ def test_ffn_fused_equals_unfused_and_oracle(H, O, B, monkeypatch):
         assert_sets_near_tie(N(sel_f[b]), ids, acts)
         if set(N(sel_f[b]).tolist()) == set(ids.tolist()):
             np.testing.assert_allclose(N(out_f[b]), want, rtol=1e-3, atol=1e-3 * np.abs(want).max())
+
+
+def test_recompute_bulk_copy_ring_equals_register_path(H, O, monkeypatch):
+    # recompute_tma (opt-in) and recompute_fast share the arithmetic: identical values
+    V, d, k, kp, B = 50000, 2048, 64, 1024, 9
+    w, z, a, codes, scales = _q4_instance(H, O, V, d, 77)
+    x = _data.queries(B, d, 78)
+    cfg = H.HireConfig(k=k, k_prime=kp, x_mode=H.X_INT8)
+    r0 = H.hire_topk(T(x), z, a, cfg)
+    monkeypatch.setenv("HIRE_RECOMPUTE_TMA", "1")
+    r1 = H.hire_topk(T(x), z, a, cfg)
+    assert torch.equal(r0.top_idx, r1.top_idx)
+    assert torch.equal(r0.top_val, r1.top_val)
