@@ -2285,6 +2285,13 @@ int hire_da_topk_run(hire_ctx ctx, hire_comm comm, hire_matrix w, hire_scorer a,
   if (w->rows != width) return invalid("da_topk: shard has " + std::to_string(w->rows) + " rows, width rule says " + std::to_string(width));
   DaPlan dp;
   RET(plan_da(p, width, world, rank, merge, uneven, &dp));
+  if (world == 1 && !std::getenv("HIRE_DA_SINGLE_GENERIC")) {
+    // one shard: DA-TOP-k is hire_topk itself (distributed.hpp:94-131 with
+    // s = 1; the reference's s = 1 equivalence, test_distributed.cpp:104-117)
+    // — no key hand-off and no second final selection
+    int64_t nc = 0;
+    return hire_topk_run(ctx, w, a, x, B, p, nullptr, top_idx, top_val, nullptr, &nc, n_top, clamped);
+  }
   // send/recv keys live in io_dev (separate from the per-stage workspace)
   const size_t sendb = align_up(static_cast<size_t>(B * dp.kq_max) * 8);
   const size_t recvb = align_up(static_cast<size_t>(world * B * dp.kq_max) * 8);

@@ -360,3 +360,19 @@ def test_recompute_bulk_copy_ring_equals_register_path(H, O, monkeypatch):
     r1 = H.hire_topk(T(x), z, a, cfg)
     assert torch.equal(r0.top_idx, r1.top_idx)
     assert torch.equal(r0.top_val, r1.top_val)
+
+
+@pytest.mark.parametrize("merge", [0, 1])
+def test_da_topk_run_single_rank_equals_oracle(H, O, merge):
+    # hire_da_topk_run with world = 1 (the bench's cfg4 at N = 1): one shard
+    import paper_2402_09360_b200.parallel as P
+    V, d, k, kp = 30000, 1024, 64, 512
+    w, z, a, codes, scales = _q4_instance(H, O, V, d, 81)
+    x = _data.queries(2, d, 82)
+    cfg = H.HireConfig(k=k, k_prime=kp, x_mode=H.X_INT8, strict=True)
+    ti, tv, cl = P.da_topk(z, a, V, T(x), cfg, None, merge=merge)
+    for b in range(2):
+        scores = O.q4_scores_int8(codes, scales, x[b], 0)
+        wi, wv, wcl, _ = O.da_topk(w, x[b], scores, 1, k, kp, 0, merge=merge)
+        assert np.array_equal(N(ti[b]).astype(np.uint32), wi)
+        assert np.array_equal(N(tv[b]).view(np.uint32), wv.view(np.uint32))
