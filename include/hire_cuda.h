@@ -185,6 +185,16 @@ HIRE_API int hire_ffn_host(hire_ctx ctx, hire_matrix u, hire_matrix v, hire_scor
 /* dense FFN (ffn.hpp:65-76), the baseline */
 HIRE_API int hire_ffn_dense_run(hire_ctx ctx, hire_matrix u, hire_matrix v, const float* x, int64_t B,
                        int phi, int strict, float* out);
+/* union_group_select (ffn.hpp:237-253): the sorted union of the B per-sample
+ * select_groups results. ids: device, capacity m / g; *n_ids = |union|
+ * (host, the call synchronises). */
+HIRE_API int hire_ffn_union_select(hire_ctx ctx, hire_matrix u, hire_scorer a, const float* x, int64_t B,
+                                   const hire_ffn_params* p, uint32_t* ids, int64_t* n_ids);
+/* ffn_common_path (ffn.hpp:223-234): ffn_dense over the dense part (du, dv;
+ * both NULL or 0 rows = none) plus ffn_group_sparse over the sparse part. */
+HIRE_API int hire_ffn_common_path_run(hire_ctx ctx, hire_matrix du, hire_matrix dv, hire_matrix u, hire_matrix v,
+                                      hire_scorer a, const float* x, int64_t B, const hire_ffn_params* p,
+                                      float* out);
 
 /* ---- DA-TOP-k (distributed.hpp:73-206) ----------------------------------- */
 HIRE_API int hire_comm_unique_id(uint8_t id[128]);

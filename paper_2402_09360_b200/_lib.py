@@ -33,7 +33,7 @@ EXPORTS = [
     "hire_scorer_info", "hire_scorer_destroy",
     "hire_scores", "hire_matvec", "hire_topk_select",
     "hire_topk_run", "hire_topk_host",
-    "hire_ffn_run", "hire_ffn_host", "hire_ffn_dense_run",
+    "hire_ffn_run", "hire_ffn_host", "hire_ffn_dense_run", "hire_ffn_union_select", "hire_ffn_common_path_run",
     "hire_comm_unique_id", "hire_comm_create", "hire_comm_destroy",
     "hire_da_topk_run", "hire_da_topk_emulated", "hire_da_ffn_run", "hire_da_ffn_emulated",
 ]
@@ -106,6 +106,8 @@ def _sig(L):
         "hire_ffn_run": [_vp, _vp, _vp, _vp, _vp, _i64, _p(FfnParams), _vp, _vp],
         "hire_ffn_host": [_vp, _vp, _vp, _vp, _vp, _i64, _p(FfnParams), _vp, _vp],
         "hire_ffn_dense_run": [_vp, _vp, _vp, _vp, _i64, _i32, _i32, _vp],
+        "hire_ffn_union_select": [_vp, _vp, _vp, _vp, _i64, _vp, _vp, _p(_i64)],
+        "hire_ffn_common_path_run": [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _i64, _vp, _vp],
         "hire_comm_unique_id": [_vp],
         "hire_comm_create": [_vp, _i32, _i32, _p(_vp)],
         "hire_comm_destroy": [_vp],

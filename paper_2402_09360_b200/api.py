@@ -384,6 +384,59 @@ def ffn_dense(f: GroupedFFN, x: torch.Tensor, strict: bool = False, ctx: Optiona
     return out
 
 
+def union_group_select(f: GroupedFFN, xs: torch.Tensor, a: ApproxScorer, k: int, k_prime: int,
+                       x_mode: int = L.X_FP32, strict: bool = False, ctx: Optional[Context] = None) -> np.ndarray:
+    """ffn.hpp:237-253: sorted union of the per-sample select_groups results
+    (the paper's dynamic overlap across a batch)."""
+    ctx = ctx or default_context()
+    xs = _x2d(xs, f.u.d)
+    g = f.group_size
+    ids = torch.empty(max(f.u.rows // max(g, 1), 1), dtype=torch.int32, device=xs.device)
+    n = C.c_int64()
+    p = L.FfnParams(k, k_prime, g, _phi(f.phi), x_mode, int(strict), 0)
+    check(lib().hire_ffn_union_select(ctx.h, f.u.h, a.h, _ptr(xs), xs.shape[0], C.byref(p), _ptr(ids), C.byref(n)))
+    return ids[:n.value].cpu().numpy().astype(np.uint32)
+
+
+@dataclass
+class CommonPathFFN:
+    """ffn.hpp:44-47: a dense part (every unit, every token) plus a
+    group-sparse part; `dense_part` None = no dense units."""
+    dense_part: Optional[GroupedFFN]
+    sparse_part: GroupedFFN
+
+
+def ffn_common_path(c: CommonPathFFN, x: torch.Tensor, a: ApproxScorer, k: int, k_prime: int,
+                    x_mode: int = L.X_FP32, strict: bool = False, ctx: Optional[Context] = None) -> torch.Tensor:
+    """ffn.hpp:223-234: ffn_dense(dense part) + ffn_group_sparse(sparse part)."""
+    ctx = ctx or default_context()
+    sp = c.sparse_part
+    x = _x2d(x, sp.u.d)
+    out = torch.empty(x.shape[0], sp.u.d, dtype=torch.float32, device=x.device)
+    p = L.FfnParams(k, k_prime, sp.group_size, _phi(sp.phi), x_mode, int(strict), 0)
+    du = c.dense_part.u.h if c.dense_part is not None else None
+    dv = c.dense_part.v.h if c.dense_part is not None else None
+    check(lib().hire_ffn_common_path_run(ctx.h, du, dv, sp.u.h, sp.v.h, a.h, _ptr(x), x.shape[0], C.byref(p),
+                                         _ptr(out)))
+    return out
+
+
+def overlap_ratio(per_sample_sets, k_groups: int) -> float:
+    """metrics.hpp:68-88: |union| / (s * k_groups); 1/s when every sample
+    selects the same groups, 1 when the selections are disjoint."""
+    if len(per_sample_sets) == 0:
+        raise L.HireInvalidArgument(L.ERR_INVALID, "overlap_ratio: no sample sets")
+    if k_groups < 1:
+        raise L.HireInvalidArgument(L.ERR_INVALID, "overlap_ratio: k_groups must be >= 1")
+    merged = set()
+    for s_ in per_sample_sets:
+        if len(s_) != k_groups:
+            raise L.HireInvalidArgument(L.ERR_INVALID,
+                                        f"overlap_ratio: sample selected {len(s_)} groups, expected {k_groups}")
+        merged.update(int(v) for v in s_)
+    return len(merged) / (len(per_sample_sets) * k_groups)
+
+
 def shard_range(l: int, s: int, i: int):
     """distributed.hpp:53-57: (first, width) of shard i of s."""
     base, extra = divmod(l, s)

@@ -867,6 +867,48 @@ int fetch_inputs(hire_ctx ctx, void* dst, const void* host_src, size_t bytes) {
   return HIRE_OK;
 }
 
+// union_group_select (ffn.hpp:237-253): sorted union of the B per-sample
+// selections. One CTA: group bitmap in shared memory, OR of every selected id,
+// popcount prefix, ascending emit. *count = |union|.
+__global__ void __launch_bounds__(1024) group_union_kernel(const uint32_t* __restrict__ sel, int64_t stride, int kg,
+                                                           int B, int ng, uint32_t* __restrict__ out,
+                                                           int64_t* __restrict__ count) {
+  hire_dev::griddep_wait();
+  hire_dev::griddep_launch();
+  extern __shared__ unsigned u_bm[];
+  __shared__ int s_scan[40];
+  const int nw = (ng + 31) / 32;
+  for (int i = threadIdx.x; i < nw; i += blockDim.x) u_bm[i] = 0u;
+  __syncthreads();
+  for (int i = threadIdx.x; i < B * kg; i += blockDim.x) {
+    const uint32_t id = sel[static_cast<int64_t>(i / kg) * stride + i % kg];
+    atomicOr(u_bm + (id >> 5), 1u << (id & 31));
+  }
+  __syncthreads();
+  const int W = (nw + 1023) / 1024, w0 = threadIdx.x * W;
+  int mine = 0;
+  for (int i = 0; i < W; ++i)
+    if (w0 + i < nw) mine += __popc(u_bm[w0 + i]);
+  int total;
+  int pos = hire_dev::block_scan_excl<1024>(mine, s_scan, &total);
+  for (int i = 0; i < W && w0 + i < nw; ++i) {
+    unsigned word = u_bm[w0 + i];
+    while (word) {
+      out[pos++] = static_cast<uint32_t>((w0 + i) * 32 + __ffs(word) - 1);
+      word &= word - 1u;
+    }
+  }
+  if (threadIdx.x == 0) *count = total;
+}
+
+// out[i] += add[i] (ffn_common_path's dense + sparse sum, ffn.hpp:232)
+__global__ void add_f32_kernel(float* __restrict__ out, const float* __restrict__ add, int64_t n) {
+  hire_dev::griddep_wait();
+  hire_dev::griddep_launch();
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = __fadd_rn(out[i], add[i]);
+}
+
 __global__ void add_offset_kernel(uint32_t* idx, int64_t n, uint32_t off) {
   hire_dev::griddep_wait();
   hire_dev::griddep_launch();
@@ -2167,6 +2209,57 @@ int hire_ffn_dense_run(hire_ctx ctx, hire_matrix u, hire_matrix v, const float* 
   CK(launch_k(ctx, iota_mod_kernel, static_cast<unsigned>(ceil_div(B * m, 256)), 256, 0, units, m, B * m));
   CK(cudaGetLastError());
   return run_down(ctx, v, units, act, m, m, B, strict, partial, out);
+}
+
+int hire_ffn_union_select(hire_ctx ctx, hire_matrix u, hire_scorer a, const float* x, int64_t B,
+                          const hire_ffn_params* p, uint32_t* ids, int64_t* n_ids) {
+  if (!ctx || !x || !ids || !n_ids) return invalid("null argument");
+  if (B < 1) return invalid("union_group_select: no input samples");
+  RET(validate_ffn(u, u, a, B, p));
+  const int64_t g = p->group_size, m = u->rows, kg = p->k / g, kpg = p->k_prime / g, ng = m / g;
+  if ((ng + 31) / 32 * 4 > 48 * 1024) return invalid("union_group_select: more than 393216 groups");
+  SelPlan sp;
+  RET(plan_select(ng, kpg, HIRE_SELECT_EXACT, 0, 0, &sp));
+  Arena ar;
+  FfnWs fw;
+  take_ffn_ws(ar, &fw, a, B, m, u->d, g, kg, kpg, sp, 1);
+  uint32_t* sel;
+  int64_t* cnt;
+  ar.take(&sel, static_cast<size_t>(B * kg));
+  ar.take(&cnt, 1);
+  RET(ar.commit(ctx));
+  RET(ffn_select(ctx, u, a, x, B, g, kg, kpg, p->phi, p->x_mode, p->strict, sp, fw, sel, kg));
+  CK(launch_k(ctx, group_union_kernel, 1u, 1024, static_cast<size_t>((ng + 31) / 32) * 4, static_cast<const uint32_t*>(sel),
+              kg, static_cast<int>(kg), static_cast<int>(B), static_cast<int>(ng), ids, cnt));
+  CK(cudaGetLastError());
+  CK(cudaMemcpyAsync(n_ids, cnt, 8, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  return HIRE_OK;
+}
+
+int hire_ffn_common_path_run(hire_ctx ctx, hire_matrix du, hire_matrix dv, hire_matrix u, hire_matrix v,
+                             hire_scorer a, const float* x, int64_t B, const hire_ffn_params* p, float* out) {
+  if (!ctx || !x || !out || !u || !v || !p) return invalid("null argument");
+  // CommonPathFFN validate (ffn.hpp:49-56)
+  if (du && dv && (du->rows != dv->rows || du->d != dv->d)) return invalid("GroupedFFN: U and V must both be d x m");
+  if (du && du->d != u->d) return invalid("CommonPathFFN: parts disagree on d");
+  if (u->rows < p->group_size) return invalid("CommonPathFFN: sparse part needs m2 >= g");
+  RET(validate_ffn(u, v, a, B, p));
+  const size_t n = static_cast<size_t>(B * u->d);
+  if (du && dv && du->rows > 0) {
+    RET(hire_ffn_dense_run(ctx, du, dv, x, B, p->phi, p->strict, out));
+  } else {
+    CK(cudaMemsetAsync(out, 0, n * 4, ctx->stream));
+  }
+  // the sparse part's output in io_dev (out stays untouched until the add)
+  RET(ensure(&ctx->io_dev, &ctx->io_dev_cap, n * 4 + static_cast<size_t>(B * p->k) * 4 + 512, ctx->stream));
+  float* sp_out = static_cast<float*>(ctx->io_dev);
+  uint32_t* sp_sel = reinterpret_cast<uint32_t*>(static_cast<char*>(ctx->io_dev) + align_up(n * 4));
+  RET(hire_ffn_run(ctx, u, v, a, x, B, p, sp_sel, sp_out));
+  CK(launch_k(ctx, add_f32_kernel, static_cast<unsigned>(ceil_div(static_cast<int64_t>(n), 256)), 256, 0, out,
+              static_cast<const float*>(sp_out), static_cast<int64_t>(n)));
+  CK(cudaGetLastError());
+  return HIRE_OK;
 }
 
 // ------------------------------------------------------------------- DA --
