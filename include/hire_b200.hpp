@@ -24,6 +24,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdint>
+#include <iterator>
 #include <cstring>
 #include <memory>
 #include <span>
@@ -485,6 +486,92 @@ inline GroupSparseResult ffn_group_sparse(const GroupedFFN& f, std::span<const f
   detail::throw_status(hire_ffn_host(detail::thread_ctx(), f.u.device(), f.v.device(), a.device(), x.data(), 1, &p,
                                      r.selected.ids.data(), r.output.data()));
   return r;
+}
+
+// ffn.hpp:65-76: every unit, ascending (strict = the reference's arithmetic).
+inline std::vector<float> ffn_dense(const GroupedFFN& f, std::span<const float> x, bool strict = true) {
+  detail::check_dims(f.dim(), x.size(), "ffn_dense");
+  detail::DevBuf dx(x.data(), static_cast<std::int64_t>(x.size() * 4));
+  detail::DevBuf dout(static_cast<std::int64_t>(f.dim() * 4));
+  detail::throw_status(hire_ffn_dense_run(detail::thread_ctx(), f.u.device(), f.v.device(), dx.as<float>(), 1,
+                                          static_cast<int>(f.phi), strict ? 1 : 0, dout.as<float>()));
+  std::vector<float> out(f.dim());
+  dout.to_host(out.data(), dout.n);
+  return out;
+}
+
+// ffn.hpp:44-47
+struct CommonPathFFN {
+  GroupedFFN dense_part;
+  GroupedFFN sparse_part;
+};
+
+// ffn.hpp:223-234: ffn_dense(dense part) + ffn_group_sparse(sparse part).
+inline std::vector<float> ffn_common_path(const CommonPathFFN& c, std::span<const float> x, const ApproxScorer& a,
+                                          std::size_t k, std::size_t k_prime, int x_mode = HIRE_X_FP32,
+                                          bool strict = true) {
+  detail::check_dims(c.sparse_part.dim(), x.size(), "ffn_common_path");
+  hire_ffn_params p{};
+  p.k = static_cast<std::int64_t>(k);
+  p.k_prime = static_cast<std::int64_t>(k_prime);
+  p.group_size = static_cast<std::int64_t>(c.sparse_part.group_size);
+  p.phi = static_cast<int>(c.sparse_part.phi);
+  p.x_mode = x_mode;
+  p.strict = strict ? 1 : 0;
+  detail::DevBuf dx(x.data(), static_cast<std::int64_t>(x.size() * 4));
+  detail::DevBuf dout(static_cast<std::int64_t>(c.sparse_part.dim() * 4));
+  const bool has_dense = c.dense_part.hidden() > 0;
+  detail::throw_status(hire_ffn_common_path_run(detail::thread_ctx(), has_dense ? c.dense_part.u.device() : nullptr,
+                                                has_dense ? c.dense_part.v.device() : nullptr,
+                                                c.sparse_part.u.device(), c.sparse_part.v.device(), a.device(),
+                                                dx.as<float>(), 1, &p, dout.as<float>()));
+  std::vector<float> out(c.sparse_part.dim());
+  dout.to_host(out.data(), dout.n);
+  return out;
+}
+
+// ffn.hpp:237-253: union of the per-sample selections (dynamic overlap).
+inline GroupIndexSet union_group_select(const GroupedFFN& f, std::span<const std::vector<float>> xs,
+                                        const ApproxScorer& a, std::size_t k, std::size_t k_prime,
+                                        int x_mode = HIRE_X_FP32, bool strict = true) {
+  if (xs.empty()) throw std::invalid_argument("union_group_select: no input samples");
+  std::vector<float> flat;
+  for (const auto& x : xs) {
+    detail::check_dims(f.dim(), x.size(), "union_group_select");
+    flat.insert(flat.end(), x.begin(), x.end());
+  }
+  hire_ffn_params p{};
+  p.k = static_cast<std::int64_t>(k);
+  p.k_prime = static_cast<std::int64_t>(k_prime);
+  p.group_size = static_cast<std::int64_t>(f.group_size);
+  p.phi = static_cast<int>(f.phi);
+  p.x_mode = x_mode;
+  p.strict = strict ? 1 : 0;
+  detail::DevBuf dx(flat.data(), static_cast<std::int64_t>(flat.size() * 4));
+  detail::DevBuf dids(static_cast<std::int64_t>(std::max<std::size_t>(f.num_groups(), 1) * 4));
+  std::int64_t n = 0;
+  detail::throw_status(hire_ffn_union_select(detail::thread_ctx(), f.u.device(), a.device(), dx.as<float>(),
+                                             static_cast<std::int64_t>(xs.size()), &p, dids.as<std::uint32_t>(), &n));
+  GroupIndexSet r;
+  r.ids.resize(static_cast<std::size_t>(n));
+  if (n) dids.to_host(r.ids.data(), n * 4);
+  return r;
+}
+
+// metrics.hpp:68-88: |union| / (s * k_groups).
+inline double overlap_ratio(const std::vector<GroupIndexSet>& per_sample_sets, std::size_t k_groups) {
+  if (per_sample_sets.empty()) throw std::invalid_argument("overlap_ratio: no sample sets");
+  if (k_groups < 1) throw std::invalid_argument("overlap_ratio: k_groups must be >= 1");
+  std::vector<std::uint32_t> merged;
+  for (const auto& s : per_sample_sets) {
+    if (s.ids.size() != k_groups)
+      throw std::invalid_argument("overlap_ratio: sample selected " + std::to_string(s.ids.size()) +
+                                  " groups, expected " + std::to_string(k_groups));
+    std::vector<std::uint32_t> next;
+    std::set_union(merged.begin(), merged.end(), s.ids.begin(), s.ids.end(), std::back_inserter(next));
+    merged.swap(next);
+  }
+  return static_cast<double>(merged.size()) / (static_cast<double>(per_sample_sets.size()) * k_groups);
 }
 
 // ----------------------------------------------------------- distributed --

@@ -63,5 +63,20 @@ int main(int argc, char** argv) {
   std::printf("\nffnout");
   for (float o : fr.output) std::printf(" %.9g", o);
   std::printf("\nrecall %.6f\n", hire::recall(r.candidates, hire::exact_topk(z, x, k, hire::Activation::kIdentity)).recall);
+  // batch-level FFN levers: dense, common path (dense = sparse = f), union over {x, -x}
+  const auto dense = hire::ffn_dense(f, x);
+  std::printf("dense");
+  for (float o : dense) std::printf(" %.9g", o);
+  const auto cp = hire::ffn_common_path(hire::CommonPathFFN{f, f}, x, a, k, kp);
+  std::printf("\ncommon");
+  for (float o : cp) std::printf(" %.9g", o);
+  std::vector<float> xn(x.size());
+  for (size_t i = 0; i < x.size(); ++i) xn[i] = -x[i];
+  const std::vector<std::vector<float>> xs = {x, xn};
+  const auto un = hire::union_group_select(f, xs, a, k, kp);
+  std::printf("\nunion");
+  for (auto id : un.ids) std::printf(" %u", id);
+  const auto s2 = hire::ffn_group_sparse(f, xn, a, k, kp).selected;
+  std::printf("\noverlap %.9g\n", hire::overlap_ratio({fr.selected, s2}, k));
   return 0;
 }

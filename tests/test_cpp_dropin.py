@@ -56,3 +56,12 @@ def test_dropin_matches_oracle(O, tmp_path):
     ids, fo = O.ffn_group_sparse(w, w, x, sr, k, kp, 1, 1)
     assert [int(i) for i in lines["ffn"]] == ids.tolist()
     assert np.array_equal(np.array([np.float32(float(v)) for v in lines["ffnout"]]), fo)
+    dense = O.ffn_dense(w, w, x, 1)
+    assert np.array_equal(np.array([np.float32(float(v)) for v in lines["dense"]]), dense)
+    common = (dense + fo).astype(np.float32)  # ffn.hpp:232
+    assert np.array_equal(np.array([np.float32(float(v)) for v in lines["common"]]), common)
+    xn = (-x).astype(np.float32)
+    ids_n, _ = O.ffn_group_sparse(w, w, xn, O.q4_scores_fpx(codes, scales, xn, 1), k, kp, 1, 1)
+    union = sorted(set(ids.tolist()) | set(ids_n.tolist()))
+    assert [int(i) for i in lines["union"]] == union
+    assert float(lines["overlap"][0]) == pytest.approx(len(union) / (2 * k))
