@@ -463,6 +463,87 @@ class DaSoftmaxWorkload:
 
 
 # ------------------------------------------------------------- reference ---
+class DecoderWorkload:
+    """cfg5 (BASELINE.json configs[4]): greedy decode steps of the 18-layer
+    ReLU decoder (d=2048, FFN 8192 as HiRE-FFN top-5% with the int4 proxy,
+    16 heads over a 1024-token KV cache, V=256000 HiRE-softmax k'=1024 k=64).
+    Each step feeds the previous step's tokens (true autoregressive chain);
+    dense parts are library code (decoder.py)."""
+    name = "cfg5"
+    proxy_kernel = "q4_score_mma / q4_score_mma_sel (all int4 proxy launches of the step: 18 FFN + vocab)"
+    span_kernel = None  # the proxy launches spread over the whole step
+
+    def __init__(self, H, batch, seed=0):
+        from paper_2402_09360_b200.decoder import DecoderConfig, HireDecoder
+        self.H = H
+        self.cfg = DecoderConfig()
+        self.B, self.d, self.k, self.kp = batch, self.cfg.d, self.cfg.vocab_k, self.cfg.vocab_k_prime
+        self.m = HireDecoder(self.cfg, batch, seed=seed)
+        g = torch.Generator(device="cuda").manual_seed(seed + 5)
+        self.tok = torch.randint(0, self.cfg.vocab, (batch,), device="cuda", generator=g)
+        self.tok0 = self.tok.clone()
+        torch.cuda.synchronize()
+
+    def inputs(self, n):
+        return [None] * n  # the chain carries its own tokens
+
+    def step(self, i, x):
+        nxt, _, _ = self.m.step(self.tok)
+        self.tok.copy_(nxt)
+        return nxt
+
+    def host_step(self, i, x_host, idx_host, val_host, ctx):
+        # end to end: tokens from pinned host memory into the captured step's
+        # static input, one graph replay, the top-k indices back to the host
+        if not hasattr(self, "_hg"):
+            self._tin = torch.zeros(self.B, dtype=torch.int64, device="cuda")
+            self._pin_in = torch.zeros(self.B, dtype=torch.int64).pin_memory()
+            self._pin_out = torch.zeros(self.B, self.k, dtype=torch.int32).pin_memory()
+            s = torch.cuda.Stream()
+            with torch.cuda.stream(s):
+                self.m.step(self._tin)
+                torch.cuda.synchronize()
+                self._hg = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(self._hg, stream=s):
+                    _, self._idx_out, _ = self.m.step(self._tin)
+        self._pin_in.copy_(torch.from_numpy(idx_host[:, 0].astype(np.int64)))
+        self._tin.copy_(self._pin_in, non_blocking=True)
+        self._hg.replay()
+        self._pin_out.copy_(self._idx_out, non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+        idx_host[:] = self._pin_out.numpy().astype(np.uint32)
+
+    def io_bytes(self):
+        return self.B * 8, self.B * self.k * 4
+
+    def proxy_bytes(self):
+        c = self.cfg
+        ffn = c.ffn * (c.d // 2 + 4)
+        return (c.layers * ffn + c.vocab * (c.d // 2 + 4)) / (c.layers + 1)  # average per proxy launch
+
+    def step_bytes(self, x):
+        return self.m.step_bytes(), 0, 0
+
+    def recall(self, x):
+        """softmax recall@k, teacher-forced on the exact-top-k model's hidden
+        state (decoder.stage_recall); the per-layer FFN recalls go in config"""
+        r = self.m.stage_recall(self.tok0)
+        self.stage_rec = r
+        return r["softmax"]
+
+    def config(self):
+        c = self.cfg
+        return {"workload": "cfg5 decode step, 18-layer ReLU decoder (BASELINE.json configs[4])", "layers": c.layers,
+                "d": c.d, "heads": c.heads, "ffn": c.ffn, "vocab": c.vocab, "kv_cache": c.ctx_len,
+                "ffn_k": c.ffn_k, "ffn_k_prime": c.ffn_k_prime, "vocab_k": c.vocab_k,
+                "vocab_k_prime": c.vocab_k_prime, "global_batch": self.B,
+                "weights": "random-init bf16 (attention N(0,1/d); FFN cfg2 family; vocab cfg3 family, tied embedding)",
+                "dense_parts": "RMSNorm, QKV/O projections (cuBLAS via torch), SDPA attention (library)",
+                "recall_oracle": "same model with exact top-k FFN units and exact logits (teacher-forced per stage)",
+                "stage_recall": getattr(self, "stage_rec", None),
+                "l2": "working set ~3.2 GB + KV cache > 126 MB L2", "select": "exact top-k'"}
+
+
 def make_ref_runner(wl, threads):
     """The reference's own CPU implementation of the workload's path:
     oracle/_ref (the unmodified headers compiled behind a C shim) when it was
@@ -556,11 +637,13 @@ def make_workload(H, args, world=1, rank=0):
         return LowRankSoftmaxWorkload(H, args.batch or 1)
     if args.workload == "cfg4":
         return DaSoftmaxWorkload(H, args.batch or 16, world, rank)
+    if args.workload == "cfg5":
+        return DecoderWorkload(H, args.batch or 1)
     return FfnWorkload(H, args.batch or 8)
 
 
 def B_default(args):
-    return args.batch or {"cfg2": 8, "cfg3": 1, "cfg1": 1, "cfg4": 16}[args.workload]
+    return args.batch or {"cfg2": 8, "cfg3": 1, "cfg1": 1, "cfg4": 16, "cfg5": 1}[args.workload]
 
 
 def measured_traffic(wl, batch):
@@ -697,14 +780,14 @@ def run_ours(args):
     achieved = pb / (k_us * 1e-6) / 1e9
     dspan = None
     kkey = "lr_score" if getattr(wl, "lowrank", False) else "proxy"
-    if spans and kkey in spans and "ffn_fused" not in prof:
+    if spans and kkey in spans and "ffn_fused" not in prof and getattr(wl, "span_kernel", "x") is not None:
         dspan = spans[kkey][1] - spans[kkey][0]
     rec = wl.recall(xs[W])
 
     # end-to-end through the C ABI with host buffers (copies inside)
     hctx = H.Context(local)
     bi, bo = wl.io_bytes()
-    xh = [xs[W + i].cpu().numpy().copy() for i in range(min(K, 64))]
+    xh = [xs[W + i].cpu().numpy().copy() if xs[W + i] is not None else None for i in range(min(K, 64))]
     if isinstance(wl, FfnWorkload):
         oa = np.empty((wl.B, wl.k), dtype=np.uint32)
         ob = np.empty((wl.B, wl.d), dtype=np.float32)
@@ -715,6 +798,8 @@ def run_ours(args):
     # runs once eagerly, then is captured into its CUDA graph (hire_*_host)
     n_cycle = len(getattr(wl, "layers", None) or getattr(wl, "copies", None) or [0])
     n_warm = max(W, 2 * n_cycle + 1)
+    if wl.name == "cfg5":  # the decode chain's tokens travel in oa[:, 0]
+        oa[:, 0] = wl.tok0.cpu().numpy().astype(np.uint32)
     for i in range(n_warm):
         wl.host_step(i, xh[i % len(xh)], oa, ob, hctx)
     barrier(world)
@@ -757,7 +842,7 @@ def run_ours(args):
         "gpu_launches": int(launches),
         "clocks": clk.summary(),
     }
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    if rank == 0 and world == 1 and not args.no_cpu_baseline and wl.name != "cfg5":
         v, cores, kind, desc = cpu_baseline(wl, args.cpu_seconds)
         line["cpu_baseline"] = {"value": round(v, 3), "unit": "tokens/s", "cores": cores, "kind": kind,
                                 "sample": desc}
@@ -774,6 +859,10 @@ def run_reference(args):
     workload's queries. Rank 0 only; other ranks exit without work."""
     world, rank, local = dist_env()
     if rank != 0:
+        return
+    if args.workload == "cfg5":
+        print(json.dumps({"impl": "reference", "unavailable": "the reference has no decoder (cfg5 glue is not in "
+                                                              "the reference library)"}), flush=True)
         return
     torch.cuda.set_device(local)
     import paper_2402_09360_b200 as H
@@ -808,7 +897,7 @@ def main():
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="cfg2", choices=["cfg1", "cfg2", "cfg3", "cfg4"])
+    ap.add_argument("--workload", default="cfg2", choices=["cfg1", "cfg2", "cfg3", "cfg4", "cfg5"])
     ap.add_argument("--batch", type=int, default=0)
     ap.add_argument("--select", default="exact", choices=["exact", "bucketed"])
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
