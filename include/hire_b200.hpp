@@ -13,9 +13,9 @@
 // row-major matrix the device holds. Device mirrors are built on first use
 // and rebuilt after any mutation through a non-const accessor.
 //
-// Proxies: int4 (ApproxScorer::quantized) and low-rank (::low_rank), the two
-// the paper evaluates; exact_copy / low_rank_quantized throw
-// std::invalid_argument (not accelerated). Extensions are defaulted so
+// Proxies: int4 (ApproxScorer::quantized), low-rank (::low_rank) and both
+// combined (::low_rank_quantized); exact_copy throws std::invalid_argument
+// (not accelerated). Extensions are defaulted so
 // reference call sites compile unchanged: HireConfig::{x_mode, select,
 // strict, n_buckets, bucket_t}, ScoreMatrix::set_device_bf16, batched
 // hire_topk_batch.
@@ -298,8 +298,22 @@ class ApproxScorer {
   static ApproxScorer exact_copy(const ScoreMatrix&) {
     throw std::invalid_argument("ApproxScorer::exact_copy: not accelerated on the B200 path");
   }
-  static ApproxScorer low_rank_quantized(const LowRankApprox&) {
-    throw std::invalid_argument("ApproxScorer::low_rank_quantized: not accelerated on the B200 path");
+  // approx.hpp:342-347: both factors through the int4 rule (per column, the
+  // device K9 build), scored over the dequantized entries — the reference's
+  // arithmetic (approx.hpp:500-516), bit-identical in strict mode.
+  static ApproxScorer low_rank_quantized(const LowRankApprox& lr) {
+    if (lr.z1.cols() != lr.rank || lr.z2.cols() != lr.rank)
+      throw std::invalid_argument("ApproxScorer: low-rank factors do not match rank " + std::to_string(lr.rank));
+    auto dequant = [](const ScoreMatrix& z) {
+      const QuantizedMatrix q = quantize_int4(z);
+      std::vector<float> v(q.rows * q.cols);
+      for (std::size_t j = 0; j < q.cols; ++j)
+        for (std::size_t i = 0; i < q.rows; ++i) v[j * q.rows + i] = q.entry(i, j);
+      return ScoreMatrix(q.rows, q.cols, std::move(v));
+    };
+    ApproxScorer a = low_rank(LowRankApprox{dequant(lr.z1), dequant(lr.z2), lr.rank});
+    a.kind_ = ScorerKind::kLowRankQuantized;
+    return a;
   }
 
   ScorerKind kind() const { return kind_; }

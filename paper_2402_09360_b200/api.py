@@ -203,6 +203,22 @@ class ApproxScorer:
                                                C.byref(h)))
         return ApproxScorer(h, L.SCORER_Q4, rows, d)
 
+    # approx.hpp:342-347 low_rank_quantized(LowRankApprox): both factors
+    # quantized per the int4 rule (per reference column: z1's d-vectors, z2's
+    # l-vectors), scored over the dequantized entries code * scale — the
+    # reference's own arithmetic (approx.hpp:500-516), so the strict low-rank
+    # kernels reproduce it bit for bit. The int4 rule runs on the device (K9).
+    @staticmethod
+    def low_rank_quantized(z1: torch.Tensor, z2: torch.Tensor) -> "ApproxScorer":
+        def q4_dequant(rows_major: torch.Tensor) -> np.ndarray:
+            q = ApproxScorer.quantize(ScoreMatrix(rows_major.float().contiguous()))
+            codes, scales = q.export_q4()
+            return codes.astype(np.float32) * scales[:, None]   # fp32 code * scale, as entry()
+        d1 = q4_dequant(z1)                                      # [r][d]: one row per z1 column
+        d2 = np.ascontiguousarray(q4_dequant(z2.t()).T)          # z2 columns are [r] rows of z2^T
+        a = ApproxScorer.low_rank(torch.from_numpy(d1).to(z1.device), torch.from_numpy(d2).to(z1.device))
+        return a
+
     # approx.hpp:339 quantized(const ScoreMatrix&) — quantize_int4 on the device (K9)
     @staticmethod
     def quantize(z: ScoreMatrix, ctx: Optional[Context] = None) -> "ApproxScorer":

@@ -376,3 +376,19 @@ def test_da_topk_run_single_rank_equals_oracle(H, O, merge):
         wi, wv, wcl, _ = O.da_topk(w, x[b], scores, 1, k, kp, 0, merge=merge)
         assert np.array_equal(N(ti[b]).astype(np.uint32), wi)
         assert np.array_equal(N(tv[b]).view(np.uint32), wv.view(np.uint32))
+
+
+def test_low_rank_quantized_scorer_equals_reference(H, O):
+    # approx.hpp:342-347, 500-516 — against the compiled reference's own LRQ scorer
+    if not O.ref_available():
+        pytest.skip("compiled reference not built")
+    g = np.random.default_rng(91)
+    V, d, r = 5000, 256, 16
+    z1 = g.standard_normal((r, d)).astype(np.float32)
+    z2 = g.standard_normal((V, r)).astype(np.float32)
+    x = _data.queries(3, d, 92)
+    a = H.ApproxScorer.low_rank_quantized(T(z1), T(z2))
+    got = N(a.scores(T(x), strict=True))
+    ref = O.RefScorer("lrq", z1=z1, z2=z2)
+    for b in range(3):
+        assert np.array_equal(got[b].view(np.uint32), ref.scores(x[b], 0).view(np.uint32)), b
