@@ -909,6 +909,18 @@ __global__ void add_f32_kernel(float* __restrict__ out, const float* __restrict_
   if (i < n) out[i] = __fadd_rn(out[i], add[i]);
 }
 
+// A caller buffer the kernels can address directly (pinned / registered host
+// memory, 16-byte aligned): its device alias; nullptr for pageable memory.
+void* host_alias(const void* p, size_t bytes) {
+  if (!p || bytes % 16 != 0 || (reinterpret_cast<uintptr_t>(p) & 15) != 0) return nullptr;
+  cudaPointerAttributes at;
+  if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  return at.type == cudaMemoryTypeHost ? at.devicePointer : nullptr;
+}
+
 __global__ void add_offset_kernel(uint32_t* idx, int64_t n, uint32_t off) {
   hire_dev::griddep_wait();
   hire_dev::griddep_launch();
@@ -1888,14 +1900,15 @@ int hire_topk_host(hire_ctx ctx, hire_matrix w, hire_scorer a, const float* x_ho
   RET(ensure_host(&ctx->io_host, &ctx->io_host_cap, in_bytes + out_bytes, ctx->stream));
   char* dv = static_cast<char*>(ctx->io_dev);
   char* hs = static_cast<char*>(ctx->io_host);
+  void* xd = nullptr;  // staged (see hire_ffn_host)
   std::memcpy(hs, x_host, xb);
   const std::vector<int64_t> key = {1, reinterpret_cast<int64_t>(w), reinterpret_cast<int64_t>(a), B, p->k, p->k_prime,
                                     p->phi, p->x_mode, p->select, p->strict, p->n_buckets, p->bucket_t,
-                                    cb ? 1 : 0, pb ? 1 : 0};
+                                    cb ? 1 : 0, pb ? 1 : 0, reinterpret_cast<int64_t>(xd)};
   int64_t res[4];
   cudaStream_t done_on = nullptr;
   RET(run_host_graph(ctx, key, res, &done_on, [&](int64_t* r) -> int {
-    RET(fetch_inputs(ctx, dv, hs, xb));
+    RET(fetch_inputs(ctx, dv, xd ? xd : hs, xb));
     char* o = hs + in_bytes;  // results are written straight into mapped host memory
     uint32_t* dcand = cb ? reinterpret_cast<uint32_t*>(o) : nullptr;
     o += align_up(cb);
@@ -2160,19 +2173,27 @@ int hire_ffn_host(hire_ctx ctx, hire_matrix u, hire_matrix v, hire_scorer a, con
   RET(ensure_host(&ctx->io_host, &ctx->io_host_cap, in_bytes + out_bytes, ctx->stream));
   char* dv = static_cast<char*>(ctx->io_dev);
   char* hs = static_cast<char*>(ctx->io_host);
-  std::memcpy(hs, x_host, xb);
+  // results go straight into caller buffers in pinned memory (no staging);
+  // the input is always staged: a graph keyed on every caller input buffer
+  // would be re-captured for each new buffer
+  void* xd = nullptr;
+  void* od = host_alias(out_host, ob);
+  void* sd = sel_host ? host_alias(sel_host, sb) : nullptr;
+  if (!xd) std::memcpy(hs, x_host, xb);
   // the output rows are written straight into mapped host memory; the unit
   // ids stay on the device (the down-projection reads them) and are stored
   // to the host by a small kernel at the end
   uint32_t* dsel = reinterpret_cast<uint32_t*>(dv + in_bytes);
-  uint32_t* hsel = reinterpret_cast<uint32_t*>(hs + in_bytes);
-  float* dout = reinterpret_cast<float*>(hs + in_bytes + align_up(sb));
+  uint32_t* hsel = sd ? static_cast<uint32_t*>(sd) : reinterpret_cast<uint32_t*>(hs + in_bytes);
+  float* dout = od ? static_cast<float*>(od) : reinterpret_cast<float*>(hs + in_bytes + align_up(sb));
   const std::vector<int64_t> key = {2, reinterpret_cast<int64_t>(u), reinterpret_cast<int64_t>(v), reinterpret_cast<int64_t>(a),
-                                    B, p->k, p->k_prime, p->group_size, p->phi, p->x_mode, p->strict};
+                                    B, p->k, p->k_prime, p->group_size, p->phi, p->x_mode, p->strict,
+                                    reinterpret_cast<int64_t>(xd), reinterpret_cast<int64_t>(od),
+                                    reinterpret_cast<int64_t>(sd), sel_host ? 1 : 0};
   int64_t res[4];
   cudaStream_t done_on = nullptr;
   RET(run_host_graph(ctx, key, res, &done_on, [&](int64_t*) -> int {
-    RET(fetch_inputs(ctx, dv, hs, xb));
+    RET(fetch_inputs(ctx, dv, xd ? xd : hs, xb));
     RET(hire_ffn_run(ctx, u, v, a, reinterpret_cast<const float*>(dv), B, p, dsel, dout));
     if (sel_host) {
       if (sb % 16 == 0) {
@@ -2186,8 +2207,8 @@ int hire_ffn_host(hire_ctx ctx, hire_matrix u, hire_matrix v, hire_scorer a, con
     return HIRE_OK;
   }));
   CK(cudaStreamSynchronize(done_on));
-  if (sel_host) std::memcpy(sel_host, hs + in_bytes, sb);
-  std::memcpy(out_host, hs + in_bytes + align_up(sb), ob);
+  if (sel_host && !sd) std::memcpy(sel_host, hs + in_bytes, sb);
+  if (!od) std::memcpy(out_host, hs + in_bytes + align_up(sb), ob);
   return HIRE_OK;
 }
 
