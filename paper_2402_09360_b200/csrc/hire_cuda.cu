@@ -270,6 +270,31 @@ int ensure_selc(hire_ctx ctx, size_t words) {
   return HIRE_OK;
 }
 
+// Zero-at-rest sample slots / bounds / list counts of the fused and list
+// selectors (fsel.cuh): [B][kFselSampleMax] samples, lo[B], cnt[B], ctr.
+int ensure_fzero(hire_ctx ctx, int64_t B) {
+  const size_t need = static_cast<size_t>(B) * (hire_dev::kFselSampleMax + 2) * 8 + hire_dev::kFselCtr * 32 * 4 +
+                      static_cast<size_t>(B) * 8;
+  if (need <= ctx->fzero_cap) return HIRE_OK;
+  if (ctx->fzero) {
+    CK(cudaStreamSynchronize(ctx->stream));
+    CK(cudaFree(ctx->fzero));
+    ctx->fzero = nullptr;
+  }
+  const size_t nb = std::max(need, ctx->fzero_cap * 2);
+  CK(cudaMalloc(&ctx->fzero, nb));
+  CK(cudaMemsetAsync(ctx->fzero, 0, nb, ctx->stream));
+  ctx->fzero_cap = nb;
+  return HIRE_OK;
+}
+
+void fzero_layout(hire_ctx ctx, int64_t B, hire_dev::FuseSel* fs) {
+  fs->samp = static_cast<uint64_t*>(ctx->fzero);
+  fs->lo = static_cast<unsigned long long*>(ctx->fzero) + static_cast<size_t>(B) * hire_dev::kFselSampleMax;
+  fs->cnt = reinterpret_cast<unsigned*>(fs->lo + B);
+  fs->ctr = reinterpret_cast<unsigned*>(fs->lo + 2 * B);
+}
+
 // Bump allocator over the context workspace. Offsets first, then one
 // ensure(); pointers are only valid for the current call.
 struct Arena {
@@ -404,7 +429,7 @@ int plan_select(int64_t n, int64_t k_prime, int sel_mode, int64_t nb_req, int64_
 // Candidate selection over scores [B][n] -> cand [B][cand_stride] ascending.
 int run_select(hire_ctx ctx, const float* scores, int64_t score_stride, int64_t n, int64_t B,
                const SelPlan& sp, uint64_t* surv, uint32_t* cand, int64_t cand_stride,
-               int* status) {
+               int* status, bool ordered = true) {
   StageScope scope(ctx, kStageSelect);
   if (sp.mode == 2) {
     const uint32_t nn = static_cast<uint32_t>(n), K = static_cast<uint32_t>(sp.k_eff);
@@ -452,6 +477,32 @@ int run_select(hire_ctx ctx, const float* scores, int64_t score_stride, int64_t 
       CK(cudaGetLastError());
       return HIRE_OK;
     }
+    const char* nolist = std::getenv("HIRE_SEL_NOLIST");
+    if (!(nolist && nolist[0] == '1') && n <= hire_dev::kFinMaxRows && K <= static_cast<uint32_t>(hire_dev::kFinCap)) {
+      // list path: sampled exact lower bound -> every key >= lo appended to
+      // a per-query list -> sel_fin_kernel (exact k'-th key, emit)
+      RET(ensure_fzero(ctx, B));
+      hire_dev::FuseSel fs{};
+      fs.n = nn;
+      fs.K = K;
+      fs.n_samp = 0;
+      fzero_layout(ctx, B, &fs);
+      uint64_t* piv = surv;                                              // [B][4]
+      uint64_t* lists = surv + 5 * B + B * kWinBins * kWinGroups / 2;    // [B][kFinCap] (>= B x 65536 words)
+      fs.lists = lists;
+      const int64_t CL = std::max<int64_t>(1, std::min<int64_t>(ceil_div(n, kWinThreads * kScanBatch),
+                                                                std::max<int64_t>(1, 8 * ctx->num_sms / B)));
+      const uint32_t perm = sample_perm(static_cast<uint64_t>(n) / 4);
+      CK(launch_k(ctx, sel_pivot_kernel, static_cast<unsigned>(B), kPivThreads, 0, scores, score_stride, nn, K,
+                  perm, piv, reinterpret_cast<unsigned*>(surv + 5 * B), 1));
+      CK(launch_k(ctx, sel_wlist_kernel, dim3(static_cast<unsigned>(CL), static_cast<unsigned>(B)), kWinThreads, 0,
+                  scores, score_stride, nn, static_cast<const uint64_t*>(piv), fs.cnt, lists, hire_dev::kFinCap));
+      CK(launch_k(ctx, sel_fin_kernel, static_cast<unsigned>(B), hire_dev::kFinThreads,
+                  static_cast<size_t>((n + 31) / 32) * 4, scores, score_stride, fs, cand, cand_stride, ordered ? 1 : 0,
+                  status));
+      CK(cudaGetLastError());
+      return HIRE_OK;
+    }
     // chunks per query: every S3 CTA of the grid must be co-resident (the
     // look-back waits on lower chunks), 4 x 256-thread CTAs per SM
     const int64_t C = std::max<int64_t>(
@@ -470,7 +521,7 @@ int run_select(hire_ctx ctx, const float* scores, int64_t score_stride, int64_t 
     uint64_t* win = lists + B * kWinGroups * kWinBins * kBinCap;      // [B][C][seg]
     const uint32_t perm = sample_perm(static_cast<uint64_t>(n) / 4);
     CK(launch_k(ctx, sel_pivot_kernel, static_cast<unsigned>(B), kPivThreads, 0, scores, score_stride,
-                nn, K, perm, piv, gh));
+                nn, K, perm, piv, gh, 0));
     CK(launch_k(ctx, sel_window_kernel, dim3(static_cast<unsigned>(C), static_cast<unsigned>(B)), kWinThreads, 0,
                 scores, score_stride, nn, static_cast<const uint64_t*>(piv), win, seg, cnt, agg, gh, lists));
     CK(launch_k(ctx, sel_wselect_kernel, static_cast<unsigned>(B), kWselThreads, 0, scores, score_stride, nn, K,
@@ -1202,24 +1253,8 @@ int run_scores_fsel(hire_ctx ctx, const hire_scorer_s* a, const float* x, int64_
   fs.samp_step = f.samp_step;
   fs.n_samp = f.n_samp;
   fs.r_lo = f.r_lo;
-  {  // dedicated zero-at-rest buffer (the arena is shared with other ops)
-    const size_t need = static_cast<size_t>(B) * (kFselSampleMax + 2) * 8 + kFselCtr * 32 * 4 + static_cast<size_t>(B) * 8;
-    if (need > ctx->fzero_cap) {
-      if (ctx->fzero) {
-        CK(cudaStreamSynchronize(ctx->stream));
-        CK(cudaFree(ctx->fzero));
-        ctx->fzero = nullptr;
-      }
-      const size_t nb = std::max(need, ctx->fzero_cap * 2);
-      CK(cudaMalloc(&ctx->fzero, nb));
-      CK(cudaMemsetAsync(ctx->fzero, 0, nb, ctx->stream));
-      ctx->fzero_cap = nb;
-    }
-  }
-  fs.samp = static_cast<uint64_t*>(ctx->fzero);
-  fs.lo = static_cast<unsigned long long*>(ctx->fzero) + static_cast<size_t>(B) * kFselSampleMax;
-  fs.cnt = reinterpret_cast<unsigned*>(fs.lo + B);
-  fs.ctr = reinterpret_cast<unsigned*>(fs.lo + 2 * B);
+  RET(ensure_fzero(ctx, B));  // dedicated zero-at-rest buffer (the arena is shared with other ops)
+  fzero_layout(ctx, B, &fs);
   {
     const int64_t U = static_cast<int64_t>(f.G) * (8 / f.ks);
     const int64_t full = a->rows / 16 / U;  // complete rounds
@@ -1279,7 +1314,7 @@ int local_candidates(hire_ctx ctx, const hire_matrix_s* w, const hire_scorer_s* 
     RET(run_scores_fsel(ctx, a, x, B, p->phi, sp, t, cand, ordered));
   } else {
     RET(run_scores(ctx, a, x, B, p->phi, p->x_mode, p->strict, t.sw, t.scores, a->rows));
-    RET(run_select(ctx, t.scores, a->rows, a->rows, B, sp, t.surv, cand, sp.k_eff, t.status));
+    RET(run_select(ctx, t.scores, a->rows, a->rows, B, sp, t.surv, cand, sp.k_eff, t.status, ordered));
   }
   RET(run_recompute(ctx, w, cand, sp.k_eff, sp.k_eff, x, B, p->phi, p->strict, t.vals, sp.k_eff));
   return HIRE_OK;

@@ -565,7 +565,7 @@ constexpr int kBinCap = 32;    // keys kept per (group, bin) list
 
 __global__ void __launch_bounds__(kPivThreads) sel_pivot_kernel(
     const float* __restrict__ scores, int64_t stride, uint32_t n, uint32_t K, uint32_t perm,
-    uint64_t* __restrict__ piv, unsigned* __restrict__ gh) {
+    uint64_t* __restrict__ piv, unsigned* __restrict__ gh, int exact_lo) {
   constexpr int NT = kPivThreads, KPT = kSel2Sample / kPivThreads;
   __shared__ RangeScratch rs;
   __shared__ unsigned s_top;
@@ -600,9 +600,13 @@ __global__ void __launch_bounds__(kPivThreads) sel_pivot_kernel(
   const long long r_lo = static_cast<long long>(ceil(mu + 4.0 * sd + 1.0));
   // bounds, not exact order statistics: lo <= key(r_lo) with at most
   // 2 r_lo + 16 sample keys above it; hi >= key(r_hi) with fewer than r_hi above
-  const uint64_t hi = r_hi >= 1 ? block_range_select<NT>(src, kSel2Sample, r_hi, &rs, 2, 16) : ~0ull;
-  const uint64_t lo = r_lo <= kSel2Sample ? block_range_select<NT>(src, kSel2Sample, r_lo, &rs, 1, 2 * r_lo + 16)
-                                          : 1ull;
+  // exact_lo (the list path, sel_wlist_kernel): only lo, as the exact
+  // sample order statistic, so the listed keys stay near r_lo/S * n
+  const uint64_t hi = (r_hi >= 1 && !exact_lo) ? block_range_select<NT>(src, kSel2Sample, r_hi, &rs, 2, 16) : ~0ull;
+  const uint64_t lo = r_lo <= kSel2Sample
+                          ? (exact_lo ? block_range_select<NT>(src, kSel2Sample, r_lo, &rs)
+                                      : block_range_select<NT>(src, kSel2Sample, r_lo, &rs, 1, 2 * r_lo + 16))
+                          : 1ull;
   if (threadIdx.x == 0) {
     const unsigned vlo = static_cast<unsigned>(lo >> 32);
     const unsigned vtop = max(vlo, r_hi >= 1 ? static_cast<unsigned>(hi >> 32) : s_top);
@@ -716,6 +720,74 @@ __global__ void __launch_bounds__(kWinThreads) sel_window_kernel(
     cq[c] = s_above;
     cq[C + c] = s_wn;
   }
+}
+
+// ---------------------------------------------------------------------
+// S2' (list path). grid (C, B), 256 threads: every key >= lo of chunk c is
+// appended to query b's list (warp-aggregated atomics on cnt[b]; list order
+// is irrelevant — sel_fin_kernel selects T and emits through a row bitmap).
+// Replaces window + window-select + emit with one scan and the finisher.
+// ---------------------------------------------------------------------
+__global__ void __launch_bounds__(kWinThreads) sel_wlist_kernel(
+    const float* __restrict__ scores, int64_t stride, uint32_t n, const uint64_t* __restrict__ piv,
+    unsigned* __restrict__ cnt, uint64_t* __restrict__ lists, int cap) {
+  constexpr int NT = kWinThreads, U = kScanBatch, STAGE = 1024;
+  // keys are staged per CTA and reserved with ONE global atomic per CTA:
+  // same-address atomics from many CTAs serialise at L2
+  __shared__ uint64_t s_keys[STAGE];
+  __shared__ unsigned s_n, s_base;
+  hire_dev::griddep_wait();
+  hire_dev::griddep_launch();
+  KTrace kt_(kKtWindow);
+  const int b = blockIdx.y, C = gridDim.x, c = blockIdx.x;
+  const int lane = threadIdx.x & 31;
+  const float* row = scores + b * stride;
+  const uint64_t base_n = n / C, extra = n % C;
+  const uint32_t first = static_cast<uint32_t>(c * base_n + (static_cast<uint64_t>(c) < extra ? c : extra));
+  const uint32_t end = first + static_cast<uint32_t>(base_n + (static_cast<uint64_t>(c) < extra ? 1 : 0));
+  const uint64_t lo = piv[4 * b];
+  uint64_t* L = lists + static_cast<int64_t>(b) * cap;
+  if (threadIdx.x == 0) s_n = 0;
+  __syncthreads();
+  for (uint32_t i0 = first; i0 < end; i0 += NT * U) {
+    float v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const uint32_t i = i0 + u * NT + threadIdx.x;
+      v[u] = i < end ? row[i] : 0.0f;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const uint32_t i = i0 + u * NT + threadIdx.x;
+      const uint64_t k = make_key(v[u], i);
+      const bool in = i < end && k >= lo;
+      const unsigned bal = __ballot_sync(0xffffffffu, in);
+      if (bal) {
+        const int leader = __ffs(bal) - 1;
+        unsigned base = 0;
+        if (lane == leader) base = atomicAdd(&s_n, static_cast<unsigned>(__popc(bal)));
+        base = __shfl_sync(0xffffffffu, base, leader);
+        const unsigned pos = base + __popc(bal & ((1u << lane) - 1u));
+        if (in && pos < static_cast<unsigned>(STAGE)) s_keys[pos] = k;
+        if (base + __popc(bal) > static_cast<unsigned>(STAGE)) {  // stage full: straight to the list
+          const bool ovf = in && pos >= static_cast<unsigned>(STAGE);
+          const unsigned ob = __ballot_sync(0xffffffffu, ovf);
+          const int ol = __ffs(ob) - 1;
+          unsigned gb = 0;
+          if (lane == ol) gb = atomicAdd(cnt + b, static_cast<unsigned>(__popc(ob)));
+          gb = __shfl_sync(0xffffffffu, gb, ol);
+          const unsigned gp = gb + __popc(ob & ((1u << lane) - 1u));
+          if (ovf && gp < static_cast<unsigned>(cap)) L[gp] = k;
+        }
+      }
+    }
+  }
+  __syncthreads();
+  const unsigned staged = min(s_n, static_cast<unsigned>(STAGE));
+  if (threadIdx.x == 0) s_base = staged ? atomicAdd(cnt + b, staged) : 0u;
+  __syncthreads();
+  for (unsigned t = threadIdx.x; t < staged; t += NT)
+    if (s_base + t < static_cast<unsigned>(cap)) L[s_base + t] = s_keys[t];
 }
 
 // ---------------------------------------------------------------------
