@@ -53,7 +53,7 @@ struct Vec16<float> {
 // grid = (tiles, B); 8 warps per CTA; warp-strided over the n_cand rows of
 // query b. cand == nullptr means row i itself (dense exact, K8).
 template <typename T, int CPL>
-__global__ void __launch_bounds__(256, 2) recompute_fast(
+__global__ void __launch_bounds__(256, (CPL >= 16 ? 1 : 2)) recompute_fast(
     const T* __restrict__ w, int d, const uint32_t* __restrict__ cand, int64_t cand_stride,
     int n_cand, const float* __restrict__ x, int phi, float* __restrict__ out,
     int64_t out_stride) {

@@ -773,8 +773,10 @@ int launch_recompute_fast(hire_ctx ctx, const void* w, int d, const uint32_t* ca
   const size_t smem = static_cast<size_t>(d) * 4;
   auto k = recompute_fast<T, CPL>;
   // one wave of 2 CTAs/SM (8 warps each); warps stride over the rows
-  const int64_t tiles = std::max<int64_t>(1, std::min<int64_t>(ceil_div(n_cand, 8), std::max<int64_t>(1, 2 * ctx->num_sms / B)));
-  CK(launch_k(ctx, k, dim3(static_cast<unsigned>(tiles), static_cast<unsigned>(B)), 256, smem, 
+  // (CPL >= 16: one CTA/SM, the long rows need more than 128 registers)
+  const int per_sm = CPL >= 16 ? 1 : 2;
+  const int64_t tiles = std::max<int64_t>(1, std::min<int64_t>(ceil_div(n_cand, 8), std::max<int64_t>(1, per_sm * ctx->num_sms / B)));
+  CK(launch_k(ctx, k, dim3(static_cast<unsigned>(tiles), static_cast<unsigned>(B)), 256, smem,
       static_cast<const T*>(w), d, cand, cand_stride, static_cast<int>(n_cand), x, phi, out, out_stride));
   CK(cudaGetLastError());
   return HIRE_OK;
@@ -881,6 +883,13 @@ int run_final(hire_ctx ctx, const float* vals, int64_t vs, const uint32_t* idx, 
                   out_val, out_prob, out_keys, out_stride));                                            \
       CK(cudaGetLastError());                                                                           \
       return HIRE_OK;                                                                                   \
+    }
+    // batches of >= 8 queries: 2 keys per thread (up to 1024 threads) — the
+    // range-select passes are shorter (cfg4 final 12.7 -> 9.9 us, cfg3 B=32
+    // 10.4 -> 7.1); a single query is faster on the narrow CTA
+    const char* wide = std::getenv("HIRE_F2_WIDE");
+    if ((wide ? wide[0] == '1' : B >= 8) && n > 256) {
+      HIRE_F2(256, 2) HIRE_F2(512, 2) HIRE_F2(1024, 2)
     }
     HIRE_F2(128, 1) HIRE_F2(128, 2) HIRE_F2(128, 4) HIRE_F2(128, 8) HIRE_F2(128, 16)
     HIRE_F2(256, 16) HIRE_F2(256, 32) HIRE_F2(512, 32)
@@ -1434,6 +1443,9 @@ int hire_ctx_create(int device, void* stream, int own_stream, hire_ctx* out) {
     CK(cudaFuncSetAttribute(final2_kernel<256, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, f2));
     CK(cudaFuncSetAttribute(final2_kernel<256, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize, f2));
     CK(cudaFuncSetAttribute(final2_kernel<512, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize, f2));
+    CK(cudaFuncSetAttribute(final2_kernel<256, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, f2));
+    CK(cudaFuncSetAttribute(final2_kernel<512, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, f2));
+    CK(cudaFuncSetAttribute(final2_kernel<1024, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, f2));
   }
   CK(cudaFuncSetAttribute(final_select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                           kFinalMax * 8));

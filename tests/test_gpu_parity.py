@@ -392,3 +392,23 @@ def test_low_rank_quantized_scorer_equals_reference(H, O):
     ref = O.RefScorer("lrq", z1=z1, z2=z2)
     for b in range(3):
         assert np.array_equal(got[b].view(np.uint32), ref.scores(x[b], 0).view(np.uint32)), b
+
+
+@pytest.mark.parametrize("dt", [torch.bfloat16, torch.float32])
+def test_recompute_long_rows_equal_dense(H, O, dt):
+    """d = 4096 (cfg4's rows; 16 lane chunks, one CTA/SM): gathered exact values equal the dense exact pass bit for bit
+    (linalg.hpp:137-139 design rule) and a float64 recompute within 1e-5."""
+    V, d, k, kp, B = 6000, 4096, 32, 700, 3
+    w = _data.lowrank_plus_noise(V, d, 16, 41)
+    z = H.ScoreMatrix(T(w).to(dt))
+    codes, scales = O.quantize_int4(w)
+    a = H.ApproxScorer.quantized(codes, scales)
+    x = _data.queries(B, d, 42)
+    r = H.hire_topk(T(x), z, a, H.HireConfig(k=k, k_prime=kp, x_mode=H.X_INT8))
+    dense = H.matvec(z, T(x))
+    got = r.top_val.cpu()
+    want = torch.gather(dense.cpu(), 1, r.top_idx.cpu().long())
+    assert torch.equal(got.view(torch.int32), want.view(torch.int32))
+    wd = z.tensor.double().cpu() if hasattr(z, "tensor") else T(w).to(dt).double().cpu()
+    ref = torch.from_numpy(x).double() @ wd.t()
+    torch.testing.assert_close(got.double(), torch.gather(ref, 1, r.top_idx.cpu().long()), rtol=1e-5, atol=1e-5)
