@@ -493,8 +493,13 @@ int run_select(hire_ctx ctx, const float* scores, int64_t score_stride, int64_t 
       const int64_t CL = std::max<int64_t>(1, std::min<int64_t>(ceil_div(n, kWinThreads * kScanBatch),
                                                                 std::max<int64_t>(1, 8 * ctx->num_sms / B)));
       const uint32_t perm = sample_perm(static_cast<uint64_t>(n) / 4);
-      CK(launch_k(ctx, sel_pivot_kernel, static_cast<unsigned>(B), kPivThreads, 0, scores, score_stride, nn, K,
-                  perm, piv, reinterpret_cast<unsigned*>(surv + 5 * B), 1));
+      // sample select on 256 / 512 threads (8-16 keys each; 128 threads: cfg1
+      // pivot 7.0 -> 4.3 us); the 2048-key sample in 4-key blocks caps NT at 512
+      const char* pe = std::getenv("HIRE_PIV_NT");
+      const int pnt = pe ? std::atoi(pe) : (B >= 8 ? 512 : 256);
+      auto pk = pnt >= 512 ? sel_pivot_kernel<512> : pnt >= 256 ? sel_pivot_kernel<256> : sel_pivot_kernel<128>;
+      CK(launch_k(ctx, pk, static_cast<unsigned>(B), pnt >= 512 ? 512 : pnt >= 256 ? 256 : 128, 0,
+                  scores, score_stride, nn, K, perm, piv, reinterpret_cast<unsigned*>(surv + 5 * B), 1));
       CK(launch_k(ctx, sel_wlist_kernel, dim3(static_cast<unsigned>(CL), static_cast<unsigned>(B)), kWinThreads, 0,
                   scores, score_stride, nn, static_cast<const uint64_t*>(piv), fs.cnt, lists, hire_dev::kFinCap));
       CK(launch_k(ctx, sel_fin_kernel, static_cast<unsigned>(B), hire_dev::kFinThreads,
@@ -520,7 +525,7 @@ int run_select(hire_ctx ctx, const float* scores, int64_t score_stride, int64_t 
     uint64_t* lists = surv + 5 * B + B * kWinBins * kWinGroups / 2;  // [B][groups][bins][cap]
     uint64_t* win = lists + B * kWinGroups * kWinBins * kBinCap;      // [B][C][seg]
     const uint32_t perm = sample_perm(static_cast<uint64_t>(n) / 4);
-    CK(launch_k(ctx, sel_pivot_kernel, static_cast<unsigned>(B), kPivThreads, 0, scores, score_stride,
+    CK(launch_k(ctx, sel_pivot_kernel<kPivThreads>, static_cast<unsigned>(B), kPivThreads, 0, scores, score_stride,
                 nn, K, perm, piv, gh, 0));
     CK(launch_k(ctx, sel_window_kernel, dim3(static_cast<unsigned>(C), static_cast<unsigned>(B)), kWinThreads, 0,
                 scores, score_stride, nn, static_cast<const uint64_t*>(piv), win, seg, cnt, agg, gh, lists));

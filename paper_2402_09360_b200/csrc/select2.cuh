@@ -563,10 +563,12 @@ constexpr int kWinBins = 256;  // window histogram bins (value-word sub-ranges o
 constexpr int kWinGroups = 8;  // chunk groups with their own histogram (bounds same-address atomics)
 constexpr int kBinCap = 32;    // keys kept per (group, bin) list
 
-__global__ void __launch_bounds__(kPivThreads) sel_pivot_kernel(
+template <int NT>
+__global__ void __launch_bounds__(NT) sel_pivot_kernel(
     const float* __restrict__ scores, int64_t stride, uint32_t n, uint32_t K, uint32_t perm,
     uint64_t* __restrict__ piv, unsigned* __restrict__ gh, int exact_lo) {
-  constexpr int NT = kPivThreads, KPT = kSel2Sample / kPivThreads;
+  constexpr int KPT = kSel2Sample / NT;
+  static_assert(KPT % 4 == 0, "the sample is loaded in 4-key blocks per thread (NT <= 512)");
   __shared__ RangeScratch rs;
   __shared__ unsigned s_top;
   hire_dev::griddep_wait();
