@@ -114,3 +114,47 @@ def test_select_in_cuda_graph(H, O):
         for b in range(2):
             wi, wv, _ = O.topk_select(h[b], 1000)
             assert np.array_equal(N(idx[b]).astype(np.uint32), wi)
+
+
+@pytest.mark.parametrize("n,kp", [(200000, 8000), (200000, 8192), (100000, 6000), (40000, 3000),
+                                  (530000, 1024), (524288, 512)])
+def test_list_path_candidates(H, O, n, kp):
+    # the list-path selector (sampled lower bound -> staged per-CTA lists ->
+    # finisher) near its limits: k' at the 8192-key list cap (the listed
+    # count overflows -> exact fallback), integer proxy scores (ties), and
+    # rows just above / at kFinMaxRows (2^19; above it the window chain runs)
+    g = np.random.default_rng(n + kp)
+    d, r = 16, 4
+    z1 = g.standard_normal((r, d)).astype(np.float32)
+    z2 = np.round(g.standard_normal((n, r)) * 2).astype(np.float32)
+    w = g.standard_normal((n, d)).astype(np.float32)
+    x = np.round(g.standard_normal((3, d))).astype(np.float32)
+    a = H.ApproxScorer.low_rank(T(z1), T(z2))
+    res = H.hire_topk(T(x), H.ScoreMatrix(T(w)), a, H.HireConfig(k=5, k_prime=kp, strict=True))
+    for b in range(3):
+        s = O.lowrank_scores(z1, z2, x[b], 0)
+        want, _, _ = O.topk_select(s, kp)
+        assert np.array_equal(N(res.cand[b]).astype(np.uint32), np.sort(want.astype(np.uint32))), b
+
+
+@pytest.mark.parametrize("kind", ["spiky", "two_level", "relu", "ascending", "all_equal"])
+def test_list_path_equals_window_chain(H, O, kind, monkeypatch):
+    # same candidate sets from the list path and the window chain
+    # (HIRE_SEL_NOLIST=1) on adversarial score rows through hire_topk
+    n, kp, d = 150000, 2000, 8
+    v = _rows(n, 5)[kind]
+    z2 = v[:, None].astype(np.float32)  # rank-1 proxy: score_i = v_i * x
+    z1 = np.zeros((1, d), np.float32)
+    z1[0, 0] = 1.0
+    x = np.zeros((2, d), np.float32)
+    x[:, 0] = 1.0
+    w = np.random.default_rng(6).standard_normal((n, d)).astype(np.float32)
+    a = H.ApproxScorer.low_rank(T(z1), T(z2))
+    cfg = H.HireConfig(k=4, k_prime=kp, strict=True)
+    r1 = H.hire_topk(T(x), H.ScoreMatrix(T(w)), a, cfg)
+    monkeypatch.setenv("HIRE_SEL_NOLIST", "1")
+    r0 = H.hire_topk(T(x), H.ScoreMatrix(T(w)), a, cfg)
+    assert torch.equal(r1.cand, r0.cand)
+    assert torch.equal(r1.top_idx, r0.top_idx)
+    want, _, _ = O.topk_select(v, kp)
+    assert np.array_equal(N(r1.cand[0]).astype(np.uint32), np.sort(want.astype(np.uint32)))
