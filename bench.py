@@ -174,10 +174,10 @@ class FfnWorkload:
     def host_step(self, i, x_host, sel_host, out_host, ctx):
         H = self.H
         f, a = self.layers[i % len(self.layers)]
-        p = H._lib.FfnParams(self.k, self.kp, 1, 1, H.X_INT8, 0, 0)
-        H._lib.check(H.lib().hire_ffn_host(ctx.h, f.u.h, f.v.h, a.h, x_host.ctypes.data_as(C.c_void_p),
-                                           self.B, C.byref(p), sel_host.ctypes.data_as(C.c_void_p),
-                                           out_host.ctypes.data_as(C.c_void_p)))
+        if not hasattr(self, "_hp"):  # call parameters built once, as a serving loop would
+            self._hp = C.byref(H._lib.FfnParams(self.k, self.kp, 1, 1, H.X_INT8, 0, 0))
+        H._lib.check(H.lib().hire_ffn_host(ctx.h, f.u.h, f.v.h, a.h, x_host.ctypes.data, self.B, self._hp,
+                                           sel_host.ctypes.data, out_host.ctypes.data))
 
     def io_bytes(self):
         return self.B * self.d * 4, self.B * self.k * 4 + self.B * self.d * 4
@@ -254,12 +254,12 @@ class SoftmaxWorkload:
 
     def host_step(self, i, x_host, idx_host, val_host, ctx):
         H = self.H
-        p = self.cfg.params()
-        n1, n2, cl = C.c_int64(), C.c_int64(), C.c_int()
-        H._lib.check(H.lib().hire_topk_host(ctx.h, self.W.h, self.A.h, x_host.ctypes.data_as(C.c_void_p),
-                                            self.B, C.byref(p), None, idx_host.ctypes.data_as(C.c_void_p),
-                                            val_host.ctypes.data_as(C.c_void_p), None, C.byref(n1),
-                                            C.byref(n2), C.byref(cl)))
+        if not hasattr(self, "_hp"):  # call parameters built once, as a serving loop would
+            self._hp = C.byref(self.cfg.params())
+            self._hn = (C.c_int64(), C.c_int64(), C.c_int())
+            self._hr = tuple(C.byref(v) for v in self._hn)
+        H._lib.check(H.lib().hire_topk_host(ctx.h, self.W.h, self.A.h, x_host.ctypes.data, self.B, self._hp, None,
+                                            idx_host.ctypes.data, val_host.ctypes.data, None, *self._hr))
 
     def io_bytes(self):
         return self.B * self.d * 4, self.B * self.k * 8
@@ -336,12 +336,12 @@ class LowRankSoftmaxWorkload:
     def host_step(self, i, x_host, idx_host, val_host, ctx):
         H = self.H
         z, a = self.copies[i % len(self.copies)]
-        p = self.cfg.params()
-        n1, n2, cl = C.c_int64(), C.c_int64(), C.c_int()
-        H._lib.check(H.lib().hire_topk_host(ctx.h, z.h, a.h, x_host.ctypes.data_as(C.c_void_p), self.B,
-                                            C.byref(p), None, idx_host.ctypes.data_as(C.c_void_p),
-                                            val_host.ctypes.data_as(C.c_void_p), None, C.byref(n1),
-                                            C.byref(n2), C.byref(cl)))
+        if not hasattr(self, "_hp"):  # call parameters built once, as a serving loop would
+            self._hp = C.byref(self.cfg.params())
+            self._hn = (C.c_int64(), C.c_int64(), C.c_int())
+            self._hr = tuple(C.byref(v) for v in self._hn)
+        H._lib.check(H.lib().hire_topk_host(ctx.h, z.h, a.h, x_host.ctypes.data, self.B, self._hp, None,
+                                            idx_host.ctypes.data, val_host.ctypes.data, None, *self._hr))
 
     def io_bytes(self):
         return self.B * self.d * 4, self.B * self.k * 8
