@@ -424,11 +424,26 @@ class DaSoftmaxWorkload:
                               merge=self.H.MERGE_GLOBAL)
 
     def host_step(self, i, x_host, idx_host, val_host, ctx):
-        xd = torch.from_numpy(x_host).cuda(non_blocking=False)
-        ti, tv, _ = self.P.da_topk(self.W, self.A, self.V, xd, self.cfg, self.comm,
+        H = self.H
+        if self.world == 1:
+            # one shard: DA-TOP-k is hire_topk (hire_da_topk_run's own world-1
+            # shortcut), whose host-buffer entry point is hire_topk_host
+            if not hasattr(self, "_hp"):
+                self._hp = C.byref(self.cfg.params())
+                self._hn = (C.c_int64(), C.c_int64(), C.c_int())
+                self._hr = tuple(C.byref(v) for v in self._hn)
+            H._lib.check(H.lib().hire_topk_host(ctx.h, self.W.h, self.A.h, x_host.ctypes.data, self.B, self._hp,
+                                                None, idx_host.ctypes.data, val_host.ctypes.data, None, *self._hr))
+            return
+        # N > 1: pinned host buffers, asynchronous copies, one synchronise
+        if not hasattr(self, "_xd"):
+            self._xd = torch.empty(self.B, self.d, device="cuda")
+        self._xd.copy_(torch.from_numpy(x_host), non_blocking=True)
+        ti, tv, _ = self.P.da_topk(self.W, self.A, self.V, self._xd, self.cfg, self.comm,
                                    merge=self.H.MERGE_GLOBAL, ctx=None)
-        idx_host[:] = ti.cpu().numpy()
-        val_host[:] = tv.cpu().numpy()
+        torch.from_numpy(idx_host.view(np.int32)).copy_(ti, non_blocking=True)
+        torch.from_numpy(val_host).copy_(tv, non_blocking=True)
+        torch.cuda.current_stream().synchronize()
 
     def io_bytes(self):
         return self.B * self.d * 4, self.B * self.k * 8
