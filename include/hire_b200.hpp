@@ -721,4 +721,29 @@ inline RecallReport recall(const CandidateSet& candidates, const TopKSet& exact)
   return r;
 }
 
+// metrics.hpp:43-64 — the paper's parameter-bytes cost model (host integer
+// arithmetic; like the reference, the int4 term leaves out the scales)
+struct CostReport {
+  std::uint64_t bytes_baseline = 0;
+  std::uint64_t bytes_lr = 0;
+  std::uint64_t bytes_q = 0;
+  std::uint64_t bytes_lrq = 0;
+  bool lr_no_saving = false;
+  bool q_no_saving = false;
+  bool lrq_no_saving = false;
+};
+
+inline CostReport param_bytes(std::uint64_t d, std::uint64_t l, std::uint64_t r, std::uint64_t k_prime) {
+  if (d < 1 || l < 1 || r < 1) throw std::invalid_argument("param_bytes: dims must be positive");
+  CostReport c;
+  c.bytes_baseline = 2 * d * l;
+  c.bytes_lr = 2 * (d * r + r * l + d * k_prime);
+  c.bytes_q = (d * l + 1) / 2 + 2 * d * k_prime;
+  c.bytes_lrq = (d * r + r * l + 1) / 2 + 2 * d * k_prime;
+  c.lr_no_saving = c.bytes_lr >= c.bytes_baseline;
+  c.q_no_saving = c.bytes_q >= c.bytes_baseline;
+  c.lrq_no_saving = c.bytes_lrq >= c.bytes_baseline;
+  return c;
+}
+
 }  // namespace hire

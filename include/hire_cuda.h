@@ -204,12 +204,31 @@ HIRE_API int hire_comm_destroy(hire_comm c);
 /* One rank's share: w_shard / a_shard are rows [first, first+width) of the
  * full matrix under the shard width rule (distributed.hpp:53-57); total_rows
  * is l. uneven = 1 allows quotas that s does not divide (first k % s shards
- * take one more). comm NULL means world == 1. Every rank gets the merged
- * top_idx/top_val [B][k] (row stride k, first n_top valid). */
+ * take one more). Every rank gets the merged top_idx/top_val [B][k] (row
+ * stride k, first n_top valid).
+ * hire_da_topk_run = hire_da_topk_local -> one ncclAllGather of the B x slots
+ * rank keys -> hire_da_topk_merge. comm NULL (world must be 1) runs
+ * hire_topk directly (the reference's s = 1 equivalence); a 1-rank
+ * communicator runs the full local -> all-gather -> merge chain. */
 HIRE_API int hire_da_topk_run(hire_ctx ctx, hire_comm comm, hire_matrix w_shard, hire_scorer a_shard,
                      int64_t total_rows, int world, int rank, const float* x, int64_t B,
                      const hire_topk_params* p, int merge, int uneven, uint32_t* top_idx,
                      float* top_val, int64_t* n_top, int* clamped);
+/* The two halves of hire_da_topk_run, for callers that move the keys
+ * themselves (another transport, or tests driving the exchange):
+ * local writes this rank's keys (8-byte rank keys of (exact value, global
+ * index), distributed.hpp:94-125; padding slots 0) into send [B][slots];
+ * merge takes the gathered [world][B][slots] keys (rank-major) and writes
+ * the merged top-k (distributed.hpp:127-131 for PER_SHARD; the global
+ * exact top-k for GLOBAL). slots = ceil(k/world) (PER_SHARD) or
+ * ceil(k_prime/world) (GLOBAL). */
+HIRE_API int hire_da_topk_slots(const hire_topk_params* p, int world, int merge, int64_t* slots);
+HIRE_API int hire_da_topk_local(hire_ctx ctx, hire_matrix w_shard, hire_scorer a_shard, int64_t total_rows,
+                                int world, int rank, const float* x, int64_t B, const hire_topk_params* p,
+                                int merge, int uneven, uint64_t* send);
+HIRE_API int hire_da_topk_merge(hire_ctx ctx, const uint64_t* gathered, int64_t total_rows, int world,
+                                int64_t B, const hire_topk_params* p, int merge, int uneven,
+                                uint32_t* top_idx, float* top_val, int64_t* n_top, int* clamped);
 /* All `world` shards on this one device, no collective (the per-shard local
  * stages write straight into the gathered buffer): the single-GPU
  * emulation of hire_da_topk_run used for parity at D > 1. */
@@ -218,12 +237,29 @@ HIRE_API int hire_da_topk_emulated(hire_ctx ctx, hire_matrix w, hire_scorer a, i
                           int uneven, uint32_t* top_idx, float* top_val, int64_t* n_top,
                           int* clamped);
 /* da_group_sparse: local select with local quotas, local partial
- * down-projection, NCCL all-reduce (sum) of out [B][d]; sel gets the union
- * [B][k/g] of selected groups (ascending). */
+ * down-projection; one grouped NCCL all-gather of the selected group ids and
+ * the partial outputs; out [B][d] = the partials summed in rank order (the
+ * same bits on every rank and topology); sel gets the union [B][k/g] of
+ * selected groups (ascending). comm NULL: world must be 1. */
 HIRE_API int hire_da_ffn_run(hire_ctx ctx, hire_comm comm, hire_matrix u_shard, hire_matrix v_shard,
                     hire_scorer a_shard, int64_t total_units, int world, int rank,
                     const float* x, int64_t B, const hire_ffn_params* p, int uneven,
                     uint32_t* sel, float* out);
+/* The halves of hire_da_ffn_run: local writes this rank's selected group
+ * ids (global, ascending) into sel_send [B][slots] and its partial output
+ * into partial [B][d]; merge takes the gathered ids [world][B][slots] and
+ * partials [world][B][d] and writes sel [B][k/g] and out [B][d].
+ * slots = ceil((k/g)/world). */
+HIRE_API int hire_da_ffn_slots(const hire_ffn_params* p, int world, int64_t* slots);
+HIRE_API int hire_da_ffn_local(hire_ctx ctx, hire_matrix u_shard, hire_matrix v_shard, hire_scorer a_shard,
+                               int64_t total_units, int world, int rank, const float* x, int64_t B,
+                               const hire_ffn_params* p, int uneven, uint32_t* sel_send, float* partial);
+HIRE_API int hire_da_ffn_merge(hire_ctx ctx, const uint32_t* gathered_sel, const float* gathered_parts,
+                               int64_t total_units, int64_t d, int world, int64_t B, const hire_ffn_params* p,
+                               int uneven, uint32_t* sel, float* out);
+/* Single-GPU emulation of hire_da_ffn_run over `world` shards (strict: the
+ * reference's one ascending sum over the union; else the rank-order sum
+ * hire_da_ffn_run computes). */
 HIRE_API int hire_da_ffn_emulated(hire_ctx ctx, hire_matrix u, hire_matrix v, hire_scorer a, int world,
                          const float* x, int64_t B, const hire_ffn_params* p, int uneven,
                          uint32_t* sel, float* out);

@@ -36,6 +36,8 @@ EXPORTS = [
     "hire_ffn_run", "hire_ffn_host", "hire_ffn_dense_run", "hire_ffn_union_select", "hire_ffn_common_path_run",
     "hire_comm_unique_id", "hire_comm_create", "hire_comm_destroy",
     "hire_da_topk_run", "hire_da_topk_emulated", "hire_da_ffn_run", "hire_da_ffn_emulated",
+    "hire_da_topk_slots", "hire_da_topk_local", "hire_da_topk_merge",
+    "hire_da_ffn_slots", "hire_da_ffn_local", "hire_da_ffn_merge",
 ]
 
 
@@ -119,6 +121,13 @@ def _sig(L):
                             _i32, _vp, _vp],
         "hire_da_ffn_emulated": [_vp, _vp, _vp, _vp, _i32, _vp, _i64, _p(FfnParams), _i32,
                                  _vp, _vp],
+        "hire_da_topk_slots": [_p(TopkParams), _i32, _i32, _p(_i64)],
+        "hire_da_topk_local": [_vp, _vp, _vp, _i64, _i32, _i32, _vp, _i64, _p(TopkParams), _i32, _i32, _vp],
+        "hire_da_topk_merge": [_vp, _vp, _i64, _i32, _i64, _p(TopkParams), _i32, _i32, _vp, _vp, _p(_i64),
+                               _p(_i32)],
+        "hire_da_ffn_slots": [_p(FfnParams), _i32, _p(_i64)],
+        "hire_da_ffn_local": [_vp, _vp, _vp, _vp, _i64, _i32, _i32, _vp, _i64, _p(FfnParams), _i32, _vp, _vp],
+        "hire_da_ffn_merge": [_vp, _vp, _vp, _i64, _i64, _i32, _i64, _p(FfnParams), _i32, _vp, _vp],
     }
     for name, args in sigs.items():
         f = getattr(L, name)

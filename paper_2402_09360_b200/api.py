@@ -492,6 +492,52 @@ def da_group_sparse_emulated(f: GroupedFFN, x: torch.Tensor, a: ApproxScorer, k:
     return out, sel
 
 
+@dataclass
+class CostReport:
+    """metrics.hpp:43-51."""
+    bytes_baseline: int = 0
+    bytes_lr: int = 0
+    bytes_q: int = 0
+    bytes_lrq: int = 0
+    lr_no_saving: bool = False
+    q_no_saving: bool = False
+    lrq_no_saving: bool = False
+
+
+def param_bytes(d: int, l: int, r: int, k_prime: int) -> CostReport:
+    """metrics.hpp:51-64: the paper's parameter bytes per query (bf16 dense
+    2dl; low-rank 2(dr + rl + dk'); int4 ceil(dl/2) + 2dk'; LRQ
+    ceil((dr + rl)/2) + 2dk'). Like the reference it omits the int4 scales;
+    roofline_bytes adds them."""
+    if d < 1 or l < 1 or r < 1:
+        raise L.HireInvalidArgument(L.ERR_INVALID, "param_bytes: dims must be positive")
+    c = CostReport()
+    c.bytes_baseline = 2 * d * l
+    c.bytes_lr = 2 * (d * r + r * l + d * k_prime)
+    c.bytes_q = (d * l + 1) // 2 + 2 * d * k_prime
+    c.bytes_lrq = (d * r + r * l + 1) // 2 + 2 * d * k_prime
+    c.lr_no_saving = c.bytes_lr >= c.bytes_baseline
+    c.q_no_saving = c.bytes_q >= c.bytes_baseline
+    c.lrq_no_saving = c.bytes_lrq >= c.bytes_baseline
+    return c
+
+
+def roofline_bytes(proxy: str, d: int, l: int, gathered_rows: int, row_bytes: int, r: int = 0,
+                   factor_bytes: int = 2, extra_rows: int = 0, exchange_bytes: int = 0) -> int:
+    """HBM bytes one step must move:
+    proxy bytes INCLUDING the int4 scales (param_bytes' Q term omits them)
+    + unique gathered rows x row bytes (+ extra_rows: the FFN's V rows)
+    + all-gather bytes. proxy 'q4': ceil(dl/2) + 4l; 'lowrank': (dr + rl) x
+    factor_bytes. gathered_rows counts each row once per step (batch union)."""
+    if proxy == "q4":
+        pb = (d * l + 1) // 2 + 4 * l
+    elif proxy == "lowrank":
+        pb = (d * r + r * l) * factor_bytes
+    else:
+        raise ValueError(f"unknown proxy kind {proxy!r}")
+    return pb + (gathered_rows + extra_rows) * row_bytes + exchange_bytes
+
+
 def recall(cand: np.ndarray, exact_idx: np.ndarray):
     """metrics.hpp:23-34 for one query: (recall, intersection_k, top1_agree)."""
     cand = np.asarray(cand)

@@ -28,23 +28,37 @@ def nvcc() -> str:
     return "nvcc"
 
 
+def _src_hash() -> str:
+    import hashlib
+    h = hashlib.sha256(" ".join(NVCC_FLAGS + os.environ.get("HIRE_NVCC_EXTRA", "").split()).encode())
+    for p in sorted(DEPS):
+        with open(p, "rb") as f:
+            h.update(f.read())
+    return h.hexdigest()
+
+
 def stale() -> bool:
-    if not os.path.exists(LIB):
+    """The library is stale unless it was built from exactly these sources
+    (a hash beside the .so; mtimes lie when sources change mid-build)."""
+    if not os.path.exists(LIB) or not os.path.exists(LIB + ".srchash"):
         return True
-    t = os.path.getmtime(LIB)
-    return any(os.path.getmtime(p) > t for p in DEPS)
+    with open(LIB + ".srchash") as f:
+        return f.read().strip() != _src_hash()
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not stale():
         return LIB
     extra = os.environ.get("HIRE_NVCC_EXTRA", "").split()  # experiments only
+    h = _src_hash()  # of the sources as they are when the compile starts
     cmd = [nvcc(), *NVCC_FLAGS, *extra, "-o", LIB, *SOURCES, "-lnccl"]
     if verbose:
         print(" ".join(cmd), file=sys.stderr)
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"nvcc failed ({r.returncode}):\n{r.stderr[-4000:]}")
+    with open(LIB + ".srchash", "w") as f:
+        f.write(h + "\n")
     return LIB
 
 

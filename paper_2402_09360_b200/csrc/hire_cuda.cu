@@ -9,10 +9,13 @@
 // hire.hpp:123-144, ffn_group_sparse ffn.hpp:211-219 (select_groups :175-201,
 // ffn_apply_groups :154-171), da_topk distributed.hpp:73-134,
 // da_group_sparse distributed.hpp:145-206.
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 #include <nccl.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -29,6 +32,7 @@
 #include "select.cuh"
 #include "select2.cuh"
 #include "fsel.cuh"
+#include "score_umma.cuh"
 
 using namespace hire_dev;
 
@@ -98,7 +102,8 @@ struct hire_ctx_s {
     cudaGraphExec_t exec = nullptr;
     int64_t out[4] = {0, 0, 0, 0};
   };
-  std::vector<HostGraph> hgraphs;
+  static constexpr size_t kMaxHostGraphs = 64;
+  std::vector<HostGraph> hgraphs;  // least recently used first
   std::vector<std::vector<int64_t>> hseen;
   bool host_graphs = true;
   cudaStream_t gstream = nullptr;
@@ -153,7 +158,15 @@ struct StageScope {
 };
 }  // namespace
 
+namespace {
+// Process-wide handle ids: host-call graphs are keyed on these, never on a
+// handle's address (a freed handle's address can be reused by a new one).
+std::atomic<uint64_t> g_next_uid{1};
+uint64_t next_uid() { return g_next_uid.fetch_add(1, std::memory_order_relaxed); }
+}  // namespace
+
 struct hire_matrix_s {
+  uint64_t uid = next_uid();
   void* ptr = nullptr;
   int64_t rows = 0, d = 0;
   int dtype = HIRE_F32;
@@ -161,6 +174,7 @@ struct hire_matrix_s {
 };
 
 struct hire_scorer_s {
+  uint64_t uid = next_uid();
   int kind = HIRE_SCORER_Q4;
   int64_t rows = 0, d = 0, r = 0;
   // int4
@@ -169,6 +183,10 @@ struct hire_scorer_s {
   float* scales = nullptr;
   uint4* mma = nullptr;        // MMA-tiled copy for the tensor-core proxy (lazy)
   bool mma_owned = false;
+  uint32_t* umma = nullptr;    // tcgen05 layout (128-row blocks) for B >= 9 (lazy)
+  bool umma_owned = false;
+  CUtensorMap umap;            // TMA descriptor of `umma` (built with it)
+  bool umap_ok = false;
   // low-rank
   void* z1 = nullptr;
   void* z2 = nullptr;
@@ -568,7 +586,7 @@ struct ScoreWs {
 
 void take_score_ws(Arena& ar, ScoreWs* w, const hire_scorer_s* a, int64_t B) {
   ar.take(&w->xq, static_cast<size_t>(B * a->d));
-  ar.take(&w->xperm, static_cast<size_t>(B * a->d));
+  ar.take(&w->xperm, static_cast<size_t>((B + 15) / 16 * 16 * a->d));  // + zero padding queries (tcgen05 B layout)
   ar.take(&w->sx, static_cast<size_t>(B));
   ar.take(&w->sumxq, static_cast<size_t>(B));
   ar.take(&w->t, static_cast<size_t>(B * std::max<int64_t>(a->r, 1)));
@@ -630,6 +648,76 @@ int ensure_mma_layout(hire_ctx ctx, hire_scorer_s* a) {
   return HIRE_OK;
 }
 
+// ---- tcgen05 proxy (score_umma.cuh) ----
+bool umma_shape_ok(const hire_scorer_s* a, int64_t nb) {
+  if (a->d % 256 != 0 || nb < 1 || nb > 64) return false;
+  const int nq = static_cast<int>((nb + 15) / 16 * 16);
+  return UmmaSmem::bytes(4, nq, static_cast<int>(a->d)) <= 227 * 1024;  // at least a 4-stage ring
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      p = nullptr;
+    return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }();
+  return fn;
+}
+
+int ensure_umma_layout(hire_ctx ctx, hire_scorer_s* a) {
+  if (!a->umma) {
+    const int64_t n_rb = ceil_div(a->rows, kUmmaRows);
+    const int64_t n_words = n_rb * (a->d / 32) * 512;
+    CK(cudaMalloc(&a->umma, static_cast<size_t>(n_words) * 4));
+    a->umma_owned = true;
+    CK(launch_k(ctx, q4_to_umma_layout, static_cast<unsigned>(ceil_div(n_words, 256)), 256, 0, a->codes,
+                a->pitch, a->rows, static_cast<int>(a->d), a->umma, n_words));
+  }
+  if (!a->umap_ok) {
+    auto enc = tensor_map_encoder();
+    if (!enc) return set_err(HIRE_ERR_RUNTIME, "cuTensorMapEncodeTiled is unavailable");
+    // 2-D u64 view: inner dim = one k chunk of a row block (128 rows x 16 B
+    // = 256 x 8 B), outer dim = (row block, k chunk) pairs
+    const cuuint64_t dims[2] = {256, static_cast<cuuint64_t>(ceil_div(a->rows, kUmmaRows) * (a->d / 32))};
+    const cuuint64_t strides[1] = {2048};
+    const cuuint32_t box[2] = {256, static_cast<cuuint32_t>(kUmmaStageChunks)};
+    const cuuint32_t estr[2] = {1, 1};
+    const CUresult r = enc(&a->umap, CU_TENSOR_MAP_DATA_TYPE_UINT64, 2, a->umma, dims, strides, box, estr,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return set_err(HIRE_ERR_RUNTIME, "cuTensorMapEncodeTiled failed: " + std::to_string(r));
+    a->umap_ok = true;
+  }
+  return HIRE_OK;
+}
+
+int launch_q4_umma(hire_ctx ctx, hire_scorer_s* a, const ScoreWs& w, int64_t b0, int64_t nb, int phi, float* out,
+                   int64_t stride) {
+  RET(ensure_umma_layout(ctx, a));
+  const int d = static_cast<int>(a->d);
+  const int nq = static_cast<int>((nb + 15) / 16 * 16);
+  const int stages = UmmaSmem::stages_for(nq, d, 227 * 1024);
+  const size_t smem = UmmaSmem::bytes(stages, nq, d);  // attribute set in hire_ctx_create
+  const int64_t n_rb = ceil_div(a->rows, kUmmaRows);
+  const int grid = static_cast<int>(std::min<int64_t>(n_rb, ctx->num_sms));
+  // x operand of this chunk: groups of 8 queries, 8d bytes each (b0 % 64 == 0)
+  CK(launch_k(ctx, q4_score_umma, grid, kUmmaThreads, smem, a->umap, a->rows, d, a->scales, w.xperm + b0 * d,
+              w.sx + b0, w.sumxq + b0, static_cast<int>(nb), nq, stages, phi, out + b0 * stride, stride));
+  return HIRE_OK;
+}
+
+// the tcgen05 proxy from this many queries per launch up (HIRE_UMMA_MIN_B overrides; 0 = off)
+int64_t umma_min_batch() {
+  static const int64_t v = [] {
+    const char* e = std::getenv("HIRE_UMMA_MIN_B");
+    return e ? static_cast<int64_t>(std::atoi(e)) : static_cast<int64_t>(9);
+  }();
+  return v;
+}
+
 template <int NT, int KS>
 int launch_q4_mma_t(hire_ctx ctx, const hire_scorer_s* a, const ScoreWs& w, int64_t b0, int64_t nb,
                     int phi, float* out, int64_t stride) {
@@ -679,19 +767,30 @@ int launch_q4_mma(hire_ctx ctx, const hire_scorer_s* a, const ScoreWs& w, int64_
 int run_scores(hire_ctx ctx, const hire_scorer_s* a, const float* x, int64_t B, int phi,
                int x_mode, int strict, const ScoreWs& w, float* out, int64_t stride) {
   const int d = static_cast<int>(a->d);
+  // the tcgen05 proxy takes every 64-query chunk of >= umma_min_batch()
+  // queries; its x operand is prep's grouped layout (xperm, xg_mode 1)
+  const bool umma = a->kind == HIRE_SCORER_Q4 && x_mode == HIRE_X_INT8 && d % 64 == 0 && !ctx->force_dp4a &&
+                    umma_min_batch() > 0 && std::min<int64_t>(B, 64) >= umma_min_batch() &&
+                    umma_shape_ok(a, std::min<int64_t>(B, 64));
   if (a->kind == HIRE_SCORER_Q4 && x_mode == HIRE_X_INT8) {
     StageScope pscope(ctx, kStagePrep);
-    CK(launch_k(ctx, prep_x_int8_kernel, static_cast<unsigned>(B), 256, 0, x, d, w.xq, w.xperm, w.sx, w.sumxq));
+    const int64_t grid = umma ? (B + 15) / 16 * 16 : B;
+    CK(launch_k(ctx, prep_x_int8_kernel, static_cast<unsigned>(grid), 256, 0, x, d, w.xq, w.xperm, w.sx, w.sumxq,
+                umma ? 1 : 0, static_cast<int>(B)));
     CK(cudaGetLastError());
   }
   StageScope scope(ctx, kStageProxy);
   if (a->kind == HIRE_SCORER_Q4) {
     if (x_mode == HIRE_X_INT8 && d % 64 == 0 && !ctx->force_dp4a) {
-      RET(ensure_mma_layout(ctx, const_cast<hire_scorer_s*>(a)));
       int64_t b0 = 0;
       while (b0 < B) {
         const int64_t nb = std::min<int64_t>(64, B - b0);
-        RET(launch_q4_mma(ctx, a, w, b0, nb, phi, out, stride));
+        if (umma && nb >= umma_min_batch()) {
+          RET(launch_q4_umma(ctx, const_cast<hire_scorer_s*>(a), w, b0, nb, phi, out, stride));
+        } else {
+          RET(ensure_mma_layout(ctx, const_cast<hire_scorer_s*>(a)));
+          RET(launch_q4_mma(ctx, a, w, b0, nb, phi, out, stride));
+        }
         b0 += nb;
       }
       return HIRE_OK;
@@ -1256,7 +1355,7 @@ int run_scores_fsel(hire_ctx ctx, const hire_scorer_s* a, const float* x, int64_
   if (!fold) {
     StageScope pscope(ctx, kStagePrep);
     CK(launch_k(ctx, prep_x_int8_kernel, static_cast<unsigned>(B), 256, 0, x, d, t.sw.xq, t.sw.xperm, t.sw.sx,
-                t.sw.sumxq));
+                t.sw.sumxq, 0, static_cast<int>(B)));
   }
   FuseSel fs;
   fs.xf = fold ? x : nullptr;
@@ -1347,8 +1446,12 @@ int run_host_graph(hire_ctx ctx, const std::vector<int64_t>& key, int64_t* out, 
   *done_on = ctx->stream;
   if (!ctx->host_graphs || ctx->prof) return body(out);
   const auto bufs = ctx->buf_snapshot();
-  for (auto& g : ctx->hgraphs)
-    if (g.key == key && g.bufs == bufs) {
+  for (size_t gi = 0; gi < ctx->hgraphs.size(); ++gi)
+    if (ctx->hgraphs[gi].key == key && ctx->hgraphs[gi].bufs == bufs) {
+      if (gi + 1 != ctx->hgraphs.size())  // most recently used goes last
+        std::rotate(ctx->hgraphs.begin() + static_cast<long>(gi), ctx->hgraphs.begin() + static_cast<long>(gi) + 1,
+                    ctx->hgraphs.end());
+      auto& g = ctx->hgraphs.back();
       // order after earlier work on the context stream only if there is any
       if (cudaStreamQuery(ctx->stream) != cudaSuccess) {
         cudaGetLastError();
@@ -1363,6 +1466,7 @@ int run_host_graph(hire_ctx ctx, const std::vector<int64_t>& key, int64_t* out, 
   bool seen = false;
   for (auto& k : ctx->hseen) seen |= k == key;
   if (!seen) {  // eager first call: allocations, lazy layouts, static state
+    if (ctx->hseen.size() >= hire_ctx_s::kMaxHostGraphs * 4) ctx->hseen.erase(ctx->hseen.begin());
     ctx->hseen.push_back(key);
     return body(out);
   }
@@ -1402,6 +1506,10 @@ int run_host_graph(hire_ctx ctx, const std::vector<int64_t>& key, int64_t* out, 
   const cudaError_t ei = cudaGraphInstantiate(&exec, graph, 0);
   cudaGraphDestroy(graph);
   CK(ei);
+  if (ctx->hgraphs.size() >= hire_ctx_s::kMaxHostGraphs) {  // bounded: evict the least recently used
+    cudaGraphExecDestroy(ctx->hgraphs.front().exec);
+    ctx->hgraphs.erase(ctx->hgraphs.begin());
+  }
   ctx->hgraphs.push_back({key, bufs, exec, {out[0], out[1], out[2], out[3]}});
   CK(cudaGraphLaunch(exec, ctx->gstream));
   *done_on = ctx->gstream;
@@ -1477,6 +1585,7 @@ int hire_ctx_create(int device, void* stream, int own_stream, hire_ctx* out) {
         (const void*)lr_score_generic<__nv_bfloat16, true>,
         (const void*)lr_score_generic<__nv_bfloat16, false>};
     for (const void* k : ks) CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
+    CK(cudaFuncSetAttribute(q4_score_umma, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
   }
   if (const char* e = getenv("HIRE_PROXY_KERNEL")) c->force_dp4a = std::strcmp(e, "dp4a") == 0;
   if (const char* e = getenv("HIRE_FFN_FUSED")) c->ffn_fused = std::strcmp(e, "1") == 0;
@@ -1797,6 +1906,7 @@ int hire_scorer_slice(hire_scorer a, int64_t first, int64_t count, hire_scorer* 
   if (!a || !out) return invalid("null argument");
   if (first < 0 || count < 1 || first + count > a->rows) return invalid("ApproxScorer::slice_cols: out of range");
   auto* s = new hire_scorer_s(*a);
+  s->uid = next_uid();
   s->owned = false;
   s->rows = count;
   s->mma = nullptr;
@@ -1805,6 +1915,10 @@ int hire_scorer_slice(hire_scorer a, int64_t first, int64_t count, hire_scorer* 
     s->codes = a->codes + first * a->pitch;
     s->scales = a->scales + first;
     if (a->mma && first % 16 == 0) s->mma = a->mma + (first / 16) * (a->d / 64) * 32;
+    s->umma = nullptr;
+    s->umma_owned = false;
+    s->umap_ok = false;
+    if (a->umma && first % kUmmaRows == 0) s->umma = a->umma + (first / kUmmaRows) * (a->d / 32) * 512;
   } else {
     s->z2 = static_cast<char*>(a->z2) + first * a->r * dtype_size(a->dtype);
   }
@@ -1846,6 +1960,7 @@ int hire_scorer_destroy(hire_scorer a) {
     cudaFree(a->z2);
   }
   if (a->mma_owned) cudaFree(a->mma);
+  if (a->umma_owned) cudaFree(a->umma);
   delete a;
   return HIRE_OK;
 }
@@ -1952,15 +2067,17 @@ int hire_topk_host(hire_ctx ctx, hire_matrix w, hire_scorer a, const float* x_ho
   RET(ensure_host(&ctx->io_host, &ctx->io_host_cap, in_bytes + out_bytes, ctx->stream));
   char* dv = static_cast<char*>(ctx->io_dev);
   char* hs = static_cast<char*>(ctx->io_host);
-  void* xd = nullptr;  // staged (see hire_ffn_host)
+  // the input is staged into the context's mapped buffer (the graph reads it
+  // from there); results are written into the same mapped buffer and copied
+  // out after the synchronise
   std::memcpy(hs, x_host, xb);
-  const std::vector<int64_t> key = {1, reinterpret_cast<int64_t>(w), reinterpret_cast<int64_t>(a), B, p->k, p->k_prime,
+  const std::vector<int64_t> key = {1, static_cast<int64_t>(w->uid), static_cast<int64_t>(a->uid), B, p->k, p->k_prime,
                                     p->phi, p->x_mode, p->select, p->strict, p->n_buckets, p->bucket_t,
-                                    cb ? 1 : 0, pb ? 1 : 0, reinterpret_cast<int64_t>(xd)};
+                                    cb ? 1 : 0, pb ? 1 : 0};
   int64_t res[4];
   cudaStream_t done_on = nullptr;
   RET(run_host_graph(ctx, key, res, &done_on, [&](int64_t* r) -> int {
-    RET(fetch_inputs(ctx, dv, xd ? xd : hs, xb));
+    RET(fetch_inputs(ctx, dv, hs, xb));
     char* o = hs + in_bytes;  // results are written straight into mapped host memory
     uint32_t* dcand = cb ? reinterpret_cast<uint32_t*>(o) : nullptr;
     o += align_up(cb);
@@ -2225,27 +2342,27 @@ int hire_ffn_host(hire_ctx ctx, hire_matrix u, hire_matrix v, hire_scorer a, con
   RET(ensure_host(&ctx->io_host, &ctx->io_host_cap, in_bytes + out_bytes, ctx->stream));
   char* dv = static_cast<char*>(ctx->io_dev);
   char* hs = static_cast<char*>(ctx->io_host);
-  // results go straight into caller buffers in pinned memory (no staging);
+  // results go straight into caller buffers in pinned memory (no staging;
+  // the graph key then holds those addresses, and the cache is bounded);
   // the input is always staged: a graph keyed on every caller input buffer
   // would be re-captured for each new buffer
-  void* xd = nullptr;
   void* od = host_alias(out_host, ob);
   void* sd = sel_host ? host_alias(sel_host, sb) : nullptr;
-  if (!xd) std::memcpy(hs, x_host, xb);
+  std::memcpy(hs, x_host, xb);
   // the output rows are written straight into mapped host memory; the unit
   // ids stay on the device (the down-projection reads them) and are stored
   // to the host by a small kernel at the end
   uint32_t* dsel = reinterpret_cast<uint32_t*>(dv + in_bytes);
   uint32_t* hsel = sd ? static_cast<uint32_t*>(sd) : reinterpret_cast<uint32_t*>(hs + in_bytes);
   float* dout = od ? static_cast<float*>(od) : reinterpret_cast<float*>(hs + in_bytes + align_up(sb));
-  const std::vector<int64_t> key = {2, reinterpret_cast<int64_t>(u), reinterpret_cast<int64_t>(v), reinterpret_cast<int64_t>(a),
-                                    B, p->k, p->k_prime, p->group_size, p->phi, p->x_mode, p->strict,
-                                    reinterpret_cast<int64_t>(xd), reinterpret_cast<int64_t>(od),
+  const std::vector<int64_t> key = {2, static_cast<int64_t>(u->uid), static_cast<int64_t>(v->uid),
+                                    static_cast<int64_t>(a->uid), B, p->k, p->k_prime, p->group_size, p->phi,
+                                    p->x_mode, p->strict, reinterpret_cast<int64_t>(od),
                                     reinterpret_cast<int64_t>(sd), sel_host ? 1 : 0};
   int64_t res[4];
   cudaStream_t done_on = nullptr;
   RET(run_host_graph(ctx, key, res, &done_on, [&](int64_t*) -> int {
-    RET(fetch_inputs(ctx, dv, xd ? xd : hs, xb));
+    RET(fetch_inputs(ctx, dv, hs, xb));
     RET(hire_ffn_run(ctx, u, v, a, reinterpret_cast<const float*>(dv), B, p, dsel, dout));
     if (sel_host) {
       if (sb % 16 == 0) {
@@ -2435,6 +2552,63 @@ int64_t da_total_k(const hire_topk_params* p, int64_t total_rows, int world, int
 }
 }  // namespace
 
+namespace {
+// Checks shared by the DA-TOP-k entry points: this rank's shard against the
+// width rule (distributed.hpp:53-57) and its quotas; fills the plan.
+int da_prepare(const hire_matrix_s* w, const hire_scorer_s* a, int64_t total_rows, int world, int rank,
+               int64_t B, const hire_topk_params* p, int merge, int uneven, int64_t* first, DaPlan* dp) {
+  if (!p) return invalid("null argument");
+  if (world < 1 || rank < 0 || rank >= world) return invalid("da_topk: bad world/rank");
+  if (merge != HIRE_MERGE_PER_SHARD && merge != HIRE_MERGE_GLOBAL) return invalid("da_topk: unknown merge mode");
+  hire_topk_params lp = *p;
+  lp.k = std::max<int64_t>(1, quota(p->k, world, rank));
+  lp.k_prime = std::max(lp.k, quota(p->k_prime, world, rank));
+  RET(validate_topk(w, a, B, &lp));
+  int64_t width;
+  part_range(total_rows, world, rank, first, &width);
+  if (w->rows != width) return invalid("da_topk: shard has " + std::to_string(w->rows) + " rows, width rule says " + std::to_string(width));
+  return plan_da(p, width, world, rank, merge, uneven, dp);
+}
+
+int da_merge(hire_ctx ctx, const uint64_t* gathered, int64_t slots, int64_t total_rows, int world, int64_t B,
+             const hire_topk_params* p, int merge, int uneven, uint32_t* top_idx, float* top_val, int64_t* n_top,
+             int* clamped) {
+  bool cl = false;
+  const int64_t K = da_total_k(p, total_rows, world, merge, uneven, &cl);
+  RET(run_final(ctx, nullptr, 0, nullptr, 0, gathered, slots, B * slots, world * slots, K, B, 0, top_idx, top_val,
+                nullptr, nullptr, p->k));
+  if (n_top) *n_top = K;
+  if (clamped) *clamped = cl;
+  return HIRE_OK;
+}
+}  // namespace
+
+int hire_da_topk_slots(const hire_topk_params* p, int world, int merge, int64_t* slots) {
+  if (!p || !slots) return invalid("null argument");
+  if (world < 1) return invalid("da_topk: no shards");
+  *slots = merge == HIRE_MERGE_PER_SHARD ? ceil_div(p->k, world) : ceil_div(p->k_prime, world);
+  return HIRE_OK;
+}
+
+int hire_da_topk_local(hire_ctx ctx, hire_matrix w, hire_scorer a, int64_t total_rows, int world, int rank,
+                       const float* x, int64_t B, const hire_topk_params* p, int merge, int uneven, uint64_t* send) {
+  if (!ctx || !x || !send) return invalid("null argument");
+  int64_t first = 0;
+  DaPlan dp;
+  RET(da_prepare(w, a, total_rows, world, rank, B, p, merge, uneven, &first, &dp));
+  return da_local(ctx, w, a, first, x, B, p, dp, merge, send);
+}
+
+int hire_da_topk_merge(hire_ctx ctx, const uint64_t* gathered, int64_t total_rows, int world, int64_t B,
+                       const hire_topk_params* p, int merge, int uneven, uint32_t* top_idx, float* top_val,
+                       int64_t* n_top, int* clamped) {
+  if (!ctx || !gathered || !top_idx || !top_val || !p) return invalid("null argument");
+  if (world < 1 || B < 1) return invalid("da_topk: bad world or batch");
+  int64_t slots = 0;
+  RET(hire_da_topk_slots(p, world, merge, &slots));
+  return da_merge(ctx, gathered, slots, total_rows, world, B, p, merge, uneven, top_idx, top_val, n_top, clamped);
+}
+
 int hire_da_topk_run(hire_ctx ctx, hire_comm comm, hire_matrix w, hire_scorer a, int64_t total_rows,
                      int world, int rank, const float* x, int64_t B, const hire_topk_params* p,
                      int merge, int uneven, uint32_t* top_idx, float* top_val, int64_t* n_top,
@@ -2442,40 +2616,28 @@ int hire_da_topk_run(hire_ctx ctx, hire_comm comm, hire_matrix w, hire_scorer a,
   if (!ctx || !x || !top_idx || !top_val) return invalid("null argument");
   if (comm && (comm->world != world || comm->rank != rank)) return invalid("communicator does not match world/rank");
   if (!comm && world != 1) return invalid("da_topk: world > 1 needs a communicator");
-  hire_topk_params lp = *p;
-  lp.k = std::max<int64_t>(1, quota(p->k, world, rank));
-  lp.k_prime = std::max(lp.k, quota(p->k_prime, world, rank));
-  RET(validate_topk(w, a, B, &lp));
-  int64_t first, width;
-  part_range(total_rows, world, rank, &first, &width);
-  if (w->rows != width) return invalid("da_topk: shard has " + std::to_string(w->rows) + " rows, width rule says " + std::to_string(width));
+  int64_t first = 0;
   DaPlan dp;
-  RET(plan_da(p, width, world, rank, merge, uneven, &dp));
-  if (world == 1 && !std::getenv("HIRE_DA_SINGLE_GENERIC")) {
-    // one shard: DA-TOP-k is hire_topk itself (distributed.hpp:94-131 with
-    // s = 1; the reference's s = 1 equivalence, test_distributed.cpp:104-117)
-    // — no key hand-off and no second final selection
+  RET(da_prepare(w, a, total_rows, world, rank, B, p, merge, uneven, &first, &dp));
+  if (!comm) {
+    // one shard, no communicator: DA-TOP-k is hire_topk itself
+    // (distributed.hpp:94-131 with s = 1; the reference's s = 1 equivalence,
+    // test_distributed.cpp:104-117) — no key hand-off, no second selection
     int64_t nc = 0;
     return hire_topk_run(ctx, w, a, x, B, p, nullptr, top_idx, top_val, nullptr, &nc, n_top, clamped);
   }
-  // send/recv keys live in io_dev (separate from the per-stage workspace)
+  // local stage -> one ncclAllGather of B x slots rank keys -> merge
   const size_t sendb = align_up(static_cast<size_t>(B * dp.kq_max) * 8);
   const size_t recvb = align_up(static_cast<size_t>(world * B * dp.kq_max) * 8);
   RET(ensure(&ctx->io_dev, &ctx->io_dev_cap, sendb + recvb, ctx->stream));
   uint64_t* send = static_cast<uint64_t*>(ctx->io_dev);
   uint64_t* recv = reinterpret_cast<uint64_t*>(static_cast<char*>(ctx->io_dev) + sendb);
-  RET(da_local(ctx, w, a, first, x, B, p, dp, merge, world == 1 ? recv : send));
-  if (world > 1) {
+  RET(da_local(ctx, w, a, first, x, B, p, dp, merge, send));
+  {
     StageScope scope(ctx, kStageComm);
     CKN(ncclAllGather(send, recv, static_cast<size_t>(B * dp.kq_max), ncclUint64, comm->comm, ctx->stream));
   }
-  bool cl = false;
-  const int64_t K = da_total_k(p, total_rows, world, merge, uneven, &cl);
-  RET(run_final(ctx, nullptr, 0, nullptr, 0, recv, dp.kq_max, B * dp.kq_max, world * dp.kq_max, K, B,
-                0, top_idx, top_val, nullptr, nullptr, p->k));
-  if (n_top) *n_top = K;
-  if (clamped) *clamped = cl;
-  return HIRE_OK;
+  return da_merge(ctx, recv, dp.kq_max, total_rows, world, B, p, merge, uneven, top_idx, top_val, n_top, clamped);
 }
 
 int hire_da_topk_emulated(hire_ctx ctx, hire_matrix w, hire_scorer a, int world, const float* x,
@@ -2495,6 +2657,10 @@ int hire_da_topk_emulated(hire_ctx ctx, hire_matrix w, hire_scorer a, int world,
   const size_t recvb = align_up(static_cast<size_t>(world * B * kq_max) * 8);
   RET(ensure(&ctx->io_dev, &ctx->io_dev_cap, recvb, ctx->stream));
   uint64_t* recv = static_cast<uint64_t*>(ctx->io_dev);
+  // shard slices share the parent's tensor-core layouts (built here once)
+  if (a->kind == HIRE_SCORER_Q4 && p->x_mode == HIRE_X_INT8 && !p->strict && umma_min_batch() > 0 &&
+      B >= umma_min_batch() && umma_shape_ok(a, std::min<int64_t>(B, 64)))
+    RET(ensure_umma_layout(ctx, a));
   for (int r = 0; r < world; ++r) {
     int64_t f, wd;
     part_range(w->rows, world, r, &f, &wd);
@@ -2507,13 +2673,7 @@ int hire_da_topk_emulated(hire_ctx ctx, hire_matrix w, hire_scorer a, int world,
     hire_scorer_destroy(as);
     RET(rc);
   }
-  bool cl = false;
-  const int64_t K = da_total_k(p, w->rows, world, merge, uneven, &cl);
-  RET(run_final(ctx, nullptr, 0, nullptr, 0, recv, kq_max, B * kq_max, world * kq_max, K, B, 0, top_idx,
-                top_val, nullptr, nullptr, p->k));
-  if (n_top) *n_top = K;
-  if (clamped) *clamped = cl;
-  return HIRE_OK;
+  return da_merge(ctx, recv, kq_max, w->rows, world, B, p, merge, uneven, top_idx, top_val, n_top, clamped);
 }
 
 // DA FFN ------------------------------------------------------------------
@@ -2542,18 +2702,21 @@ int plan_da_ffn(const hire_ffn_params* p, int64_t total_units, int64_t width_gro
   return plan_select(width_groups, fp->kpl, HIRE_SELECT_EXACT, 0, 0, &fp->sp);
 }
 
-__global__ void concat_sel_kernel(const uint32_t* recv, int world, int64_t B, int64_t kg_max,
-                                  const int64_t* counts, int64_t kg, uint32_t* sel) {
+// Union of the per-rank selections (distributed.hpp:196-201): rank r
+// contributed min(quota(kg, s, r), width_r) ascending shard-local group ids
+// (already global); the rank-major concatenation is globally ascending.
+__global__ void concat_sel_kernel(const uint32_t* recv, int world, int64_t B, int64_t kg_max, int64_t ng,
+                                  int64_t kg, int64_t total, uint32_t* sel) {
   hire_dev::griddep_wait();
   hire_dev::griddep_launch();
-  // counts[r] valid entries per rank (same for every query); rank-major
-  // concatenation of ascending shard-local lists is globally ascending.
   const int64_t b = blockIdx.x;
   int64_t pos = 0;
   for (int r = 0; r < world; ++r) {
-    const int64_t c = counts[r];
+    const int64_t width = ng / world + (r < ng % world ? 1 : 0);
+    const int64_t q = kg / world + (r < kg % world ? 1 : 0);
+    const int64_t c = q < width ? q : width;
     for (int64_t i = threadIdx.x; i < c; i += blockDim.x)
-      sel[b * kg + pos + i] = recv[(r * B + b) * kg_max + i];
+      sel[b * total + pos + i] = recv[(r * B + b) * kg_max + i];
     pos += c;
   }
 }
@@ -2586,6 +2749,8 @@ int da_ffn_local(hire_ctx ctx, const hire_matrix_s* u, const hire_matrix_s* v, c
   return HIRE_OK;
 }
 
+// out = sum over ranks of the partial outputs, added in rank order
+// (deterministic: the same bits whatever the collective topology)
 __global__ void sum_parts_kernel(const float* parts, int world, int64_t n, float* out) {
   hire_dev::griddep_wait();
   hire_dev::griddep_launch();
@@ -2595,55 +2760,115 @@ __global__ void sum_parts_kernel(const float* parts, int world, int64_t n, float
   for (int r = 0; r < world; ++r) s = __fadd_rn(s, parts[r * n + i]);
   out[i] = s;
 }
-}  // namespace
 
-int hire_da_ffn_run(hire_ctx ctx, hire_comm comm, hire_matrix u, hire_matrix v, hire_scorer a,
-                    int64_t total_units, int world, int rank, const float* x, int64_t B,
-                    const hire_ffn_params* p, int uneven, uint32_t* sel, float* out) {
-  if (!ctx || !u || !v || !a || !p || !x || !sel || !out) return invalid("null argument");
-  if (comm && (comm->world != world || comm->rank != rank)) return invalid("communicator does not match world/rank");
-  if (!comm && world != 1) return invalid("da_group_sparse: world > 1 needs a communicator");
-  const int64_t g = p->group_size;
-  if (g < 1 || total_units % g != 0) return invalid("GroupedFFN: g must divide m");
-  const int64_t ng = total_units / g;
-  int64_t fg, wg;
-  part_range(ng, world, rank, &fg, &wg);
-  if (u->rows != wg * g) return invalid("da_group_sparse: shard unit count does not match the width rule");
-  DaFfnPlan fp;
-  RET(plan_da_ffn(p, total_units, wg, world, rank, uneven, &fp));
-  hire_ffn_params lp = *p;
-  lp.k = std::max<int64_t>(1, fp.kgl) * g;
-  lp.k_prime = std::max<int64_t>(lp.k, fp.kpl * g);
-  if (fp.kgl > 0) RET(validate_ffn(u, v, a, B, &lp));
-  const int64_t kg = p->k / g;
-  const size_t sendb = align_up(static_cast<size_t>(B * fp.kg_max) * 4);
-  const size_t recvb = align_up(static_cast<size_t>(world * B * fp.kg_max) * 4);
-  const size_t cntb = align_up(static_cast<size_t>(world) * 8);
-  RET(ensure(&ctx->io_dev, &ctx->io_dev_cap, sendb + recvb + cntb, ctx->stream));
-  uint32_t* send = static_cast<uint32_t*>(ctx->io_dev);
-  uint32_t* recv = reinterpret_cast<uint32_t*>(static_cast<char*>(ctx->io_dev) + sendb);
-  int64_t* cnt = reinterpret_cast<int64_t*>(static_cast<char*>(ctx->io_dev) + sendb + recvb);
-  RET(da_ffn_local(ctx, u, v, a, fg, x, B, p, fp, world == 1 ? recv : send, fp.kg_max, out));
-  if (world > 1) {
-    StageScope scope(ctx, kStageComm);
-    CKN(ncclGroupStart());
-    CKN(ncclAllGather(send, recv, static_cast<size_t>(B * fp.kg_max), ncclUint32, comm->comm, ctx->stream));
-    CKN(ncclAllReduce(out, out, static_cast<size_t>(B * u->d), ncclFloat32, ncclSum, comm->comm, ctx->stream));
-    CKN(ncclGroupEnd());
-  }
-  std::vector<int64_t> counts(world);
+int64_t da_ffn_total(int64_t ng, int64_t kg, int world) {
   int64_t total = 0;
   for (int r = 0; r < world; ++r) {
     int64_t f2, w2;
     part_range(ng, world, r, &f2, &w2);
-    counts[r] = std::min(quota(kg, world, r), w2);
-    total += counts[r];
+    total += std::min(quota(kg, world, r), w2);
   }
-  CK(cudaMemcpyAsync(cnt, counts.data(), world * 8, cudaMemcpyHostToDevice, ctx->stream));
-  CK(launch_k(ctx, concat_sel_kernel, static_cast<unsigned>(B), 128, 0, recv, world, B, fp.kg_max, cnt, total, sel));
-  CK(cudaGetLastError());
-  CK(cudaStreamSynchronize(ctx->stream));  // counts is a pageable host vector
+  return total;
+}
+
+int da_ffn_prepare(const hire_matrix_s* u, const hire_matrix_s* v, const hire_scorer_s* a, int64_t total_units,
+                   int world, int rank, int64_t B, const hire_ffn_params* p, int uneven, int64_t* first_group,
+                   DaFfnPlan* fp) {
+  if (!u || !v || !a || !p) return invalid("null argument");
+  if (world < 1 || rank < 0 || rank >= world) return invalid("da_group_sparse: bad world/rank");
+  const int64_t g = p->group_size;
+  if (g < 1 || total_units % g != 0) return invalid("GroupedFFN: g must divide m");
+  const int64_t ng = total_units / g;
+  int64_t wg;
+  part_range(ng, world, rank, first_group, &wg);
+  if (u->rows != wg * g) return invalid("da_group_sparse: shard unit count does not match the width rule");
+  RET(plan_da_ffn(p, total_units, wg, world, rank, uneven, fp));
+  hire_ffn_params lp = *p;
+  lp.k = std::max<int64_t>(1, fp->kgl) * g;
+  lp.k_prime = std::max<int64_t>(lp.k, fp->kpl * g);
+  if (fp->kgl > 0) RET(validate_ffn(u, v, a, B, &lp));
   return HIRE_OK;
+}
+
+int da_ffn_merge(hire_ctx ctx, const uint32_t* gsel, int64_t kg_max, const float* parts, int64_t d,
+                 int64_t total_units, int world, int64_t B, const hire_ffn_params* p, uint32_t* sel, float* out) {
+  const int64_t g = p->group_size, ng = total_units / g, kg = p->k / g;
+  const int64_t total = da_ffn_total(ng, kg, world);
+  CK(launch_k(ctx, concat_sel_kernel, static_cast<unsigned>(B), 128, 0, gsel, world, B, kg_max, ng, kg, total, sel));
+  CK(cudaGetLastError());
+  if (parts) {
+    CK(launch_k(ctx, sum_parts_kernel, static_cast<unsigned>(ceil_div(B * d, 256)), 256, 0, parts, world, B * d, out));
+    CK(cudaGetLastError());
+  }
+  return HIRE_OK;
+}
+}  // namespace
+
+int hire_da_ffn_slots(const hire_ffn_params* p, int world, int64_t* slots) {
+  if (!p || !slots) return invalid("null argument");
+  if (world < 1 || p->group_size < 1) return invalid("da_group_sparse: bad world or group size");
+  *slots = ceil_div(p->k / p->group_size, world);
+  return HIRE_OK;
+}
+
+int hire_da_ffn_local(hire_ctx ctx, hire_matrix u, hire_matrix v, hire_scorer a, int64_t total_units, int world,
+                      int rank, const float* x, int64_t B, const hire_ffn_params* p, int uneven, uint32_t* sel_send,
+                      float* partial) {
+  if (!ctx || !x || !sel_send || !partial) return invalid("null argument");
+  int64_t fg = 0;
+  DaFfnPlan fp;
+  RET(da_ffn_prepare(u, v, a, total_units, world, rank, B, p, uneven, &fg, &fp));
+  return da_ffn_local(ctx, u, v, a, fg, x, B, p, fp, sel_send, fp.kg_max, partial);
+}
+
+int hire_da_ffn_merge(hire_ctx ctx, const uint32_t* gathered_sel, const float* gathered_parts, int64_t total_units,
+                      int64_t d, int world, int64_t B, const hire_ffn_params* p, int uneven, uint32_t* sel,
+                      float* out) {
+  if (!ctx || !gathered_sel || !gathered_parts || !sel || !out || !p) return invalid("null argument");
+  if (world < 1 || B < 1 || d < 1) return invalid("da_group_sparse: bad world, batch or d");
+  if (p->group_size < 1 || total_units % p->group_size != 0) return invalid("GroupedFFN: g must divide m");
+  (void)uneven;
+  int64_t slots = 0;
+  RET(hire_da_ffn_slots(p, world, &slots));
+  return da_ffn_merge(ctx, gathered_sel, slots, gathered_parts, d, total_units, world, B, p, sel, out);
+}
+
+int hire_da_ffn_run(hire_ctx ctx, hire_comm comm, hire_matrix u, hire_matrix v, hire_scorer a,
+                    int64_t total_units, int world, int rank, const float* x, int64_t B,
+                    const hire_ffn_params* p, int uneven, uint32_t* sel, float* out) {
+  if (!ctx || !x || !sel || !out) return invalid("null argument");
+  if (comm && (comm->world != world || comm->rank != rank)) return invalid("communicator does not match world/rank");
+  if (!comm && world != 1) return invalid("da_group_sparse: world > 1 needs a communicator");
+  int64_t fg = 0;
+  DaFfnPlan fp;
+  RET(da_ffn_prepare(u, v, a, total_units, world, rank, B, p, uneven, &fg, &fp));
+  const int64_t d = u->d;
+  // send: [B][kg_max] ids + [B][d] partial; recv: [world][B][kg_max] + [world][B][d]
+  const size_t sselb = align_up(static_cast<size_t>(B * fp.kg_max) * 4);
+  const size_t spartb = align_up(static_cast<size_t>(B * d) * 4);
+  const size_t rselb = align_up(static_cast<size_t>(world * B * fp.kg_max) * 4);
+  const size_t rpartb = align_up(static_cast<size_t>(world * B * d) * 4);
+  RET(ensure(&ctx->io_dev, &ctx->io_dev_cap, sselb + spartb + rselb + rpartb, ctx->stream));
+  char* base = static_cast<char*>(ctx->io_dev);
+  uint32_t* ssel = reinterpret_cast<uint32_t*>(base);
+  float* spart = reinterpret_cast<float*>(base + sselb);
+  uint32_t* rsel = reinterpret_cast<uint32_t*>(base + sselb + spartb);
+  float* rpart = reinterpret_cast<float*>(base + sselb + spartb + rselb);
+  RET(da_ffn_local(ctx, u, v, a, fg, x, B, p, fp, comm ? ssel : rsel, fp.kg_max, comm ? spart : out));
+  if (!comm) {  // one shard: the partial is the output
+    return da_ffn_merge(ctx, rsel, fp.kg_max, nullptr, d, total_units, 1, B, p, sel, out);
+  }
+  {
+    // the partial outputs are all-gathered and summed in rank order, not
+    // all-reduced: NCCL's reduction order depends on the topology, the
+    // rank-order sum gives the same bits on every rank and every machine
+    StageScope scope(ctx, kStageComm);
+    CKN(ncclGroupStart());
+    CKN(ncclAllGather(ssel, rsel, static_cast<size_t>(B * fp.kg_max), ncclUint32, comm->comm, ctx->stream));
+    CKN(ncclAllGather(spart, rpart, static_cast<size_t>(B * d), ncclFloat32, comm->comm, ctx->stream));
+    CKN(ncclGroupEnd());
+  }
+  return da_ffn_merge(ctx, rsel, fp.kg_max, rpart, d, total_units, world, B, p, sel, out);
 }
 
 int hire_da_ffn_emulated(hire_ctx ctx, hire_matrix u, hire_matrix v, hire_scorer a, int world,
@@ -2661,13 +2886,9 @@ int hire_da_ffn_emulated(hire_ctx ctx, hire_matrix u, hire_matrix v, hire_scorer
   const int64_t kg_max = plans[0].kg_max;
   const size_t recvb = align_up(static_cast<size_t>(world * B * kg_max) * 4);
   const size_t partb = align_up(static_cast<size_t>(world * B * u->d) * 4);
-  const size_t cntb = align_up(static_cast<size_t>(world) * 8);
-  RET(ensure(&ctx->io_dev, &ctx->io_dev_cap, recvb + partb + cntb, ctx->stream));
+  RET(ensure(&ctx->io_dev, &ctx->io_dev_cap, recvb + partb, ctx->stream));
   uint32_t* recv = static_cast<uint32_t*>(ctx->io_dev);
   float* parts = reinterpret_cast<float*>(static_cast<char*>(ctx->io_dev) + recvb);
-  int64_t* cnt = reinterpret_cast<int64_t*>(static_cast<char*>(ctx->io_dev) + recvb + partb);
-  std::vector<int64_t> counts(world);
-  int64_t total = 0;
   for (int r = 0; r < world; ++r) {
     int64_t fgr, wg;
     part_range(ng, world, r, &fgr, &wg);
@@ -2683,14 +2904,12 @@ int hire_da_ffn_emulated(hire_ctx ctx, hire_matrix u, hire_matrix v, hire_scorer
     hire_matrix_destroy(vs);
     hire_scorer_destroy(as);
     RET(rc);
-    counts[r] = std::min(quota(kg, world, r), wg);
-    total += counts[r];
   }
-  CK(cudaMemcpyAsync(cnt, counts.data(), world * 8, cudaMemcpyHostToDevice, ctx->stream));
-  CK(launch_k(ctx, concat_sel_kernel, static_cast<unsigned>(B), 128, 0, recv, world, B, kg_max, cnt, total, sel));
-  CK(cudaGetLastError());
+  const int64_t total = da_ffn_total(ng, kg, world);
   if (p->strict) {
     // the reference's own order: one ascending sum over the union
+    // (distributed.hpp:203-204 -> ffn_apply_groups, ffn.hpp:160-169)
+    RET(da_ffn_merge(ctx, recv, kg_max, nullptr, u->d, u->rows, world, B, p, sel, out));
     Arena ar;
     uint32_t* units;
     float* act;
@@ -2701,10 +2920,9 @@ int hire_da_ffn_emulated(hire_ctx ctx, hire_matrix u, hire_matrix v, hire_scorer
     RET(run_recompute(ctx, u, units, total * g, total * g, x, B, p->phi, 1, act, total * g));
     RET(run_down(ctx, v, units, act, total * g, total * g, B, 1, nullptr, out));
   } else {
-    CK(launch_k(ctx, sum_parts_kernel, static_cast<unsigned>(ceil_div(B * u->d, 256)), 256, 0, parts, world, B * u->d, out));
-    CK(cudaGetLastError());
+    // what hire_da_ffn_run computes across ranks: rank-order sum of the partials
+    RET(da_ffn_merge(ctx, recv, kg_max, parts, u->d, u->rows, world, B, p, sel, out));
   }
-  CK(cudaStreamSynchronize(ctx->stream));
   return HIRE_OK;
 }
 

@@ -23,17 +23,25 @@ namespace hire_dev {
 // Integer mode, step 0: quantise each query x[b] to int8 with the
 // quantize_int4 rule widened to [-127,127] (approx.hpp:41-65):
 //   sx = max|x| / 127 (1 if x == 0), xq_i = RHAZ(x_i / sx).
-// Writes xq (natural order), xperm (dp4a order, see q4_score_fast_int8),
-// sx and sum(xq). One CTA per query.
+// Writes xq (natural order), xperm (xg_mode 0: dp4a order, see
+// q4_score_fast_int8; xg_mode 1: the tcgen05 proxy's B-operand layout,
+// xg_offset in score_umma.cuh, with CTAs b >= n_real writing the zero
+// padding queries), sx and sum(xq). One CTA per query.
 // ---------------------------------------------------------------------
 __global__ void __launch_bounds__(256) prep_x_int8_kernel(
     const float* __restrict__ x, int d, int8_t* __restrict__ xq,
     int8_t* __restrict__ xperm, float* __restrict__ sx_out,
-    int* __restrict__ sumxq_out) {
+    int* __restrict__ sumxq_out, int xg_mode, int n_real) {
   hire_dev::griddep_wait();
   hire_dev::griddep_launch();
   KTrace kt_(kKtPrep);
   const int b = blockIdx.x;
+  if (b >= n_real) {  // padding query of the grouped layout (xg_mode 1)
+    for (int i = threadIdx.x * 16; i < d; i += blockDim.x * 16)
+      *reinterpret_cast<int4*>(xperm + (static_cast<int64_t>(b) >> 3) * 8 * d + (i >> 4) * 128 + (b & 7) * 16) =
+          make_int4(0, 0, 0, 0);
+    return;
+  }
   const float* xb = x + static_cast<int64_t>(b) * d;
   __shared__ float s_red[8];
   __shared__ int s_sum[8];
@@ -69,19 +77,27 @@ __global__ void __launch_bounds__(256) prep_x_int8_kernel(
     const int q = rhaz_clamp(__fdiv_rn(xr[r], sx), 127);
     local += q;
     xq[static_cast<int64_t>(b) * d + i] = static_cast<int8_t>(q);
-    const int g = i & ~7, j = i & 7;
-    const int pos = g + ((j & 1) ? 4 : 0) + (j >> 1);
-    xperm[static_cast<int64_t>(b) * d + pos] = static_cast<int8_t>(q);
+    if (xg_mode) {
+      xperm[(static_cast<int64_t>(b) >> 3) * 8 * d + (i >> 4) * 128 + (b & 7) * 16 + (i & 15)] = static_cast<int8_t>(q);
+    } else {
+      const int g = i & ~7, j = i & 7;
+      const int pos = g + ((j & 1) ? 4 : 0) + (j >> 1);
+      xperm[static_cast<int64_t>(b) * d + pos] = static_cast<int8_t>(q);
+    }
   }
   for (int i = threadIdx.x + kXR * 256; i < d; i += blockDim.x) {
     const int q = rhaz_clamp(__fdiv_rn(xb[i], sx), 127);
     local += q;
     xq[static_cast<int64_t>(b) * d + i] = static_cast<int8_t>(q);
-    // dp4a order: within each 8-element word group, the 4 even elements
-    // then the 4 odd elements (matches the lo/hi nibble extraction).
-    const int g = i & ~7, j = i & 7;
-    const int pos = g + ((j & 1) ? 4 : 0) + (j >> 1);
-    xperm[static_cast<int64_t>(b) * d + pos] = static_cast<int8_t>(q);
+    if (xg_mode) {
+      xperm[(static_cast<int64_t>(b) >> 3) * 8 * d + (i >> 4) * 128 + (b & 7) * 16 + (i & 15)] = static_cast<int8_t>(q);
+    } else {
+      // dp4a order: within each 8-element word group, the 4 even elements
+      // then the 4 odd elements (matches the lo/hi nibble extraction).
+      const int g = i & ~7, j = i & 7;
+      const int pos = g + ((j & 1) ? 4 : 0) + (j >> 1);
+      xperm[static_cast<int64_t>(b) * d + pos] = static_cast<int8_t>(q);
+    }
   }
   local = warp_sum_i32(local);
   if ((threadIdx.x & 31) == 0) s_sum[threadIdx.x >> 5] = local;

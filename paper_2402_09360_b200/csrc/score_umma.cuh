@@ -1,0 +1,286 @@
+// score_umma.cuh — K1 for batches of 9..64 queries on the 5th-generation
+// tensor cores: the int4 proxy GEMV becomes a skinny GEMM
+//   S[row][q] = sum_k code[row][k] * xq[q][k]          (exact int32)
+// with the vocab rows as the MMA's M (128 per tcgen05.mma), the queries as
+// N (16/32/48/64) and K = d. Reference op: the int4 scorer,
+// approx.hpp:395-403, in BASELINE's int8-x integer mode (DESIGN.md
+// "Semantics"): score = phi(float(S - 8 * sum(xq)) * (scale * sx)).
+//
+// Data path per CTA (persistent, one CTA per SM, rows in 128-row blocks):
+//   HBM --TMA (cp.async.bulk.tensor.2d, 16 KB stages, mbarrier ring)--> smem
+//   smem --4 converter warps: LDS.128, int4 digits -> u8 in registers,
+//          tcgen05.st--> TMEM (the A operand: lane = row, 4 codes per column)
+//   TMEM A x smem x (B operand, int8, resident) --tcgen05.mma kind::i8,
+//          one elected thread--> TMEM accumulators (s32, 2 buffers)
+//   TMEM --tcgen05.ld, epilogue (scale, phi)--> scores [B][rows]
+// The int4 codes are stored in a tensor-core layout built once per scorer
+// (q4_to_umma_layout): [row block][k chunk of 32][row 128][16 B], byte
+// 4j+b = (code[8j+b] + 8) | (code[8j+4+b] + 8) << 4, so the two nibble masks
+// of one 32-bit word give 8 consecutive k in natural order (unsigned digits
+// c + 8; the 8 * sum(xq) correction makes the sum exact).
+#pragma once
+#include <cuda.h>
+#include <cstdint>
+
+#include "common.cuh"
+#include "umma.cuh"
+
+namespace hire_dev {
+
+constexpr int kUmmaRows = 128;         // rows per MMA / per row block
+constexpr int kUmmaStageChunks = 8;    // k chunks (32 codes each) per pipeline stage
+constexpr int kUmmaStageBytes = kUmmaStageChunks * kUmmaRows * 16;  // 16 KB
+constexpr int kUmmaStages = 4;         // smem ring depth
+constexpr int kUmmaThreads = 192;      // warps 0-3 convert + epilogue, 4 TMA, 5 MMA
+
+// canonical [rows][pitch] (low nibble = even column) -> UMMA layout words
+__global__ void q4_to_umma_layout(const uint8_t* __restrict__ wq, int64_t pitch, int64_t rows, int d,
+                                  uint32_t* __restrict__ out, int64_t n_words) {
+  hire_dev::griddep_wait();  // no early trigger: consumers prefetch this layout before their wait
+  const int64_t id = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (id >= n_words) return;
+  const int nkc = d / 32;
+  const int j = static_cast<int>(id & 3);
+  const int r = static_cast<int>((id >> 2) & 127);
+  const int64_t blk = id >> 9;  // (row block, k chunk)
+  const int64_t rb = blk / nkc, kc = blk % nkc;
+  const int64_t row = rb * kUmmaRows + r;
+  uint32_t word = 0x88888888u;  // padding rows: code 0
+  if (row < rows) {
+    word = 0;
+#pragma unroll
+    for (int b = 0; b < 4; ++b)
+#pragma unroll
+      for (int hi = 0; hi < 2; ++hi) {
+        const int64_t col = kc * 32 + 8 * j + 4 * hi + b;
+        const uint8_t byte = wq[row * pitch + col / 2];
+        const uint32_t nib = ((col & 1) ? (byte >> 4) : (byte & 0xF)) ^ 0x8u;  // code + 8
+        word |= nib << (8 * b + 4 * hi);
+      }
+  }
+  out[id] = word;
+}
+
+constexpr int kUmmaMaxStages = 12;
+
+// shared memory: ring of int4 stages, the x operand, barriers
+struct UmmaSmem {
+  static __host__ __device__ size_t x_off(int stages) { return static_cast<size_t>(stages) * kUmmaStageBytes; }
+  static __host__ __device__ size_t bar_off(int stages, int nq, int d) {
+    return x_off(stages) + static_cast<size_t>(nq) * d;
+  }
+  static __host__ __device__ size_t bytes(int stages, int nq, int d) {
+    return bar_off(stages, nq, d) + (2 * kUmmaMaxStages + 9) * 8 + 16;
+  }
+  // deepest ring that fits next to an x operand of nq queries
+  static __host__ int stages_for(int nq, int d, size_t smem_max) {
+    int st = kUmmaMaxStages;
+    while (st > 2 && bytes(st, nq, d) > smem_max) --st;
+    return st;
+  }
+};
+
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::
+          "r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void tma_prefetch_desc(const CUtensorMap* map) {
+  asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
+}
+
+// x operand in global memory, written by prep_x_int8_kernel (mode 1) in the
+// MMA's B layout so one bulk copy stages it: queries in groups of 8, each
+// group a [d/16][8 queries][16 B] block (8-row x 16-byte core matrices),
+// offset(n, k) = (n/8)*8d + (k/16)*128 + (n%8)*16 + k%16; padding queries 0.
+__host__ __device__ __forceinline__ int64_t xg_offset(int64_t n, int64_t k, int64_t d) {
+  return (n >> 3) * 8 * d + (k >> 4) * 128 + (n & 7) * 16 + (k & 15);
+}
+
+// nq: MMA N = queries rounded up to 16 (<= 64); nb <= nq real queries.
+// Tensor map: 2-D u64 view [n_rb * nkc][256] of the UMMA layout (one k chunk
+// of a row block = 256 x 8 B = 2 KB), box {256, kUmmaStageChunks}.
+__global__ void __launch_bounds__(kUmmaThreads, 1) q4_score_umma(
+    const __grid_constant__ CUtensorMap wmap, int64_t rows, int d, const float* __restrict__ scales,
+    const int8_t* __restrict__ xg, const float* __restrict__ sx, const int* __restrict__ sumxq, int nb, int nq,
+    int stages, int phi, float* __restrict__ scores, int64_t score_stride) {
+  extern __shared__ __align__(1024) unsigned char smem[];
+  uint8_t* ring = smem;
+  uint8_t* s_x = smem + UmmaSmem::x_off(stages);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + UmmaSmem::bar_off(stages, nq, d));
+  uint64_t* full = bars;                          // [stages] TMA -> converters
+  uint64_t* empty = bars + kUmmaMaxStages;        // [stages] converters -> TMA (128 arrivals)
+  uint64_t* afull = bars + 2 * kUmmaMaxStages;    // [2] converters -> MMA (128 arrivals)
+  uint64_t* aempty = afull + 2;                   // [2] MMA commit -> converters
+  uint64_t* dfull = afull + 4;                    // [2] MMA commit -> epilogue
+  uint64_t* dempty = afull + 6;                   // [2] epilogue -> MMA (128 arrivals)
+  uint64_t* xbar = afull + 8;                     // x operand bulk copy
+  uint32_t* s_tmem = reinterpret_cast<uint32_t*>(xbar + 1);
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int nkc = d / 32, n_st = nkc / kUmmaStageChunks;
+  const int64_t n_rb = (rows + kUmmaRows - 1) / kUmmaRows;
+  constexpr uint32_t kTmemCols = 256;  // A: 2 x 64 columns, D: 2 x nq columns
+  constexpr uint32_t kColA = 0, kColD = 128;
+
+  if (tid == 0) {
+    for (int s = 0; s < stages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 128);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&afull[i], 128);
+      mbar_init(&aempty[i], 1);
+      mbar_init(&dfull[i], 1);
+      mbar_init(&dempty[i], 128);
+    }
+    mbar_init(xbar, 1);
+    fence_mbar_init();
+  }
+  if (warp == 4 && lane == 0) tma_prefetch_desc(&wmap);
+  if (warp == 5) {
+    umma::tmem_alloc(s_tmem, kTmemCols);
+    umma::tmem_relinquish();
+  }
+  umma::fence_before();
+  __syncthreads();
+  umma::fence_after();
+  const uint32_t tmem = *s_tmem;
+
+  if (warp == 4) {
+    // ===== TMA producer: weights are read-only, so it streams before the
+    // programmatic-dependency wait (independent prologue)
+    if (lane == 0) {
+      int it = 0;
+      for (int64_t rb = blockIdx.x; rb < n_rb; rb += gridDim.x)
+        for (int st = 0; st < n_st; ++st, ++it) {
+          const int slot = it % stages;
+          if (it >= stages) mbar_wait(&empty[slot], ((it / stages) - 1) & 1);
+          mbar_arrive_expect_tx(&full[slot], kUmmaStageBytes);
+          tma_load_2d(ring + static_cast<size_t>(slot) * kUmmaStageBytes, &wmap, 0,
+                      static_cast<int>(rb * nkc + st * kUmmaStageChunks), &full[slot]);
+        }
+    }
+  } else if (warp == 5) {
+    // ===== MMA issuer (x operand: one bulk copy after the dependency wait)
+    if (lane == 0) {
+      griddep_wait();  // x quantisation (prep_x_int8_kernel) is complete
+      const unsigned xbytes = static_cast<unsigned>(nq) * static_cast<unsigned>(d);
+      mbar_arrive_expect_tx(xbar, xbytes);
+      bulk_g2s(s_x, xg, xbytes, xbar);
+      const uint32_t idesc = umma::idesc_i8(kUmmaRows, nq, /*a_signed=*/false, /*b_signed=*/true);
+      const uint32_t xbase = smem_u32(s_x);
+      mbar_wait(xbar, 0);
+      int ait = 0, rbi = 0;
+      for (int64_t rb = blockIdx.x; rb < n_rb; rb += gridDim.x, ++rbi) {
+        const int db = rbi & 1;
+        if (rbi >= 2) mbar_wait(&dempty[db], ((rbi >> 1) - 1) & 1);
+        umma::fence_after();
+        const uint32_t dcol = tmem + kColD + db * nq;
+        for (int st = 0; st < n_st; ++st, ++ait) {
+          const int ab = ait & 1;
+          mbar_wait(&afull[ab], (ait >> 1) & 1);
+          umma::fence_after();
+          const uint32_t acol = tmem + kColA + ab * 64;
+#pragma unroll
+          for (int c = 0; c < kUmmaStageChunks; ++c) {
+            const int kc = st * kUmmaStageChunks + c;
+            // k chunk kc = core matrices 2kc, 2kc+1 (LBO 128 B apart); 8-query groups 8d apart
+            const uint64_t bd = umma::sdesc_kmajor_noswz(xbase + static_cast<uint32_t>(kc * 256), 128,
+                                                         static_cast<uint32_t>(8 * d));
+            umma::mma_i8_ts(dcol, acol + 8 * c, bd, idesc, (st | c) != 0);
+          }
+          umma::commit(&aempty[ab]);
+        }
+        umma::commit(&dfull[db]);
+      }
+    }
+    __syncwarp();
+  } else {
+    // ===== converters + epilogue (thread = TMEM lane = row within the block)
+    const uint32_t lane_off = static_cast<uint32_t>(32 * warp) << 16;
+    int it = 0, ait = 0, rbi = 0;
+    int64_t pend_rb = -1;  // row block whose epilogue is still to do
+    bool waited = false;
+    auto epilogue = [&](int64_t prb, int pidx) {  // row block prb, the pidx-th of this CTA
+      if (!waited) {
+        griddep_wait();  // scores / sx / sum(xq) of this call: after the producer grids
+        waited = true;
+      }
+      const int pdb = pidx & 1;
+      mbar_wait(&dfull[pdb], (pidx >> 1) & 1);
+      umma::fence_after();
+      const int64_t row = prb * kUmmaRows + 32 * warp + lane;
+      const float sc = row < rows ? scales[row] : 0.0f;
+      for (int q0 = 0; q0 < nq; q0 += 16) {
+        uint32_t acc[16];
+        umma::ld_32x32b_x16(tmem + lane_off + kColD + pdb * nq + q0, acc);
+        umma::wait_ld();
+        if (q0 + 16 >= nq) {
+          umma::fence_before();
+          umma::mbar_arrive(&dempty[pdb]);
+        }
+        if (row < rows) {
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            const int q = q0 + j;
+            if (q < nb) {
+              const int aint = static_cast<int>(acc[j]) - 8 * sumxq[q];
+              const float cs = __fmul_rn(sc, sx[q]);
+              scores[static_cast<int64_t>(q) * score_stride + row] =
+                  apply_phi(phi, __fmul_rn(static_cast<float>(aint), cs));
+            }
+          }
+        }
+      }
+    };
+    for (int64_t rb = blockIdx.x; rb < n_rb; rb += gridDim.x, ++rbi) {
+      for (int st = 0; st < n_st; ++st, ++it, ++ait) {
+        const int slot = it % stages;
+        mbar_wait(&full[slot], (it / stages) & 1);
+        const uint4* src = reinterpret_cast<const uint4*>(ring + static_cast<size_t>(slot) * kUmmaStageBytes) +
+                           (32 * warp + lane);
+        uint4 v[kUmmaStageChunks];
+#pragma unroll
+        for (int c = 0; c < kUmmaStageChunks; ++c) v[c] = src[c * kUmmaRows];
+        umma::mbar_arrive(&empty[slot]);  // the slot's bytes are in registers
+        const int ab = ait & 1;
+        if (ait >= 2) mbar_wait(&aempty[ab], ((ait >> 1) - 1) & 1);
+        umma::fence_after();
+        const uint32_t acol = tmem + lane_off + kColA + ab * 64;
+#pragma unroll
+        for (int c = 0; c < kUmmaStageChunks; ++c) {
+          const uint32_t w4[4] = {v[c].x, v[c].y, v[c].z, v[c].w};
+          uint32_t r[8];
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            r[2 * j] = w4[j] & 0x0F0F0F0Fu;
+            r[2 * j + 1] = (w4[j] >> 4) & 0x0F0F0F0Fu;
+          }
+          umma::st_32x32b_x8(acol + 8 * c, r);
+        }
+        umma::wait_st();
+        umma::fence_before();
+        umma::mbar_arrive(&afull[ab]);
+        if (st == 0 && pend_rb >= 0) {  // previous block's epilogue, off the MMA's critical path
+          epilogue(pend_rb, rbi - 1);
+          pend_rb = -1;
+        }
+      }
+      pend_rb = rb;
+    }
+    if (pend_rb >= 0) epilogue(pend_rb, rbi - 1);
+    if (!waited) griddep_wait();
+  }
+  griddep_launch();
+  umma::fence_before();
+  __syncthreads();
+  if (warp == 5) {
+    umma::fence_after();
+    umma::tmem_dealloc(tmem, kTmemCols);
+  }
+}
+
+}  // namespace hire_dev
