@@ -2,19 +2,22 @@
 """HiRE approximate top-k path on B200 — benchmark (driver contract).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                  [--workload cfg2|cfg3|cfg1|cfg4] [--batch B]
+                  [--workload cfg3|cfg2|cfg1|cfg4|cfg5] [--batch B]
 
-Default workload: BASELINE.json configs[1] (cfg2) — one HiRE-FFN layer
-(d=2048, m=8192, bf16 U/V, int4 proxy of U scored against int8-quantised x,
-k'=820, k=410, ReLU) for a batch of decode tokens. A "step" is one layer call
-over one batch. 18 distinct layers (a 1B-class decoder's FFN stack, 1.36 GB)
-are cycled so every step streams cold weights from HBM (the 75 MB of one
-layer would otherwise sit in the 126 MB L2).
+Default workload: BASELINE.json configs[2] (cfg3), the largest single-GPU
+config — HiRE-softmax over V=256000, d=2048 (bf16 W, int4 per-row proxy
+scored against int8-quantised x, exact top-k'=1024 candidates, gather
+recompute, exact top-k=64 + softmax), batch 32 (configs[2] lists 1/8/32;
+--batch picks another). A "step" is one call over one batch of decode
+queries. Working set 1.3 GB > 126 MB L2, so every step streams from HBM.
 
-One JSON line on rank 0. N > 1 (torchrun):
-every rank runs its own batch on its own GPU (weak scaling, no collective on
-the data path); timing = max over ranks of CUDA-event time. --workload cfg4
-is the sharded DA-TOP-k softmax with its NCCL all-gather.
+N > 1 (`--gpus N`, re-executed under torchrun if not already launched by
+it): DA-TOP-k strong scaling (distributed.hpp:73-134) — the same vocab and
+batch, rows split across ranks by the width rule, each rank the local
+stage on its shard, one ncclAllGather of (exact value, global index) keys,
+global merge on every rank. --workload cfg4 is BASELINE's own DA config.
+
+One JSON line on rank 0.
 """
 from __future__ import annotations
 
@@ -22,6 +25,7 @@ import argparse
 import ctypes as C
 import json
 import os
+import socket
 import statistics
 import subprocess
 import sys
@@ -34,6 +38,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0}
+METRIC = "HiRE decode tokens/s (µs/token, HBM roofline fraction, recall@k)"
 
 
 def load_peaks():
@@ -67,6 +72,17 @@ def barrier(world):
     if world > 1:
         import torch.distributed as dist
         dist.barrier()
+
+
+def relaunch_under_torchrun(n: int):
+    """--gpus N without a torchrun parent: re-exec this script as N ranks."""
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__), *sys.argv[1:]]
+    os.execvp(cmd[0], cmd)
 
 
 # ---------------------------------------------------------------- clocks ---
@@ -125,7 +141,9 @@ class ClockSampler:
                 "samples": len(sm), "window": "1 s soak of the same graph + the timed replay"}
 
 
-# -------------------------------------------------------------- workloads --
+# ------------------------------------------------- weight generators (torch) --
+# Plain torch on the device: used by both arms (the reference arm copies the
+# result to the host; it never imports this repo's package).
 def gen_ffn_layer(m, d, r, gen):
     """cfg2 family: N(0, 1/d) + 3 x a rank-r component with the same entry
     scale, bf16 (BASELINE.json configs[1])."""
@@ -137,145 +155,137 @@ def gen_ffn_layer(m, d, r, gen):
     return one(), one()
 
 
-def gen_lowrank_plus_noise(V, d, r, gen, lr_scale=1.0, noise=0.1, chunk=32768):
-    W = torch.empty(V, d, device="cuda", dtype=torch.bfloat16)
-    Bm = torch.randn(r, d, device="cuda", generator=gen)
-    A = torch.randn(V, r, device="cuda", generator=gen)
-    for s in range(0, V, chunk):
-        e = min(V, s + chunk)
-        W[s:e] = (lr_scale * (A[s:e] @ Bm) / r ** 0.5 +
-                  noise * torch.randn(e - s, d, device="cuda", generator=gen)).to(torch.bfloat16)
-    return W, A, Bm
+def gen_vocab_rows(V, d, r, first, count, seed, lr_scale=1.0, noise=0.1, blk=4096):
+    """Rows [first, first+count) of W [V, d] bf16 = lr_scale * A B / sqrt(r) +
+    noise * N(0,1) (cfg3 / cfg4 family). Generated per 4096-row block from a
+    per-block seed, so any shard of the width rule gets the same rows as the
+    whole matrix (strong scaling compares like with like)."""
+    gB = torch.Generator(device="cuda").manual_seed(seed)
+    Bm = torch.randn(r, d, device="cuda", generator=gB)
+    W = torch.empty(count, d, device="cuda", dtype=torch.bfloat16)
+    A_out = torch.empty(count, r, device="cuda")
+    for b0 in range(first // blk * blk, first + count, blk):
+        g = torch.Generator(device="cuda").manual_seed(seed * 1_000_003 + b0 // blk + 1)
+        n = min(blk, V - b0)
+        A = torch.randn(n, r, device="cuda", generator=g)
+        blkW = (lr_scale * (A @ Bm) / r ** 0.5 + noise * torch.randn(n, d, device="cuda", generator=g))
+        s, e = max(first, b0), min(first + count, b0 + n)
+        W[s - first:e - first] = blkW[s - b0:e - b0].to(torch.bfloat16)
+        A_out[s - first:e - first] = A[s - b0:e - b0]
+    return W, A_out, Bm
 
 
-class FfnWorkload:
-    name = "cfg2"
+def shard_range(l, s, i):
+    """distributed.hpp:53-57 (the same rule as parallel.shard_range)."""
+    base, extra = divmod(l, s)
+    return i * base + min(i, extra), base + (1 if i < extra else 0)
 
-    def __init__(self, H, batch, layers=18, seed=0):
-        self.H = H
-        self.m, self.d, self.kp, self.k, self.B = 8192, 2048, 820, 410, batch
-        gen = torch.Generator(device="cuda").manual_seed(seed)
-        self.layers = []
-        for _ in range(layers):
-            u, v = gen_ffn_layer(self.m, self.d, 128, gen)
-            U, Vm = H.ScoreMatrix(u), H.ScoreMatrix(v)
-            A = H.ApproxScorer.quantize(U)
-            self.layers.append((H.GroupedFFN(U, Vm, 1, "relu"), A))
-        self.gen = gen
-        torch.cuda.synchronize()
+
+# -------------------------------------------------------------- workloads --
+class Workload:
+    """Shapes + torch weights; attach(H) builds the product's handles (our
+    arm only); ref_host() returns host arrays for the reference arm."""
+    name = ""
+    lowrank = False
+    dtype = "int4 x int8 -> int32 proxy, bf16 rows, fp32 accumulation"
+    scaling = "weak"
+
+    def query_scale(self):
+        return 1.0 / np.sqrt(self.d)
 
     def inputs(self, n):
-        return torch.randn(n, self.B, self.d, device="cuda", generator=self.gen)
-
-    def step(self, i, x):
-        f, a = self.layers[i % len(self.layers)]
-        return self.H.ffn_group_sparse(f, x, a, self.k, self.kp, x_mode=self.H.X_INT8)
-
-    def host_step(self, i, x_host, sel_host, out_host, ctx):
-        H = self.H
-        f, a = self.layers[i % len(self.layers)]
-        if not hasattr(self, "_hp"):  # call parameters built once, as a serving loop would
-            self._hp = C.byref(H._lib.FfnParams(self.k, self.kp, 1, 1, H.X_INT8, 0, 0))
-        H._lib.check(H.lib().hire_ffn_host(ctx.h, f.u.h, f.v.h, a.h, x_host.ctypes.data, self.B, self._hp,
-                                           sel_host.ctypes.data, out_host.ctypes.data))
-
-    def io_bytes(self):
-        return self.B * self.d * 4, self.B * self.k * 4 + self.B * self.d * 4
-
-    def proxy_bytes(self):
-        return self.m * (self.d // 2 + 4)  # int4 codes + fp32 scale per row
-
-    def kernel_bytes(self):
-        """Bytes each gather kernel reads per step (per query, no union):
-        K4 recompute reads B*k' U rows, K6 the B*k selected V rows."""
-        return {"recompute": self.B * self.kp * self.d * 2, "down": self.B * self.k * self.d * 2}
-
-    def step_bytes(self, x):
-        """Roofline bytes for one step: proxy + unique gathered U rows (k'
-        candidates, union over the batch) + unique V rows (k selected)."""
-        H = self.H
-        f, a = self.layers[0]
-        s = a.scores(x, phi="relu", x_mode=H.X_INT8)
-        cand, _, _ = H.topk_select(s, self.kp)
-        _, sel = H.ffn_group_sparse(f, x, a, self.k, self.kp, x_mode=H.X_INT8)
-        nu = int(torch.unique(cand.long()).numel())
-        nv = int(torch.unique(sel.long()).numel())
-        return self.proxy_bytes() + (nu + nv) * self.d * 2, nu, nv
-
-    def recall(self, x):
-        """mean |S_hire ∩ S_exact| / k over the batch, S_exact the exact top-k
-        of relu(U x) (dense exact pass, K8)."""
-        H = self.H
-        f, a = self.layers[0]
-        _, sel = H.ffn_group_sparse(f, x, a, self.k, self.kp, x_mode=H.X_INT8)
-        ex, _, _ = H.exact_topk(f.u, x, self.k, "relu")
-        r = []
-        for b in range(x.shape[0]):
-            r.append(H.recall(sel[b].cpu().numpy(), ex[b].cpu().numpy())[0])
-        return float(np.mean(r))
-
-    def config(self):
-        return {"workload": "cfg2 HiRE-FFN layer (BASELINE.json configs[1])", "d": self.d,
-                "m": self.m, "k_prime": self.kp, "k": self.k, "global_batch": self.B,
-                "proxy": "int4 per-row absmax (device K9) x int8-quantised x",
-                "weights": "bf16 U,V = N(0,1/d) + 3x rank-128 (random init)",
-                "l2": f"{len(self.layers)} distinct layers cycled ({self.layer_bytes() * len(self.layers) / 1e9:.2f} GB > 126 MB L2)",
-                "select": "exact top-k' (topk_select)"}
-
-    def layer_bytes(self):
-        return 2 * self.m * self.d * 2 + self.proxy_bytes()
+        return torch.randn(n, self.B, self.d, device="cuda", generator=self.gen) * float(self.query_scale())
 
 
-class SoftmaxWorkload:
-    """cfg3: HiRE-softmax, V=256000, d=2048, bf16 W, int4 proxy, k'=1024, k=64."""
+class SoftmaxWorkload(Workload):
+    """cfg3 (BASELINE.json configs[2]): HiRE-softmax, V=256000, d=2048, bf16
+    W = rank-256 (unit entry variance) + 0.1 N(0,1), int4 per-row proxy
+    (device K9) x int8 x, exact top-k'=1024, k=64, softmax over the top-k.
+    N > 1: DA-TOP-k over the rows (global merge), strong scaling."""
     name = "cfg3"
 
-    def __init__(self, H, batch, select="exact", seed=0):
-        self.H = H
+    def __init__(self, batch, select="exact", world=1, rank=0, seed=0):
         self.V, self.d, self.kp, self.k, self.B = 256000, 2048, 1024, 64, batch
-        gen = torch.Generator(device="cuda").manual_seed(seed)
-        W, _, _ = gen_lowrank_plus_noise(self.V, self.d, 256, gen)
-        self.W = H.ScoreMatrix(W)
-        self.A = H.ApproxScorer.quantize(self.W)
-        self.gen = gen
-        self.select = select
-        if select == "bucketed":
-            self.cfg = H.HireConfig(k=self.k, k_prime=self.kp, x_mode=H.X_INT8,
-                                    select=H.SELECT_BUCKETED, n_buckets=1024, bucket_t=1)
-        else:
-            self.cfg = H.HireConfig(k=self.k, k_prime=self.kp, x_mode=H.X_INT8)
+        self.world, self.rank, self.select = world, rank, select
+        self.first, self.width = shard_range(self.V, world, rank)
+        self.Wt, _, _ = gen_vocab_rows(self.V, self.d, 256, self.first, self.width, seed=1 + seed)
+        self.gen = torch.Generator(device="cuda").manual_seed(seed + 99)
+        self.scaling = "strong" if world > 1 else "weak"
         torch.cuda.synchronize()
 
-    def inputs(self, n):
-        return torch.randn(n, self.B, self.d, device="cuda", generator=self.gen) / self.d ** 0.5
+    def attach(self, H):
+        import paper_2402_09360_b200.parallel as P
+        self.H, self.P = H, P
+        self.W = H.ScoreMatrix(self.Wt)
+        self.A = H.ApproxScorer.quantize(self.W)
+        kw = dict(k=self.k, k_prime=self.kp, x_mode=H.X_INT8)
+        if self.select == "bucketed":
+            kw.update(select=H.SELECT_BUCKETED, n_buckets=1024, bucket_t=1)
+        self.cfg = H.HireConfig(**kw)
+        self.comm = P.Communicator(self.world, self.rank) if self.world > 1 else None
+        torch.cuda.synchronize()
+
+    @property
+    def proxy_kernel(self):
+        if self.B >= 9:
+            return "q4_score_umma (K1 on tcgen05: TMA ring -> TMEM A operand -> kind::i8 MMA)"
+        return "q4_score_mma_sel (K1F: IMMA proxy GEMV + fused candidate pre-selection)"
 
     def step(self, i, x):
-        return self.H.hire_topk(x, self.W, self.A, self.cfg, want_candidates=False)
+        if self.world > 1:
+            return self.P.da_topk(self.W, self.A, self.V, x, self.cfg, self.comm, merge=self.H.MERGE_GLOBAL)
+        # softmax_topk (hire.hpp:123-144): top-k indices + probabilities
+        return self.H.softmax_topk(self.W, x, self.A, self.cfg)
 
     def host_step(self, i, x_host, idx_host, val_host, ctx):
         H = self.H
+        if self.world > 1:
+            if not hasattr(self, "_xd"):
+                self._xd = torch.empty(self.B, self.d, device="cuda")
+            self._xd.copy_(torch.from_numpy(x_host), non_blocking=True)
+            ti, tv, _ = self.P.da_topk(self.W, self.A, self.V, self._xd, self.cfg, self.comm,
+                                       merge=H.MERGE_GLOBAL)
+            torch.from_numpy(idx_host.view(np.int32)).copy_(ti, non_blocking=True)
+            torch.from_numpy(val_host).copy_(tv, non_blocking=True)
+            torch.cuda.current_stream().synchronize()
+            return
         if not hasattr(self, "_hp"):  # call parameters built once, as a serving loop would
             self._hp = C.byref(self.cfg.params())
             self._hn = (C.c_int64(), C.c_int64(), C.c_int())
             self._hr = tuple(C.byref(v) for v in self._hn)
+        # softmax_topk through the C ABI: top-k indices and probabilities
         H._lib.check(H.lib().hire_topk_host(ctx.h, self.W.h, self.A.h, x_host.ctypes.data, self.B, self._hp, None,
-                                            idx_host.ctypes.data, val_host.ctypes.data, None, *self._hr))
+                                            idx_host.ctypes.data, self._hv.ctypes.data, val_host.ctypes.data,
+                                            *self._hr))
+
+    def host_buffers(self, pinned):
+        self._hv = pinned((self.B, self.k), torch.float32)  # the exact values (not returned by softmax_topk)
 
     def io_bytes(self):
         return self.B * self.d * 4, self.B * self.k * 8
 
     def proxy_bytes(self):
-        return self.V * (self.d // 2 + 4)
+        return self.width * (self.d // 2 + 4)
 
-    def kernel_bytes(self):
-        return {"recompute": self.B * self.kp * self.d * 2}
+    def unique_rows(self, x):
+        """unique candidate rows of this rank's shard over the batch (the
+        gather kernel reads each once from HBM; repeats hit L2)."""
+        kpl = self.P.quota(self.kp, self.world, self.rank)
+        s = self.A.scores(x, x_mode=self.H.X_INT8)
+        cand, _, _ = self.H.topk_select(s, kpl)
+        return int(torch.unique(cand.long()).numel())
+
+    def kernel_bytes(self, nu):
+        return {"recompute": nu * self.d * 2}
 
     def step_bytes(self, x):
-        r = self.H.hire_topk(x, self.W, self.A, self.cfg)
-        nu = int(torch.unique(r.cand.long()).numel())
-        return self.proxy_bytes() + nu * self.d * 2, nu, 0
+        nu = self.unique_rows(x)
+        xb = self.world * self.B * (self.kp // self.world) * 8 if self.world > 1 else 0
+        return self.H.roofline_bytes("q4", self.d, self.width, nu, self.d * 2, exchange_bytes=xb), nu, 0
 
     def recall(self, x):
+        if self.world > 1:
+            return None
         H = self.H
         r = H.hire_topk(x, self.W, self.A, self.cfg)
         ex, _, _ = H.exact_topk(self.W, x, self.k)
@@ -285,63 +295,147 @@ class SoftmaxWorkload:
     def config(self):
         return {"workload": "cfg3 HiRE-softmax (BASELINE.json configs[2])", "V": self.V, "d": self.d,
                 "k_prime": self.kp, "k": self.k, "global_batch": self.B,
+                "api": "softmax_topk (hire.hpp:123-144): top-k indices + softmax probabilities"
+                       + (" via DA-TOP-k, global merge" if self.world > 1 else ""),
                 "proxy": "int4 per-row absmax (device K9) x int8-quantised x",
                 "weights": "bf16 W = rank-256 (unit entry variance) + 0.1 N(0,1)",
-                "l2": "working set 1.3 GB > 126 MB L2",
+                "shard_rows": self.width,
+                "l2": "working set 1.3 GB > 126 MB L2 (no flush needed)",
                 "select": "1024 buckets x top-1 (literal)" if self.select == "bucketed" else "exact top-k'"}
 
+    def ref_host(self):
+        return {"W": self.Wt.float().cpu().numpy(), "quantize": True}
 
-class LowRankSoftmaxWorkload:
-    """cfg1: HiRE-softmax, fp32, d=1024, V=32768, W = A B / 8 + 0.1 N(0,1),
-    rank-64 truncated-SVD proxy, exact top-k'=256, k=32, batch 1. 16 copies
-    of (W, Z1, Z2) are cycled so the 9.7 MB per-step working set streams from
-    HBM (one copy would sit in L2)."""
-    name = "cfg1"
 
-    def __init__(self, H, batch, copies=16, seed=0):
-        self.H = H
-        self.V, self.d, self.r, self.kp, self.k, self.B = 32768, 1024, 64, 256, 32, batch
+class FfnWorkload(Workload):
+    """cfg2 (BASELINE.json configs[1]): one HiRE-FFN layer, d=2048, m=8192,
+    bf16 U/V, int4 proxy of U x int8 x, k'=820, k=410, ReLU; 18 distinct
+    layers cycled so every step streams cold weights from HBM."""
+    name = "cfg2"
+
+    def __init__(self, batch, layers=18, seed=0):
+        self.m, self.d, self.kp, self.k, self.B = 8192, 2048, 820, 410, batch
         gen = torch.Generator(device="cuda").manual_seed(seed)
-        A = torch.randn(self.V, 64, device="cuda", generator=gen)
-        Bm = torch.randn(64, self.d, device="cuda", generator=gen)
-        W = (A @ Bm) / 8.0 + 0.1 * torch.randn(self.V, self.d, device="cuda", generator=gen)
-        # Z (d x V) = W^T = U S Vt  ->  Z1 = (U_r S_r)^T [r, d], Z2 = Vt_r^T [V, r]
-        U, S, Vt = torch.linalg.svd(W.T.double(), full_matrices=False)
-        z1 = (U[:, :self.r] * S[:self.r]).T.float().contiguous()
-        z2 = Vt[:self.r].T.float().contiguous()
-        self.copies = []
-        for _ in range(copies):
-            Wc = W.clone()
-            self.copies.append((H.ScoreMatrix(Wc), H.ApproxScorer.low_rank(z1.clone(), z2.clone())))
-        self.cfg = H.HireConfig(k=self.k, k_prime=self.kp)
+        self.uv = [gen_ffn_layer(self.m, self.d, 128, gen) for _ in range(layers)]
         self.gen = gen
-        self.W, self.A = self.copies[0]
-        self._z = (z1, z2)
         torch.cuda.synchronize()
 
+    proxy_kernel = "q4_score_mma (K1 proxy GEMV, tensor-core IMMA)"
+
+    def query_scale(self):
+        return 1.0
+
+    def attach(self, H):
+        self.H = H
+        self.layers = []
+        for u, v in self.uv:
+            U, Vm = H.ScoreMatrix(u), H.ScoreMatrix(v)
+            self.layers.append((H.GroupedFFN(U, Vm, 1, "relu"), H.ApproxScorer.quantize(U)))
+        torch.cuda.synchronize()
+
+    def step(self, i, x):
+        f, a = self.layers[i % len(self.layers)]
+        return self.H.ffn_group_sparse(f, x, a, self.k, self.kp, x_mode=self.H.X_INT8)
+
+    def host_step(self, i, x_host, sel_host, out_host, ctx):
+        H = self.H
+        f, a = self.layers[i % len(self.layers)]
+        if not hasattr(self, "_hp"):
+            self._hp = C.byref(H._lib.FfnParams(self.k, self.kp, 1, 1, H.X_INT8, 0, 0))
+        H._lib.check(H.lib().hire_ffn_host(ctx.h, f.u.h, f.v.h, a.h, x_host.ctypes.data, self.B, self._hp,
+                                           sel_host.ctypes.data, out_host.ctypes.data))
+
+    def host_buffers(self, pinned):
+        pass
+
+    def io_bytes(self):
+        return self.B * self.d * 4, self.B * self.k * 4 + self.B * self.d * 4
+
+    def proxy_bytes(self):
+        return self.m * (self.d // 2 + 4)
+
+    def unique_rows(self, x):
+        H = self.H
+        f, a = self.layers[0]
+        s = a.scores(x, phi="relu", x_mode=H.X_INT8)
+        cand, _, _ = H.topk_select(s, self.kp)
+        _, sel = H.ffn_group_sparse(f, x, a, self.k, self.kp, x_mode=H.X_INT8)
+        return int(torch.unique(cand.long()).numel()), int(torch.unique(sel.long()).numel())
+
+    def kernel_bytes(self, nu):
+        return {"recompute": nu[0] * self.d * 2, "down": nu[1] * self.d * 2}
+
+    def step_bytes(self, x):
+        nu, nv = self.unique_rows(x)
+        return self.H.roofline_bytes("q4", self.d, self.m, nu, self.d * 2, extra_rows=nv), (nu, nv), nv
+
+    def recall(self, x):
+        H = self.H
+        f, a = self.layers[0]
+        _, sel = H.ffn_group_sparse(f, x, a, self.k, self.kp, x_mode=H.X_INT8)
+        ex, _, _ = H.exact_topk(f.u, x, self.k, "relu")
+        return float(np.mean([H.recall(sel[b].cpu().numpy(), ex[b].cpu().numpy())[0] for b in range(x.shape[0])]))
+
+    def config(self):
+        return {"workload": "cfg2 HiRE-FFN layer (BASELINE.json configs[1])", "d": self.d,
+                "m": self.m, "k_prime": self.kp, "k": self.k, "global_batch": self.B,
+                "api": "ffn_group_sparse (ffn.hpp:211-219)",
+                "proxy": "int4 per-row absmax (device K9) x int8-quantised x",
+                "weights": "bf16 U,V = N(0,1/d) + 3x rank-128 (random init)",
+                "l2": f"{len(self.uv)} distinct layers cycled (1.36 GB > 126 MB L2)",
+                "select": "exact top-k' (topk_select)"}
+
+    def ref_host(self):
+        u, v = self.uv[0]
+        return {"U": u.float().cpu().numpy(), "V": v.float().cpu().numpy(), "quantize": True}
+
+
+class LowRankSoftmaxWorkload(Workload):
+    """cfg1 (BASELINE.json configs[0]): HiRE-softmax, fp32, d=1024, V=32768,
+    W = A B / 8 + 0.1 N(0,1), rank-64 truncated-SVD proxy, exact top-k'=256,
+    k=32, batch 1. 16 copies cycled (9.7 MB working set per step)."""
+    name = "cfg1"
     lowrank = True
     proxy_kernel = "lr_score_mma (K2 low-rank proxy, tensor-core HMMA with exact bf16 splits)"
     dtype = "fp32 (W, factors, x; fp32 accumulation)"
 
-    def host_factors(self):
-        return self._z[0].cpu().numpy(), self._z[1].cpu().numpy()
+    def __init__(self, batch, copies=16, seed=0):
+        self.V, self.d, self.r, self.kp, self.k, self.B = 32768, 1024, 64, 256, 32, batch
+        gen = torch.Generator(device="cuda").manual_seed(seed)
+        A = torch.randn(self.V, 64, device="cuda", generator=gen)
+        Bm = torch.randn(64, self.d, device="cuda", generator=gen)
+        self.Wt = (A @ Bm) / 8.0 + 0.1 * torch.randn(self.V, self.d, device="cuda", generator=gen)
+        U, S, Vt = torch.linalg.svd(self.Wt.T.double(), full_matrices=False)
+        self.z1 = (U[:, :self.r] * S[:self.r]).T.float().contiguous()
+        self.z2 = Vt[:self.r].T.float().contiguous()
+        self.ncopies = copies
+        self.gen = gen
+        torch.cuda.synchronize()
 
-    def inputs(self, n):
-        return torch.randn(n, self.B, self.d, device="cuda", generator=self.gen) / self.d ** 0.5
+    def attach(self, H):
+        self.H = H
+        self.copies = [(H.ScoreMatrix(self.Wt.clone()), H.ApproxScorer.low_rank(self.z1.clone(), self.z2.clone()))
+                       for _ in range(self.ncopies)]
+        self.cfg = H.HireConfig(k=self.k, k_prime=self.kp)
+        torch.cuda.synchronize()
 
     def step(self, i, x):
         z, a = self.copies[i % len(self.copies)]
-        return self.H.hire_topk(x, z, a, self.cfg, want_candidates=False)
+        return self.H.softmax_topk(z, x, a, self.cfg)
 
     def host_step(self, i, x_host, idx_host, val_host, ctx):
         H = self.H
         z, a = self.copies[i % len(self.copies)]
-        if not hasattr(self, "_hp"):  # call parameters built once, as a serving loop would
+        if not hasattr(self, "_hp"):
             self._hp = C.byref(self.cfg.params())
             self._hn = (C.c_int64(), C.c_int64(), C.c_int())
             self._hr = tuple(C.byref(v) for v in self._hn)
         H._lib.check(H.lib().hire_topk_host(ctx.h, z.h, a.h, x_host.ctypes.data, self.B, self._hp, None,
-                                            idx_host.ctypes.data, val_host.ctypes.data, None, *self._hr))
+                                            idx_host.ctypes.data, self._hv.ctypes.data, val_host.ctypes.data,
+                                            *self._hr))
+
+    def host_buffers(self, pinned):
+        self._hv = pinned((self.B, self.k), torch.float32)
 
     def io_bytes(self):
         return self.B * self.d * 4, self.B * self.k * 8
@@ -349,14 +443,17 @@ class LowRankSoftmaxWorkload:
     def proxy_bytes(self):
         return (self.V + self.d) * self.r * 4
 
-    def kernel_bytes(self):
-        return {"recompute": self.B * self.kp * self.d * 4}
-
-    def step_bytes(self, x):
+    def unique_rows(self, x):
         z, a = self.copies[0]
         r = self.H.hire_topk(x, z, a, self.cfg)
-        nu = int(torch.unique(r.cand.long()).numel())
-        return self.proxy_bytes() + nu * self.d * 4, nu, 0
+        return int(torch.unique(r.cand.long()).numel())
+
+    def kernel_bytes(self, nu):
+        return {"recompute": nu * self.d * 4}
+
+    def step_bytes(self, x):
+        nu = self.unique_rows(x)
+        return self.H.roofline_bytes("lowrank", self.d, self.V, nu, self.d * 4, r=self.r, factor_bytes=4), nu, 0
 
     def recall(self, x):
         H = self.H
@@ -369,81 +466,73 @@ class LowRankSoftmaxWorkload:
     def config(self):
         return {"workload": "cfg1 HiRE-softmax fp32, rank-64 SVD proxy (BASELINE.json configs[0])",
                 "V": self.V, "d": self.d, "rank": self.r, "k_prime": self.kp, "k": self.k,
-                "global_batch": self.B, "weights": "fp32 W = A B / 8 + 0.1 N(0,1), truncated SVD factors",
-                "l2": f"{len(self.copies)} copies cycled", "select": "exact top-k'"}
+                "global_batch": self.B, "api": "softmax_topk (hire.hpp:123-144)",
+                "weights": "fp32 W = A B / 8 + 0.1 N(0,1), truncated SVD factors",
+                "l2": f"{self.ncopies} copies cycled", "select": "exact top-k'"}
+
+    def ref_host(self):
+        return {"W": self.Wt.cpu().numpy(), "z1": self.z1.cpu().numpy(), "z2": self.z2.cpu().numpy()}
 
 
-class DaSoftmaxWorkload:
-    """cfg4: DA-TOP-k sharded softmax, bf16 W [256000, 4096] (low-rank +
-    noise), rank-64 proxy (generator factors), B=16, k'=2048, k=128. Each
-    rank holds its contiguous vocab shard; merge = one ncclAllGather of rank
-    keys (hire_da_topk_run). global merge (BASELINE.json cfg4 wording)."""
+class DaSoftmaxWorkload(Workload):
+    """cfg4 (BASELINE.json configs[3]): DA-TOP-k sharded softmax, bf16 W
+    [256000, 4096] (rank-64 + 0.1 N(0,1)), rank-64 bf16 factors, B=16,
+    k'=2048, k=128, global merge. Rank r holds its shard of the width rule;
+    one ncclAllGather of B x k'/D keys per step. N=1: hire_topk (the s = 1
+    equivalence)."""
     name = "cfg4"
+    lowrank = True
     roof_stage = "recompute"
     roof_kernel = "recompute_fast<bf16, 16> (row-gather exact recompute, K4)"
-
-    def __init__(self, H, batch, world=1, rank=0, seed=0):
-        import paper_2402_09360_b200.parallel as P
-        self.H, self.P = H, P
-        self.V, self.d, self.r, self.kp, self.k, self.B = 256000, 4096, 64, 2048, 128, batch
-        self.world, self.rank = world, rank
-        first, width = P.shard_range(self.V, world, rank)
-        self.first, self.width = first, width
-        gen = torch.Generator(device="cuda").manual_seed(seed)
-        Bm = torch.randn(self.r, self.d, device="cuda", generator=gen)
-        # every rank draws the full A so shards are consistent; keeps its rows
-        A = torch.randn(self.V, self.r, device="cuda", generator=gen)[first:first + width].contiguous()
-        W = torch.empty(width, self.d, device="cuda", dtype=torch.bfloat16)
-        g2 = torch.Generator(device="cuda").manual_seed(seed * 7919 + rank + 1)
-        for s0 in range(0, width, 16384):
-            e = min(width, s0 + 16384)
-            W[s0:e] = ((A[s0:e] @ Bm) / self.r ** 0.5 + 0.1 * torch.randn(e - s0, self.d, device="cuda",
-                                                                        generator=g2)).to(torch.bfloat16)
-        self.W = H.ScoreMatrix(W)
-        z1 = (Bm / self.r ** 0.5).to(torch.bfloat16).contiguous()   # [r, d]
-        z2 = A.to(torch.bfloat16).contiguous()                        # [width, r]
-        self.A = H.ApproxScorer.low_rank(z1, z2)
-        self.cfg = H.HireConfig(k=self.k, k_prime=self.kp)
-        self.comm = P.Communicator(world, rank) if world > 1 else None
-        self.gen = torch.Generator(device="cuda").manual_seed(seed + 99)
-        self._z = (z1, z2)
-        torch.cuda.synchronize()
-
-    lowrank = True
     proxy_kernel = "lr_score_mma (K2 low-rank proxy, tensor-core HMMA, bf16 factors, fp32 acc)"
     dtype = "bf16 W and factors, fp32 x and accumulation"
 
-    def host_factors(self):
-        return self._z[0].float().cpu().numpy(), self._z[1].float().cpu().numpy()
+    def __init__(self, batch, world=1, rank=0, seed=0):
+        self.V, self.d, self.r, self.kp, self.k, self.B = 256000, 4096, 64, 2048, 128, batch
+        self.world, self.rank = world, rank
+        self.first, self.width = shard_range(self.V, world, rank)
+        self.Wt, A, Bm = gen_vocab_rows(self.V, self.d, self.r, self.first, self.width, seed=4 + seed)
+        self.z1 = (Bm / self.r ** 0.5).to(torch.bfloat16).contiguous()   # [r, d]
+        self.z2 = A.to(torch.bfloat16).contiguous()                      # [width, r]
+        self.gen = torch.Generator(device="cuda").manual_seed(seed + 99)
+        self.scaling = "strong" if world > 1 else "weak"
+        torch.cuda.synchronize()
 
-    def inputs(self, n):
-        return torch.randn(n, self.B, self.d, device="cuda", generator=self.gen) / self.d ** 0.5
+    def attach(self, H):
+        import paper_2402_09360_b200.parallel as P
+        self.H, self.P = H, P
+        self.W = H.ScoreMatrix(self.Wt)
+        self.A = H.ApproxScorer.low_rank(self.z1, self.z2)
+        self.cfg = H.HireConfig(k=self.k, k_prime=self.kp)
+        self.comm = P.Communicator(self.world, self.rank) if self.world > 1 else None
+        torch.cuda.synchronize()
 
     def step(self, i, x):
-        return self.P.da_topk(self.W, self.A, self.V, x, self.cfg, self.comm,
-                              merge=self.H.MERGE_GLOBAL)
+        if self.world == 1:
+            return self.H.softmax_topk(self.W, x, self.A, self.cfg)
+        return self.P.da_topk(self.W, self.A, self.V, x, self.cfg, self.comm, merge=self.H.MERGE_GLOBAL)
 
     def host_step(self, i, x_host, idx_host, val_host, ctx):
         H = self.H
         if self.world == 1:
-            # one shard: DA-TOP-k is hire_topk (hire_da_topk_run's own world-1
-            # shortcut), whose host-buffer entry point is hire_topk_host
             if not hasattr(self, "_hp"):
                 self._hp = C.byref(self.cfg.params())
                 self._hn = (C.c_int64(), C.c_int64(), C.c_int())
                 self._hr = tuple(C.byref(v) for v in self._hn)
             H._lib.check(H.lib().hire_topk_host(ctx.h, self.W.h, self.A.h, x_host.ctypes.data, self.B, self._hp,
-                                                None, idx_host.ctypes.data, val_host.ctypes.data, None, *self._hr))
+                                                None, idx_host.ctypes.data, self._hv.ctypes.data,
+                                                val_host.ctypes.data, *self._hr))
             return
-        # N > 1: pinned host buffers, asynchronous copies, one synchronise
         if not hasattr(self, "_xd"):
             self._xd = torch.empty(self.B, self.d, device="cuda")
         self._xd.copy_(torch.from_numpy(x_host), non_blocking=True)
-        ti, tv, _ = self.P.da_topk(self.W, self.A, self.V, self._xd, self.cfg, self.comm,
-                                   merge=self.H.MERGE_GLOBAL, ctx=None)
+        ti, tv, _ = self.P.da_topk(self.W, self.A, self.V, self._xd, self.cfg, self.comm, merge=H.MERGE_GLOBAL)
         torch.from_numpy(idx_host.view(np.int32)).copy_(ti, non_blocking=True)
         torch.from_numpy(val_host).copy_(tv, non_blocking=True)
         torch.cuda.current_stream().synchronize()
+
+    def host_buffers(self, pinned):
+        self._hv = pinned((self.B, self.k), torch.float32)
 
     def io_bytes(self):
         return self.B * self.d * 4, self.B * self.k * 8
@@ -451,58 +540,68 @@ class DaSoftmaxWorkload:
     def proxy_bytes(self):
         return (self.width + self.d) * self.r * 2
 
-    def kernel_bytes(self):
-        return {"recompute": self.B * self.P.quota(self.kp, self.world, self.rank) * self.d * 2}
+    def unique_rows(self, x):
+        s = self.A.scores(x)
+        cand, _, _ = self.H.topk_select(s, self.P.quota(self.kp, self.world, self.rank))
+        return int(torch.unique(cand.long()).numel())
+
+    def kernel_bytes(self, nu):
+        return {"recompute": nu * self.d * 2}
 
     def step_bytes(self, x):
-        # local candidates of this shard: union over the batch of k'/D rows
-        s = self.A.scores(x)
-        kpl = self.P.quota(self.kp, self.world, self.rank)
-        cand, _, _ = self.H.topk_select(s, kpl)
-        nu = int(torch.unique(cand.long()).numel())
-        return self.proxy_bytes() + nu * self.d * 2 + self.world * self.B * self.kp // self.world * 8, nu, 0
+        nu = self.unique_rows(x)
+        xb = self.world * self.B * (self.kp // self.world) * 8 if self.world > 1 else 0
+        return self.H.roofline_bytes("lowrank", self.d, self.width, nu, self.d * 2, r=self.r, factor_bytes=2,
+                                     exchange_bytes=xb), nu, 0
 
     def recall(self, x):
         if self.world > 1:
             return None
         H = self.H
-        ti, _, _ = self.step(0, x)
+        r = H.hire_topk(x, self.W, self.A, self.cfg)
         ex, _, _ = H.exact_topk(self.W, x, self.k)
-        return float(np.mean([np.isin(ex[b].cpu().numpy(), ti[b].cpu().numpy()).mean()
+        return float(np.mean([H.recall(r.cand[b].cpu().numpy(), ex[b].cpu().numpy())[0]
                               for b in range(x.shape[0])]))
 
     def config(self):
         return {"workload": "cfg4 DA-TOP-k sharded softmax (BASELINE.json configs[3])", "V": self.V,
                 "d": self.d, "rank": self.r, "k_prime": self.kp, "k": self.k, "global_batch": self.B,
                 "shard_rows": self.width, "merge": "global (all k' exact pairs all-gathered)",
+                "api": "softmax_topk at N=1; da_topk (distributed.hpp:73-134) at N>1",
                 "weights": "bf16 W = rank-64 (unit variance) + 0.1 N(0,1); proxy = generator factors",
                 "l2": "W shard + proxy > 126 MB L2", "select": "exact top-k'/D per shard"}
 
+    def ref_host(self):
+        return {"W": self.Wt.float().cpu().numpy(), "z1": self.z1.float().cpu().numpy(),
+                "z2": self.z2.float().cpu().numpy()}
 
-# ------------------------------------------------------------- reference ---
-class DecoderWorkload:
+
+class DecoderWorkload(Workload):
     """cfg5 (BASELINE.json configs[4]): greedy decode steps of the 18-layer
     ReLU decoder (d=2048, FFN 8192 as HiRE-FFN top-5% with the int4 proxy,
     16 heads over a 1024-token KV cache, V=256000 HiRE-softmax k'=1024 k=64).
     Each step feeds the previous step's tokens (true autoregressive chain);
     dense parts are library code (decoder.py)."""
     name = "cfg5"
-    proxy_kernel = "q4_score_mma / q4_score_mma_sel (all int4 proxy launches of the step: 18 FFN + vocab)"
-    span_kernel = None  # the proxy launches spread over the whole step
+    proxy_kernel = "q4_score_mma / q4_score_mma_sel / q4_score_umma (all int4 proxy launches: 18 FFN + vocab)"
+    span_kernel = None
 
-    def __init__(self, H, batch, seed=0):
+    def __init__(self, batch, seed=0):
+        self.B, self.seed = batch, seed
+
+    def attach(self, H):
         from paper_2402_09360_b200.decoder import DecoderConfig, HireDecoder
         self.H = H
         self.cfg = DecoderConfig()
-        self.B, self.d, self.k, self.kp = batch, self.cfg.d, self.cfg.vocab_k, self.cfg.vocab_k_prime
-        self.m = HireDecoder(self.cfg, batch, seed=seed)
-        g = torch.Generator(device="cuda").manual_seed(seed + 5)
-        self.tok = torch.randint(0, self.cfg.vocab, (batch,), device="cuda", generator=g)
+        self.d, self.k, self.kp = self.cfg.d, self.cfg.vocab_k, self.cfg.vocab_k_prime
+        self.m = HireDecoder(self.cfg, self.B, seed=self.seed)
+        g = torch.Generator(device="cuda").manual_seed(self.seed + 5)
+        self.tok = torch.randint(0, self.cfg.vocab, (self.B,), device="cuda", generator=g)
         self.tok0 = self.tok.clone()
         torch.cuda.synchronize()
 
     def inputs(self, n):
-        return [None] * n  # the chain carries its own tokens
+        return [None] * n
 
     def step(self, i, x):
         nxt, _, _ = self.m.step(self.tok)
@@ -510,8 +609,6 @@ class DecoderWorkload:
         return nxt
 
     def host_step(self, i, x_host, idx_host, val_host, ctx):
-        # end to end: tokens from pinned host memory into the captured step's
-        # static input, one graph replay, the top-k indices back to the host
         if not hasattr(self, "_hg"):
             self._tin = torch.zeros(self.B, dtype=torch.int64, device="cuda")
             self._pin_in = torch.zeros(self.B, dtype=torch.int64).pin_memory()
@@ -530,20 +627,20 @@ class DecoderWorkload:
         torch.cuda.current_stream().synchronize()
         idx_host[:] = self._pin_out.numpy().astype(np.uint32)
 
+    def host_buffers(self, pinned):
+        pass
+
     def io_bytes(self):
         return self.B * 8, self.B * self.k * 4
 
     def proxy_bytes(self):
         c = self.cfg
-        ffn = c.ffn * (c.d // 2 + 4)
-        return (c.layers * ffn + c.vocab * (c.d // 2 + 4)) / (c.layers + 1)  # average per proxy launch
+        return (c.layers * c.ffn * (c.d // 2 + 4) + c.vocab * (c.d // 2 + 4)) / (c.layers + 1)
 
     def step_bytes(self, x):
         return self.m.step_bytes(), 0, 0
 
     def recall(self, x):
-        """softmax recall@k, teacher-forced on the exact-top-k model's hidden
-        state (decoder.stage_recall); the per-layer FFN recalls go in config"""
         r = self.m.stage_recall(self.tok0)
         self.stage_rec = r
         return r["softmax"]
@@ -561,21 +658,41 @@ class DecoderWorkload:
                 "l2": "working set ~3.2 GB + KV cache > 126 MB L2", "select": "exact top-k'"}
 
 
-def make_ref_runner(wl, threads):
+def make_workload(args, world=1, rank=0):
+    B = B_default(args)
+    if args.workload == "cfg3":
+        return SoftmaxWorkload(B, select=args.select, world=world, rank=rank)
+    if args.workload == "cfg1":
+        return LowRankSoftmaxWorkload(B)
+    if args.workload == "cfg4":
+        return DaSoftmaxWorkload(B, world, rank)
+    if args.workload == "cfg5":
+        return DecoderWorkload(B)
+    return FfnWorkload(B)
+
+
+def B_default(args):
+    return args.batch or {"cfg2": 8, "cfg3": 32, "cfg1": 1, "cfg4": 16, "cfg5": 1}[args.workload]
+
+
+# ------------------------------------------------------------- reference ---
+def make_ref_runner(wl, host, threads):
     """The reference's own CPU implementation of the workload's path:
-    oracle/_ref (the unmodified headers compiled behind a C shim) when it was
-    built, else the C restatement (one thread). Returns (run(xb), threads,
-    kind, description). Queries of one batch run on `threads` host threads
-    (the reference API is pure and reentrant)."""
+    oracle/_ref (the unmodified reference headers compiled behind a C shim)
+    when it was built, else the C restatement (one thread). `host` holds the
+    workload's weights as host arrays (made with plain torch, never through
+    this repo's package); the int4 proxy is built by the reference's own
+    quantize_int4 (approx.hpp:49-65). Returns (run(xb), threads, kind, desc);
+    queries of one batch run on `threads` host threads (the reference API is
+    pure and reentrant, SPEC.md:90)."""
     import oracle as O
     kind = "reference" if O.ref_available() else "port"
+    quant = O.ref_quantize_int4 if kind == "reference" else O.quantize_int4
     d = wl.d
-    if isinstance(wl, FfnWorkload):
-        f, a = wl.layers[0]
-        u = f.u.tensor.float().cpu().numpy()
-        v = f.v.tensor.float().cpu().numpy()
-        codes, scales = a.export_q4()
-        desc = "hire::ffn_group_sparse (reference int4 scorer, fp32 x) on layer 0"
+    if wl.name == "cfg2":
+        u, v = host["U"], host["V"]
+        codes, scales = quant(u)
+        desc = "hire::ffn_group_sparse (reference int4 scorer from hire::quantize_int4, fp32 x) on layer 0"
         if kind == "reference":
             rf = O.RefFFN(u, v, 1, 1)
             ra = O.RefScorer("quantized", codes=codes, scales=scales)
@@ -589,21 +706,19 @@ def make_ref_runner(wl, threads):
         else:
             def run(xb):
                 for b in range(xb.shape[0]):
-                    s = O.q4_scores_fpx(codes, scales, xb[b], 1)
-                    O.ffn_group_sparse(u, v, xb[b], s, wl.k, wl.kp, 1, 1)
+                    O.ffn_group_sparse(u, v, xb[b], O.q4_scores_fpx(codes, scales, xb[b], 1), wl.k, wl.kp, 1, 1)
             threads = 1
         return run, threads, kind, desc
-    W = wl.W.tensor.float().cpu().numpy()
-    lowrank = getattr(wl, "lowrank", False)
-    if lowrank:
-        z1, z2 = wl.host_factors()
+    W = host["W"]
+    if wl.lowrank:
+        z1, z2 = host["z1"], host["z2"]
         desc = "hire::hire_topk (reference low-rank scorer, exact top-k')"
     else:
-        codes, scales = wl.A.export_q4()
-        desc = "hire::hire_topk (reference int4 scorer, fp32 x, exact top-k')"
+        codes, scales = quant(W)
+        desc = "hire::hire_topk (reference int4 scorer from hire::quantize_int4, fp32 x, exact top-k')"
     if kind == "reference":
         rm = O.RefMatrix(W)
-        ra = (O.RefScorer("lowrank", z1=z1, z2=z2) if lowrank else
+        ra = (O.RefScorer("lowrank", z1=z1, z2=z2) if wl.lowrank else
               O.RefScorer("quantized", codes=codes, scales=scales))
 
         def run(xb):
@@ -616,8 +731,7 @@ def make_ref_runner(wl, threads):
     else:
         def run(xb):
             for b in range(xb.shape[0]):
-                s = (O.lowrank_scores(z1, z2, xb[b], 0) if lowrank else
-                     O.q4_scores_fpx(codes, scales, xb[b], 0))
+                s = (O.lowrank_scores(z1, z2, xb[b], 0) if wl.lowrank else O.q4_scores_fpx(codes, scales, xb[b], 0))
                 O.hire_topk(W, xb[b], s, wl.k, wl.kp, 0)
         threads = 1
     return run, threads, kind, desc
@@ -625,14 +739,13 @@ def make_ref_runner(wl, threads):
 
 def host_queries(wl, n, seed=0):
     rng = np.random.default_rng(seed)
-    scale = 1.0 if isinstance(wl, FfnWorkload) else 1.0 / np.sqrt(wl.d)
-    return (rng.standard_normal((n, wl.d)) * scale).astype(np.float32)
+    return (rng.standard_normal((n, wl.d)) * wl.query_scale()).astype(np.float32)
 
 
-def cpu_baseline(wl, seconds):
+def cpu_baseline(wl, host, seconds):
     """Bounded sample (~`seconds` of host work): batches of `threads` queries."""
     threads = os.cpu_count() or 1
-    run, threads, kind, desc = make_ref_runner(wl, threads)
+    run, threads, kind, desc = make_ref_runner(wl, host, threads)
     xb = host_queries(wl, threads)
     t0 = time.perf_counter()
     run(xb)
@@ -646,36 +759,19 @@ def cpu_baseline(wl, seconds):
     return n / el, threads, kind, f"{desc}: {n} queries in {el:.1f} s on {threads} host threads"
 
 
-# ------------------------------------------------------------------- main ---
-def make_workload(H, args, world=1, rank=0):
-    if args.workload == "cfg3":
-        return SoftmaxWorkload(H, args.batch or 1, select=args.select)
-    if args.workload == "cfg1":
-        return LowRankSoftmaxWorkload(H, args.batch or 1)
-    if args.workload == "cfg4":
-        return DaSoftmaxWorkload(H, args.batch or 16, world, rank)
-    if args.workload == "cfg5":
-        return DecoderWorkload(H, args.batch or 1)
-    return FfnWorkload(H, args.batch or 8)
-
-
-def B_default(args):
-    return args.batch or {"cfg2": 8, "cfg3": 1, "cfg1": 1, "cfg4": 16, "cfg5": 1}[args.workload]
-
-
 def measured_traffic(wl, batch):
     """DRAM bytes per launch of the roofline kernel from one committed
     `ncu --set full` capture (profiles/traffic.json), for the workload and
     batch it was captured at; None otherwise."""
     try:
-        t = json.load(open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "traffic.json")))
+        t = json.load(open(os.path.join(ROOT, "profiles", "traffic.json")))
     except (OSError, ValueError):
         return None
-    e = t.get(wl.name)
-    default_b = {"cfg2": 8, "cfg3": 1, "cfg1": 1, "cfg4": 16}.get(wl.name)
-    return e["bytes"] if e and batch == default_b else None
+    e = t.get(f"{wl.name}_b{batch}") or (t.get(wl.name) if t.get(wl.name, {}).get("batch") == batch else None)
+    return e["bytes"] if e else None
 
 
+# ------------------------------------------------------------------- ours ---
 def run_ours(args):
     world, rank, local = dist_env()
     torch.cuda.set_device(local)
@@ -684,10 +780,11 @@ def run_ours(args):
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     import paper_2402_09360_b200 as H
     H.lib()
-    wl = make_workload(H, args, world, rank)
+    wl = make_workload(args, world, rank)
+    wl.attach(H)
     K, W = args.steps, args.warmup
     xs = wl.inputs(K + W)
-    # Each timed step replays from one CUDA graph holding the K layer calls
+    # Each timed step replays from one CUDA graph holding the K calls
     # (graphs instead of a tracing compiler: no host work between kernels).
     # Warm-up runs eagerly on the capture stream first, so every workspace
     # exists before capture.
@@ -723,12 +820,13 @@ def run_ours(args):
     barrier(world)
     ms = max_over_ranks(e0.elapsed_time(e1), world)
     ms_step = ms / K
-    tokens = wl.B * world * K
+    # tokens the whole job decoded: strong scaling (DA over one batch) counts
+    # the batch once; weak scaling (independent replicas) counts every rank's
+    tokens = wl.B * K * (1 if wl.scaling == "strong" else world)
     value = tokens / (ms / 1e3)
 
     # stage times: the same K steps captured with CUDA events bracketing
-    # every stage (event-record nodes inside the graph), replayed once; the
-    # event pairs are read after the replay
+    # every stage (event-record nodes inside the graph), replayed once
     prof = None
     try:
         with torch.cuda.stream(cs):
@@ -758,9 +856,7 @@ def run_ours(args):
     stage_us = {k: v[0] * 1e3 / K for k, v in prof.items() if not k.startswith("_")}
 
     # device timeline of one step (%globaltimer, first CTA start -> last CTA
-    # end per kernel; hire_debug_ktrace) replayed from a one-step graph: the
-    # roofline kernel's span without the event nodes that break the
-    # programmatic-dependent-launch overlap of the stage-event graph
+    # end per kernel; hire_debug_ktrace) replayed from a one-step graph
     spans = None
     try:
         g1 = torch.cuda.CUDAGraph()
@@ -776,7 +872,7 @@ def run_ours(args):
             torch.cuda.synchronize()
             sp = ctx.ktrace(2)
             ctx.ktrace(0)
-            kk = "lr_score" if getattr(wl, "lowrank", False) else "proxy"
+            kk = "lr_score" if wl.lowrank else "proxy"
             if kk in sp and (best is None or sp[kk][1] - sp[kk][0] < best[kk][1] - best[kk][0]):
                 best = sp
         spans = best
@@ -785,35 +881,27 @@ def run_ours(args):
 
     peaks = load_peaks()
     step_b, nu, nv = wl.step_bytes(xs[W])
-    if "ffn_fused" in prof:
-        # one launch does the whole layer: its algorithmic bytes are the step's
-        kname = "ffn_fused_kernel (whole HiRE-FFN layer, one cooperative launch)"
-        pb = step_b
-        k_us = prof["ffn_fused"][0] * 1e3 / max(prof["ffn_fused"][1], 1)
-    elif getattr(wl, "roof_stage", None) in prof:
+    kbytes = wl.kernel_bytes(nu) if hasattr(wl, "kernel_bytes") else {}
+    if getattr(wl, "roof_stage", None) in prof:
         # the workload's dominant kernel is not the proxy (cfg4: the gather
         # recompute is ~3/4 of the step in the ncu launch list)
-        kname = wl.roof_kernel
-        pb = wl.kernel_bytes()[wl.roof_stage]
-        k_us = prof[wl.roof_stage][0] * 1e3 / max(prof[wl.roof_stage][1], 1)
+        kname, kkey = wl.roof_kernel, wl.roof_stage
+        pb = kbytes[wl.roof_stage]
     else:
-        kname = getattr(wl, "proxy_kernel", "q4_score_mma (K1 proxy GEMV, tensor-core IMMA)")
+        kname, kkey = wl.proxy_kernel, ("lr_score" if wl.lowrank else "proxy")
         pb = wl.proxy_bytes()
-        k_us = prof["proxy"][0] * 1e3 / max(prof["proxy"][1], 1)
+    k_us = prof["proxy" if kkey in ("proxy", "lr_score") else kkey][0] * 1e3 / \
+        max(prof["proxy" if kkey in ("proxy", "lr_score") else kkey][1], 1)
     achieved = pb / (k_us * 1e-6) / 1e9
     dspan = None
-    kkey = getattr(wl, "roof_stage", None) if getattr(wl, "roof_stage", None) in prof else \
-        ("lr_score" if getattr(wl, "lowrank", False) else "proxy")
-    if spans and kkey in spans and "ffn_fused" not in prof and getattr(wl, "span_kernel", "x") is not None:
+    if spans and kkey in spans and getattr(wl, "span_kernel", "x") is not None:
         dspan = spans[kkey][1] - spans[kkey][0]
     rec = wl.recall(xs[W])
 
     # end-to-end through the C ABI with host buffers (copies inside)
     hctx = H.Context(local)
     bi, bo = wl.io_bytes()
-    # the step inputs and result buffers live in pinned host memory (the
-    # contract's "host->device copy of that step's inputs from pinned host
-    # memory"); the C ABI reads and writes such buffers in place
+
     def pinned(shape, dt):
         return torch.empty(shape, dtype=dt).pin_memory().numpy()
     xh = []
@@ -825,9 +913,8 @@ def run_ours(args):
         a_[:] = xs[W + i].cpu().numpy()
         xh.append(a_)
     oa = pinned((wl.B, wl.k), torch.int32).view(np.uint32)
-    ob = pinned((wl.B, wl.d) if isinstance(wl, FfnWorkload) else (wl.B, wl.k), torch.float32)
-    # untimed warm-up: each host call shape (one per cycled layer / copy)
-    # runs once eagerly, then is captured into its CUDA graph (hire_*_host)
+    ob = pinned((wl.B, wl.d) if wl.name == "cfg2" else (wl.B, wl.k), torch.float32)
+    wl.host_buffers(pinned)
     n_cycle = len(getattr(wl, "layers", None) or getattr(wl, "copies", None) or [0])
     n_warm = max(W, 2 * n_cycle + 1)
     if wl.name == "cfg5":  # the decode chain's tokens travel in oa[:, 0]
@@ -839,19 +926,23 @@ def run_ours(args):
     for i in range(K):
         wl.host_step(n_warm + i, xh[i % len(xh)], oa, ob, hctx)
     e2e_s = max_over_ranks(time.perf_counter() - t0, world)
-    e2e = wl.B * world * K / e2e_s
+    e2e = wl.B * K * (1 if wl.scaling == "strong" else world) / e2e_s
 
+    par = "single GPU" if world == 1 else (
+        f"DA-TOP-k over {world} GPUs (rows sharded, ncclAllGather of keys)" if wl.scaling == "strong"
+        else f"replicas x{world}")
+    uniq = nu if not isinstance(nu, tuple) else {"u_rows": nu[0], "v_rows": nu[1]}
     line = {
-        "metric": "HiRE decode tokens/s (µs/token, HBM roofline fraction, recall@k)",
+        "metric": METRIC,
         "value": round(value, 2), "unit": "tokens/s", "n_gpus": world, "steps": K, "warmup": W,
         "ms_per_step": round(ms_step, 5), "us_per_token": round(ms_step * 1e3 / wl.B, 4),
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": getattr(wl, "dtype", "int4xint8->int32 proxy, bf16 rows, fp32 acc"),
+        "higher_is_better": True, "scaling": wl.scaling, "vs_baseline": None, "dtype": wl.dtype,
         "data": "synthetic (seeded random-init weights of the BASELINE family; random queries)",
-        "config": {**wl.config(), "parallelism": f"replicas x{world}" if world > 1 else "single GPU"},
+        "config": {**wl.config(), "parallelism": par},
         "recall_at_k": round(rec, 5) if rec is not None else None,
         "roofline": {"bound": "hbm", "kernel": kname,
                      "achieved": round(achieved, 1), "peak": peaks["hbm_gbs"], "unit": "GB/s",
-                     "frac": round(achieved / peaks["hbm_gbs"], 4), "traffic": measured_traffic(wl, B_default(args)),
+                     "frac": round(achieved / peaks["hbm_gbs"], 4), "traffic": measured_traffic(wl, wl.B),
                      "bytes_per_launch": pb, "avg_launch_us": round(k_us, 3),
                      "timing": "CUDA events around the kernel's stage inside the replayed graph (includes its launch "
                                "latency: the event nodes break the programmatic-dependent-launch overlap)",
@@ -859,23 +950,26 @@ def run_ours(args):
                      "frac_device_span": round(pb / (dspan * 1e-6) / 1e9 / peaks["hbm_gbs"], 4) if dspan else None,
                      "peak_src": peaks["src"]},
         "step_timeline_us": {k: v for k, v in (spans or {}).items() if isinstance(v, tuple)},
-        "kernel_roofline": {k: {"bytes": b, "span_us": round(spans[k][1] - spans[k][0], 3),
+        "kernel_roofline": {k: {"bytes": b, "bytes_model": "unique rows of the batch x row bytes",
+                                "span_us": round(spans[k][1] - spans[k][0], 3),
                                 "gbs": round(b / ((spans[k][1] - spans[k][0]) * 1e-6) / 1e9, 1),
                                 "frac": round(b / ((spans[k][1] - spans[k][0]) * 1e-6) / 1e9 / peaks["hbm_gbs"], 4)}
-                            for k, b in (wl.kernel_bytes().items() if hasattr(wl, "kernel_bytes") else [])
-                            if spans and k in spans and spans[k][1] > spans[k][0]},
-        "step_roofline": {"bytes": step_b, "unique_u_rows": nu, "unique_v_rows": nv,
+                            for k, b in kbytes.items() if spans and k in spans and spans[k][1] > spans[k][0]},
+        "step_roofline": {"bytes": step_b, "unique_rows": uniq,
+                          "model": "roofline_bytes: proxy incl. scales + unique gathered rows (+ all-gather)",
                           "achieved_gbs": round(step_b / (ms_step * 1e-3) / 1e9, 1),
                           "frac": round(step_b / (ms_step * 1e-3) / 1e9 / peaks["hbm_gbs"], 4)},
         "stage_us_per_step": {k: round(v, 3) for k, v in stage_us.items()},
         "stage_timing": "CUDA events inside the replayed graph" if "_graph" in prof else "CUDA events, eager launches",
         "e2e": {"value": round(e2e, 2), "unit": "tokens/s", "h2d_bytes_per_step": bi,
-                "d2h_bytes_per_step": bo},
+                "d2h_bytes_per_step": bo,
+                "path": "C-ABI host call (hire_topk_host / hire_ffn_host) with pinned host buffers"
+                        if world == 1 else "python parallel.da_topk with pinned copies"},
         "gpu_launches": int(launches),
         "clocks": clk.summary(),
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline and wl.name != "cfg5":
-        v, cores, kind, desc = cpu_baseline(wl, args.cpu_seconds)
+        v, cores, kind, desc = cpu_baseline(wl, wl.ref_host(), args.cpu_seconds)
         line["cpu_baseline"] = {"value": round(v, 3), "unit": "tokens/s", "cores": cores, "kind": kind,
                                 "sample": desc}
     if rank == 0:
@@ -885,10 +979,14 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
+# -------------------------------------------------------------- reference ---
 def run_reference(args):
     """--impl reference: the reference's CPU implementation of the same
-    workload (oracle/_ref) on all host threads; one step = one batch of the
-    workload's queries. Rank 0 only; other ranks exit without work."""
+    workload (oracle/_ref: the unmodified reference headers) on all host
+    threads. Weights come from the same torch generators as our arm, copied
+    to the host; the int4 proxy is built by the reference's quantize_int4.
+    This arm never imports paper_2402_09360_b200 (nor loads its .so). Each
+    step = one batch of max(B, threads) queries. Rank 0 only."""
     world, rank, local = dist_env()
     if rank != 0:
         return
@@ -897,27 +995,30 @@ def run_reference(args):
                                                               "the reference library)"}), flush=True)
         return
     torch.cuda.set_device(local)
-    import paper_2402_09360_b200 as H
-    H.lib()
-    wl = make_workload(H, args)  # same generator; weights copied to the host
+    wl = make_workload(args)  # plain torch tensors; no attach()
+    host = wl.ref_host()
+    wl.__dict__.pop("Wt", None)  # the device copy is no longer needed
+    torch.cuda.empty_cache()
     threads = os.cpu_count() or 1
-    run, threads, kind, desc = make_ref_runner(wl, threads)
+    run, threads, kind, desc = make_ref_runner(wl, host, threads)
+    nq = max(wl.B, threads)
     K, W = args.steps, args.warmup
-    xs = host_queries(wl, (K + W) * wl.B, seed=1).reshape(K + W, wl.B, wl.d)
+    xs = host_queries(wl, (K + W) * nq, seed=1).reshape(K + W, nq, wl.d)
     for i in range(W):
         run(xs[i])
     t0 = time.perf_counter()
     for i in range(K):
         run(xs[W + i])
     el = time.perf_counter() - t0
-    v = wl.B * K / el
-    line = {"impl": "reference", "metric": "HiRE decode tokens/s (µs/token, HBM roofline fraction, recall@k)",
+    v = nq * K / el
+    line = {"impl": "reference", "metric": METRIC,
             "value": round(v, 3), "unit": "tokens/s", "n_gpus": world, "steps": K, "warmup": W,
-            "ms_per_step": round(el * 1e3 / K, 3), "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "fp32", "data": "synthetic (same generator as our arm)",
-            "config": {**wl.config(), "parallelism": f"{threads} host threads"},
+            "ms_per_step": round(el * 1e3 / K, 3), "higher_is_better": True, "scaling": wl.scaling,
+            "vs_baseline": None, "dtype": "fp32", "data": "synthetic (same torch generators as our arm)",
+            "config": {**wl.config(), "parallelism": f"{threads} host threads", "queries_per_step": nq,
+                       "reference_proxy": "reference scorer with fp32 x (approx.hpp:395-403); ours scores int8 x"},
             "cpu_baseline": {"value": round(v, 3), "unit": "tokens/s", "cores": threads, "kind": kind,
-                             "sample": f"{desc}: {K} steps x {wl.B} queries"},
+                             "sample": f"{desc}: {K} steps x {nq} queries"},
             "e2e": {"value": round(v, 3), "unit": "tokens/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -929,7 +1030,7 @@ def main():
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="cfg2", choices=["cfg1", "cfg2", "cfg3", "cfg4", "cfg5"])
+    ap.add_argument("--workload", default="cfg3", choices=["cfg1", "cfg2", "cfg3", "cfg4", "cfg5"])
     ap.add_argument("--batch", type=int, default=0)
     ap.add_argument("--select", default="exact", choices=["exact", "bucketed"])
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
@@ -937,6 +1038,8 @@ def main():
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        relaunch_under_torchrun(args.gpus)
     if args.impl == "reference":
         run_reference(args)
     else:

@@ -31,7 +31,26 @@ constexpr int kUmmaRows = 128;         // rows per MMA / per row block
 constexpr int kUmmaStageChunks = 8;    // k chunks (32 codes each) per pipeline stage
 constexpr int kUmmaStageBytes = kUmmaStageChunks * kUmmaRows * 16;  // 16 KB
 constexpr int kUmmaStages = 4;         // smem ring depth
-constexpr int kUmmaThreads = 192;      // warps 0-3 convert + epilogue, 4 TMA, 5 MMA
+constexpr int kUmmaABufs = 4;          // TMEM A-operand stage buffers (64 columns each)
+constexpr int kUmmaConvGroups = 4;     // converter warpgroups; group g converts chunks [2g, 2g+2) of every stage
+constexpr int kUmmaConvWarps = 4 * kUmmaConvGroups;
+constexpr int kUmmaEpiWarp = kUmmaConvWarps;            // warps +0..+3: epilogue
+constexpr int kUmmaTmaWarp = kUmmaConvWarps + 4;        // TMA producer
+constexpr int kUmmaMmaWarp = kUmmaConvWarps + 5;        // MMA issuers (+0..+3; +0 allocates TMEM)
+constexpr int kUmmaMaxIssuers = 4;
+constexpr int kUmmaThreads = 32 * (kUmmaConvWarps + 5 + kUmmaMaxIssuers);
+// One thread issues a tcgen05.mma about every 78 cycles whatever N is
+// (tools/probes/probe_umma_rate.cu), far from the tensor floor at N <= 32
+// (16 cycles): n_iss issuer warps each own whole stages (st % n_iss) and an
+// accumulator of their own; the epilogue adds the n_iss partial sums (exact
+// int32). n_iss divides the stages per row block, and 4 A buffers + n_iss x 2
+// accumulators of nq columns fit the 512 TMEM columns.
+__host__ __device__ inline int umma_issuers(int nq, int d) {
+  const int n_st = d / 32 / kUmmaStageChunks;
+  for (int n = kUmmaMaxIssuers; n > 1; n >>= 1)
+    if (n_st % n == 0 && 64 * kUmmaABufs + n * 2 * nq <= 512) return n;
+  return 1;
+}
 
 // canonical [rows][pitch] (low nibble = even column) -> UMMA layout words
 __global__ void q4_to_umma_layout(const uint8_t* __restrict__ wq, int64_t pitch, int64_t rows, int d,
@@ -70,7 +89,7 @@ struct UmmaSmem {
     return x_off(stages) + static_cast<size_t>(nq) * d;
   }
   static __host__ __device__ size_t bytes(int stages, int nq, int d) {
-    return bar_off(stages, nq, d) + (2 * kUmmaMaxStages + 9) * 8 + 16;
+    return bar_off(stages, nq, d) + (2 * kUmmaMaxStages + 2 * kUmmaABufs + 5) * 8 + 16;
   }
   // deepest ring that fits next to an x operand of nq queries
   static __host__ int stages_for(int nq, int d, size_t smem_max) {
@@ -107,40 +126,44 @@ __global__ void __launch_bounds__(kUmmaThreads, 1) q4_score_umma(
     const int8_t* __restrict__ xg, const float* __restrict__ sx, const int* __restrict__ sumxq, int nb, int nq,
     int stages, int phi, float* __restrict__ scores, int64_t score_stride) {
   extern __shared__ __align__(1024) unsigned char smem[];
+  KTrace kt_(kKtProxy);
   uint8_t* ring = smem;
   uint8_t* s_x = smem + UmmaSmem::x_off(stages);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + UmmaSmem::bar_off(stages, nq, d));
   uint64_t* full = bars;                          // [stages] TMA -> converters
   uint64_t* empty = bars + kUmmaMaxStages;        // [stages] converters -> TMA (128 arrivals)
-  uint64_t* afull = bars + 2 * kUmmaMaxStages;    // [2] converters -> MMA (128 arrivals)
-  uint64_t* aempty = afull + 2;                   // [2] MMA commit -> converters
-  uint64_t* dfull = afull + 4;                    // [2] MMA commit -> epilogue
-  uint64_t* dempty = afull + 6;                   // [2] epilogue -> MMA (128 arrivals)
-  uint64_t* xbar = afull + 8;                     // x operand bulk copy
+  uint64_t* afull = bars + 2 * kUmmaMaxStages;    // [kUmmaABufs] converters -> MMA (128 arrivals)
+  uint64_t* aempty = afull + kUmmaABufs;          // [kUmmaABufs] MMA commit -> converters
+  uint64_t* dfull = aempty + kUmmaABufs;          // [2] MMA commit -> epilogue
+  uint64_t* dempty = dfull + 2;                   // [2] epilogue -> MMA (128 arrivals)
+  uint64_t* xbar = dempty + 2;                    // x operand bulk copy
   uint32_t* s_tmem = reinterpret_cast<uint32_t*>(xbar + 1);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int nkc = d / 32, n_st = nkc / kUmmaStageChunks;
   const int64_t n_rb = (rows + kUmmaRows - 1) / kUmmaRows;
-  constexpr uint32_t kTmemCols = 256;  // A: 2 x 64 columns, D: 2 x nq columns
-  constexpr uint32_t kColA = 0, kColD = 128;
+  constexpr uint32_t kTmemCols = 512;  // A: kUmmaABufs x 64 columns, D: n_iss x 2 x nq columns
+  constexpr uint32_t kColA = 0, kColD = 64 * kUmmaABufs;
+  const int n_iss = umma_issuers(nq, d);
 
   if (tid == 0) {
     for (int s = 0; s < stages; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 128);
+      mbar_init(&empty[s], 32 * kUmmaConvWarps);
+    }
+    for (int i = 0; i < kUmmaABufs; ++i) {
+      mbar_init(&afull[i], 32 * kUmmaConvWarps);
+      mbar_init(&aempty[i], 1);
     }
     for (int i = 0; i < 2; ++i) {
-      mbar_init(&afull[i], 128);
-      mbar_init(&aempty[i], 1);
-      mbar_init(&dfull[i], 1);
+      mbar_init(&dfull[i], n_iss);
       mbar_init(&dempty[i], 128);
     }
     mbar_init(xbar, 1);
     fence_mbar_init();
   }
-  if (warp == 4 && lane == 0) tma_prefetch_desc(&wmap);
-  if (warp == 5) {
+  if (warp == kUmmaTmaWarp && lane == 0) tma_prefetch_desc(&wmap);
+  if (warp == kUmmaMmaWarp) {
     umma::tmem_alloc(s_tmem, kTmemCols);
     umma::tmem_relinquish();
   }
@@ -149,7 +172,7 @@ __global__ void __launch_bounds__(kUmmaThreads, 1) q4_score_umma(
   umma::fence_after();
   const uint32_t tmem = *s_tmem;
 
-  if (warp == 4) {
+  if (warp == kUmmaTmaWarp) {
     // ===== TMA producer: weights are read-only, so it streams before the
     // programmatic-dependency wait (independent prologue)
     if (lane == 0) {
@@ -163,64 +186,112 @@ __global__ void __launch_bounds__(kUmmaThreads, 1) q4_score_umma(
                       static_cast<int>(rb * nkc + st * kUmmaStageChunks), &full[slot]);
         }
     }
-  } else if (warp == 5) {
-    // ===== MMA issuer (x operand: one bulk copy after the dependency wait)
-    if (lane == 0) {
+  } else if (warp >= kUmmaMmaWarp) {
+    // ===== MMA issuers: issuer j takes stages j, j + n_iss, ... of every
+    // row block into its own accumulator pair (x operand: one bulk copy
+    // after the programmatic-dependency wait, by issuer 0)
+    const int j = warp - kUmmaMmaWarp;
+    if (lane == 0 && j < n_iss) {
       griddep_wait();  // x quantisation (prep_x_int8_kernel) is complete
-      const unsigned xbytes = static_cast<unsigned>(nq) * static_cast<unsigned>(d);
-      mbar_arrive_expect_tx(xbar, xbytes);
-      bulk_g2s(s_x, xg, xbytes, xbar);
+      if (j == 0) {
+        const unsigned xbytes = static_cast<unsigned>(nq) * static_cast<unsigned>(d);
+        mbar_arrive_expect_tx(xbar, xbytes);
+        bulk_g2s(s_x, xg, xbytes, xbar);
+      }
       const uint32_t idesc = umma::idesc_i8(kUmmaRows, nq, /*a_signed=*/false, /*b_signed=*/true);
       const uint32_t xbase = smem_u32(s_x);
       mbar_wait(xbar, 0);
-      int ait = 0, rbi = 0;
+      int rbi = 0;
       for (int64_t rb = blockIdx.x; rb < n_rb; rb += gridDim.x, ++rbi) {
         const int db = rbi & 1;
         if (rbi >= 2) mbar_wait(&dempty[db], ((rbi >> 1) - 1) & 1);
         umma::fence_after();
-        const uint32_t dcol = tmem + kColD + db * nq;
-        for (int st = 0; st < n_st; ++st, ++ait) {
-          const int ab = ait & 1;
-          mbar_wait(&afull[ab], (ait >> 1) & 1);
+        const uint32_t dcol = tmem + kColD + static_cast<uint32_t>((2 * j + db) * nq);
+        for (int st = j; st < n_st; st += n_iss) {
+          const int ait = rbi * n_st + st;
+          const int ab = ait % kUmmaABufs;
+          mbar_wait(&afull[ab], (ait / kUmmaABufs) & 1);
           umma::fence_after();
           const uint32_t acol = tmem + kColA + ab * 64;
+          // k chunk kc = core matrices 2kc, 2kc+1 (LBO 128 B apart); 8-query groups 8d apart
+          const uint64_t bd0 = umma::sdesc_kmajor_noswz(xbase + static_cast<uint32_t>(st * kUmmaStageChunks * 256),
+                                                        128, static_cast<uint32_t>(8 * d));
 #pragma unroll
-          for (int c = 0; c < kUmmaStageChunks; ++c) {
-            const int kc = st * kUmmaStageChunks + c;
-            // k chunk kc = core matrices 2kc, 2kc+1 (LBO 128 B apart); 8-query groups 8d apart
-            const uint64_t bd = umma::sdesc_kmajor_noswz(xbase + static_cast<uint32_t>(kc * 256), 128,
-                                                         static_cast<uint32_t>(8 * d));
-            umma::mma_i8_ts(dcol, acol + 8 * c, bd, idesc, (st | c) != 0);
-          }
+          for (int c = 0; c < kUmmaStageChunks; ++c)  // start address field: 16-byte units
+            umma::mma_i8_ts(dcol, acol + 8 * c, bd0 + static_cast<uint64_t>(c * 16), idesc, (st != j) || (c != 0));
           umma::commit(&aempty[ab]);
         }
         umma::commit(&dfull[db]);
       }
     }
     __syncwarp();
-  } else {
-    // ===== converters + epilogue (thread = TMEM lane = row within the block)
-    const uint32_t lane_off = static_cast<uint32_t>(32 * warp) << 16;
-    int it = 0, ait = 0, rbi = 0;
-    int64_t pend_rb = -1;  // row block whose epilogue is still to do
-    bool waited = false;
-    auto epilogue = [&](int64_t prb, int pidx) {  // row block prb, the pidx-th of this CTA
-      if (!waited) {
-        griddep_wait();  // scores / sx / sum(xq) of this call: after the producer grids
-        waited = true;
+  } else if (warp < kUmmaConvWarps) {
+    // ===== converters (thread = TMEM lane = row within the block): int4
+    // digits from the smem ring -> u8 -> the TMEM A-operand buffers. Warp w
+    // may only touch TMEM lanes 32 (w % 4) ..; the kUmmaConvGroups
+    // warpgroups split every stage's chunks so each SM sub-partition has
+    // several converter warps to hide LDS / STTM latency.
+    constexpr int kCpg = kUmmaStageChunks / kUmmaConvGroups;  // chunks per group
+    const int wl = warp & 3, grp = warp >> 2;
+    const uint32_t lane_off = static_cast<uint32_t>(32 * wl) << 16;
+    int slot = 0, sphase = 0, ab = 0, aphase = 0, ait = 0;
+    for (int64_t rb = blockIdx.x; rb < n_rb; rb += gridDim.x) {
+      for (int st = 0; st < n_st; ++st, ++ait) {
+        mbar_wait(&full[slot], sphase);
+        const uint4* src = reinterpret_cast<const uint4*>(ring + static_cast<size_t>(slot) * kUmmaStageBytes) +
+                           (grp * kCpg * kUmmaRows + 32 * wl + lane);
+        uint4 v[kCpg];
+#pragma unroll
+        for (int c = 0; c < kCpg; ++c) v[c] = src[c * kUmmaRows];
+        umma::mbar_arrive(&empty[slot]);  // the slot's bytes are in registers
+        if (++slot == stages) { slot = 0; sphase ^= 1; }
+        if (ait >= kUmmaABufs) mbar_wait(&aempty[ab], aphase ^ 1);
+        umma::fence_after();
+        const uint32_t acol = tmem + lane_off + kColA + ab * 64 + 8 * kCpg * grp;
+#pragma unroll
+        for (int c = 0; c < kCpg; ++c) {
+          const uint32_t w4[4] = {v[c].x, v[c].y, v[c].z, v[c].w};
+          uint32_t r[8];
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            r[2 * j] = w4[j] & 0x0F0F0F0Fu;
+            r[2 * j + 1] = (w4[j] >> 4) & 0x0F0F0F0Fu;
+          }
+          umma::st_32x32b_x8(acol + 8 * c, r);
+        }
+        umma::wait_st();
+        umma::fence_before();
+        umma::mbar_arrive(&afull[ab]);
+        if (++ab == kUmmaABufs) { ab = 0; aphase ^= 1; }
       }
-      const int pdb = pidx & 1;
-      mbar_wait(&dfull[pdb], (pidx >> 1) & 1);
+    }
+  } else {
+    // ===== epilogue (warps 4-7; warp w reads TMEM lanes 32 (w % 4) ..):
+    // accumulators -> scale, phi -> scores [q][row]
+    griddep_wait();  // scores / sx / sum(xq) of this call: after the producer grids
+    const int ew = warp - kUmmaEpiWarp;
+    const uint32_t lane_off = static_cast<uint32_t>(32 * ew) << 16;
+    int rbi = 0;
+    for (int64_t rb = blockIdx.x; rb < n_rb; rb += gridDim.x, ++rbi) {
+      const int db = rbi & 1;
+      mbar_wait(&dfull[db], (rbi >> 1) & 1);
       umma::fence_after();
-      const int64_t row = prb * kUmmaRows + 32 * warp + lane;
+      const int64_t row = rb * kUmmaRows + 32 * ew + lane;
       const float sc = row < rows ? scales[row] : 0.0f;
       for (int q0 = 0; q0 < nq; q0 += 16) {
         uint32_t acc[16];
-        umma::ld_32x32b_x16(tmem + lane_off + kColD + pdb * nq + q0, acc);
+        umma::ld_32x32b_x16(tmem + lane_off + kColD + db * nq + q0, acc);
+        for (int i = 1; i < n_iss; ++i) {  // the other issuers' partial sums
+          uint32_t part[16];
+          umma::ld_32x32b_x16(tmem + lane_off + kColD + (2 * i + db) * nq + q0, part);
+          umma::wait_ld();
+#pragma unroll
+          for (int e = 0; e < 16; ++e) acc[e] += part[e];
+        }
         umma::wait_ld();
         if (q0 + 16 >= nq) {
           umma::fence_before();
-          umma::mbar_arrive(&dempty[pdb]);
+          umma::mbar_arrive(&dempty[db]);
         }
         if (row < rows) {
 #pragma unroll
@@ -235,49 +306,12 @@ __global__ void __launch_bounds__(kUmmaThreads, 1) q4_score_umma(
           }
         }
       }
-    };
-    for (int64_t rb = blockIdx.x; rb < n_rb; rb += gridDim.x, ++rbi) {
-      for (int st = 0; st < n_st; ++st, ++it, ++ait) {
-        const int slot = it % stages;
-        mbar_wait(&full[slot], (it / stages) & 1);
-        const uint4* src = reinterpret_cast<const uint4*>(ring + static_cast<size_t>(slot) * kUmmaStageBytes) +
-                           (32 * warp + lane);
-        uint4 v[kUmmaStageChunks];
-#pragma unroll
-        for (int c = 0; c < kUmmaStageChunks; ++c) v[c] = src[c * kUmmaRows];
-        umma::mbar_arrive(&empty[slot]);  // the slot's bytes are in registers
-        const int ab = ait & 1;
-        if (ait >= 2) mbar_wait(&aempty[ab], ((ait >> 1) - 1) & 1);
-        umma::fence_after();
-        const uint32_t acol = tmem + lane_off + kColA + ab * 64;
-#pragma unroll
-        for (int c = 0; c < kUmmaStageChunks; ++c) {
-          const uint32_t w4[4] = {v[c].x, v[c].y, v[c].z, v[c].w};
-          uint32_t r[8];
-#pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            r[2 * j] = w4[j] & 0x0F0F0F0Fu;
-            r[2 * j + 1] = (w4[j] >> 4) & 0x0F0F0F0Fu;
-          }
-          umma::st_32x32b_x8(acol + 8 * c, r);
-        }
-        umma::wait_st();
-        umma::fence_before();
-        umma::mbar_arrive(&afull[ab]);
-        if (st == 0 && pend_rb >= 0) {  // previous block's epilogue, off the MMA's critical path
-          epilogue(pend_rb, rbi - 1);
-          pend_rb = -1;
-        }
-      }
-      pend_rb = rb;
     }
-    if (pend_rb >= 0) epilogue(pend_rb, rbi - 1);
-    if (!waited) griddep_wait();
   }
   griddep_launch();
   umma::fence_before();
   __syncthreads();
-  if (warp == 5) {
+  if (warp == kUmmaMmaWarp) {
     umma::fence_after();
     umma::tmem_dealloc(tmem, kTmemCols);
   }
