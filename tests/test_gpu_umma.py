@@ -67,3 +67,71 @@ def test_umma_full_vocab_cfg3_b32(H, O):
     for b in (0, 17, 31):
         want = O.q4_scores_int8(codes, scales, x[b], 0)
         assert np.array_equal(got[b].view(np.uint32), want.view(np.uint32)), b
+
+
+# ---- hire_topk on the tcgen05 proxy (9..64 queries): candidates through the selector ---
+def _inst(H, O, V, d, seed, kind="lowrank"):
+    if kind == "lowrank":
+        w = _data.lowrank_plus_noise(V, d, 32, seed)
+    elif kind == "int_ties":
+        g = np.random.default_rng(seed)
+        w = g.integers(-7, 8, size=(V, d)).astype(np.float32)
+        w[:, 0] = 7.0
+    else:  # equal rows: every score ties
+        g = np.random.default_rng(seed)
+        w = np.tile(g.standard_normal((1, d)).astype(np.float32), (V, 1))
+    codes, scales = O.quantize_int4(w)
+    return w, H.ScoreMatrix(T(w)), H.ApproxScorer.quantized(codes, scales), codes, scales
+
+
+def _want(O, codes, scales, x, kp):
+    idx, _, _ = O.topk_select(O.q4_scores_int8(codes, scales, x, 0), kp)
+    return np.sort(idx.astype(np.uint32))
+
+
+@pytest.mark.parametrize("V,d,kp,B", [(100000, 256, 1024, 9), (256000, 256, 1024, 32), (60000, 512, 4000, 17),
+                                      (200000, 256, 2048, 64), (30001, 256, 512, 12)])
+def test_umma_topk_candidates_bitexact(H, O, V, d, kp, B):
+    w, z, a, codes, scales = _inst(H, O, V, d, V + B)
+    x = _data.queries(B, d, V + 1)
+    r = H.hire_topk(T(x), z, a, H.HireConfig(k=16, k_prime=kp, x_mode=H.X_INT8))
+    for b in range(B):
+        assert np.array_equal(r.cand[b].cpu().numpy().astype(np.uint32), _want(O, codes, scales, x[b], kp)), b
+
+
+@pytest.mark.parametrize("kind", ["int_ties", "equal_rows"])
+def test_umma_topk_ties_and_fallback(H, O, kind):
+    V, d, kp, B = 40000, 256, 700, 12
+    w, z, a, codes, scales = _inst(H, O, V, d, 4, kind)
+    x = np.round(_data.queries(B, d, 5, scale=3.0)).astype(np.float32)
+    x[2] = 0.0  # all-zero query: every score 0, ties broken by index
+    r = H.hire_topk(T(x), z, a, H.HireConfig(k=4, k_prime=kp, x_mode=H.X_INT8))
+    for b in range(B):
+        assert np.array_equal(r.cand[b].cpu().numpy().astype(np.uint32), _want(O, codes, scales, x[b], kp)), b
+
+
+def test_umma_topk_graph_replay(H, O):
+    """zero-at-rest selector state under CUDA-graph replay, an all-zero
+    query (exact fallback) inside a replay"""
+    V, d, kp, B = 150000, 256, 1024, 24
+    w, z, a, codes, scales = _inst(H, O, V, d, 8)
+    cfg = H.HireConfig(k=64, k_prime=kp, x_mode=H.X_INT8)
+    x = _data.queries(B, d, 9)
+    g = np.random.default_rng(11)
+    xd = T(x)
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        H.hire_topk(xd, z, a, cfg)
+        torch.cuda.synchronize()
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph, stream=s):
+            r = H.hire_topk(xd, z, a, cfg)
+    for it in range(4):
+        xh = (g.standard_normal((B, d)) / np.sqrt(d)).astype(np.float32)
+        if it == 2:
+            xh[5] = 0.0
+        xd.copy_(T(xh))
+        graph.replay()
+        torch.cuda.synchronize()
+        for b in range(B):
+            assert np.array_equal(r.cand[b].cpu().numpy().astype(np.uint32), _want(O, codes, scales, xh[b], kp)), (it, b)
