@@ -32,13 +32,22 @@ constexpr int kUmmaStageChunks = 8;    // k chunks (32 codes each) per pipeline 
 constexpr int kUmmaStageBytes = kUmmaStageChunks * kUmmaRows * 16;  // 16 KB
 constexpr int kUmmaStages = 4;         // smem ring depth
 constexpr int kUmmaABufs = 4;          // TMEM A-operand stage buffers (64 columns each)
-constexpr int kUmmaConvGroups = 4;     // converter warpgroups; group g converts chunks [2g, 2g+2) of every stage
+#ifndef HIRE_UMMA_CONV_GROUPS
+#define HIRE_UMMA_CONV_GROUPS 3
+#endif
+#ifndef HIRE_UMMA_EPI_GROUPS
+#define HIRE_UMMA_EPI_GROUPS 2
+#endif
+// converter warpgroups; group g converts chunks [g*8/G, (g+1)*8/G) of every stage
+constexpr int kUmmaConvGroups = HIRE_UMMA_CONV_GROUPS;
 constexpr int kUmmaConvWarps = 4 * kUmmaConvGroups;
-constexpr int kUmmaEpiWarp = kUmmaConvWarps;            // warps +0..+3: epilogue
-constexpr int kUmmaTmaWarp = kUmmaConvWarps + 4;        // TMA producer
-constexpr int kUmmaMmaWarp = kUmmaConvWarps + 5;        // MMA issuers (+0..+3; +0 allocates TMEM)
+constexpr int kUmmaEpiGroups = HIRE_UMMA_EPI_GROUPS;    // epilogue warpgroups, alternate row blocks
+constexpr int kUmmaEpiWarp = kUmmaConvWarps;            // warps +0..+4E-1: epilogue
+constexpr int kUmmaTmaWarp = kUmmaEpiWarp + 4 * kUmmaEpiGroups;  // TMA producer
+constexpr int kUmmaMmaWarp = kUmmaTmaWarp + 1;          // MMA issuers (+0..+3; +0 allocates TMEM)
 constexpr int kUmmaMaxIssuers = 4;
-constexpr int kUmmaThreads = 32 * (kUmmaConvWarps + 5 + kUmmaMaxIssuers);
+constexpr int kUmmaThreads = 32 * (kUmmaMmaWarp + kUmmaMaxIssuers);
+static_assert(kUmmaEpiGroups == 1 || kUmmaEpiGroups == 2, "one accumulator pair per epilogue group");
 // One thread issues a tcgen05.mma about every 78 cycles whatever N is
 // (tools/probes/probe_umma_rate.cu), far from the tensor floor at N <= 32
 // (16 cycles): n_iss issuer warps each own whole stages (st % n_iss) and an
@@ -231,25 +240,28 @@ __global__ void __launch_bounds__(kUmmaThreads, 1) q4_score_umma(
     // may only touch TMEM lanes 32 (w % 4) ..; the kUmmaConvGroups
     // warpgroups split every stage's chunks so each SM sub-partition has
     // several converter warps to hide LDS / STTM latency.
-    constexpr int kCpg = kUmmaStageChunks / kUmmaConvGroups;  // chunks per group
+    constexpr int kCpg = (kUmmaStageChunks + kUmmaConvGroups - 1) / kUmmaConvGroups;  // max chunks per group
     const int wl = warp & 3, grp = warp >> 2;
+    const int c0 = grp * kUmmaStageChunks / kUmmaConvGroups, c1 = (grp + 1) * kUmmaStageChunks / kUmmaConvGroups;
     const uint32_t lane_off = static_cast<uint32_t>(32 * wl) << 16;
     int slot = 0, sphase = 0, ab = 0, aphase = 0, ait = 0;
     for (int64_t rb = blockIdx.x; rb < n_rb; rb += gridDim.x) {
       for (int st = 0; st < n_st; ++st, ++ait) {
         mbar_wait(&full[slot], sphase);
         const uint4* src = reinterpret_cast<const uint4*>(ring + static_cast<size_t>(slot) * kUmmaStageBytes) +
-                           (grp * kCpg * kUmmaRows + 32 * wl + lane);
+                           (c0 * kUmmaRows + 32 * wl + lane);
         uint4 v[kCpg];
 #pragma unroll
-        for (int c = 0; c < kCpg; ++c) v[c] = src[c * kUmmaRows];
+        for (int c = 0; c < kCpg; ++c)
+          if (c0 + c < c1) v[c] = src[c * kUmmaRows];
         umma::mbar_arrive(&empty[slot]);  // the slot's bytes are in registers
         if (++slot == stages) { slot = 0; sphase ^= 1; }
         if (ait >= kUmmaABufs) mbar_wait(&aempty[ab], aphase ^ 1);
         umma::fence_after();
-        const uint32_t acol = tmem + lane_off + kColA + ab * 64 + 8 * kCpg * grp;
+        const uint32_t acol = tmem + lane_off + kColA + ab * 64 + 8 * c0;
 #pragma unroll
         for (int c = 0; c < kCpg; ++c) {
+          if (c0 + c >= c1) break;
           const uint32_t w4[4] = {v[c].x, v[c].y, v[c].z, v[c].w};
           uint32_t r[8];
 #pragma unroll
@@ -266,13 +278,18 @@ __global__ void __launch_bounds__(kUmmaThreads, 1) q4_score_umma(
       }
     }
   } else {
-    // ===== epilogue (warps 4-7; warp w reads TMEM lanes 32 (w % 4) ..):
-    // accumulators -> scale, phi -> scores [q][row]
+    // ===== epilogue (warp w reads TMEM lanes 32 (w % 4) ..): accumulators
+    // -> scale, phi -> scores [q][row]. With two warpgroups, group eg takes
+    // the row blocks rbi % 2 == eg, i.e. accumulator buffer db = eg.
     griddep_wait();  // scores / sx / sum(xq) of this call: after the producer grids
-    const int ew = warp - kUmmaEpiWarp;
+    const int ew = (warp - kUmmaEpiWarp) & 3, eg = (warp - kUmmaEpiWarp) >> 2;
     const uint32_t lane_off = static_cast<uint32_t>(32 * ew) << 16;
+    // per-query constants in registers (lane l: queries l, l + 32)
+    const int s8a = lane < nb ? 8 * sumxq[lane] : 0, s8b = lane + 32 < nb ? 8 * sumxq[lane + 32] : 0;
+    const float sxa = lane < nb ? sx[lane] : 0.0f, sxb = lane + 32 < nb ? sx[lane + 32] : 0.0f;
     int rbi = 0;
     for (int64_t rb = blockIdx.x; rb < n_rb; rb += gridDim.x, ++rbi) {
+      if (rbi % kUmmaEpiGroups != eg) continue;
       const int db = rbi & 1;
       mbar_wait(&dfull[db], (rbi >> 1) & 1);
       umma::fence_after();
@@ -293,16 +310,16 @@ __global__ void __launch_bounds__(kUmmaThreads, 1) q4_score_umma(
           umma::fence_before();
           umma::mbar_arrive(&dempty[db]);
         }
-        if (row < rows) {
 #pragma unroll
-          for (int j = 0; j < 16; ++j) {
-            const int q = q0 + j;
-            if (q < nb) {
-              const int aint = static_cast<int>(acc[j]) - 8 * sumxq[q];
-              const float cs = __fmul_rn(sc, sx[q]);
-              scores[static_cast<int64_t>(q) * score_stride + row] =
-                  apply_phi(phi, __fmul_rn(static_cast<float>(aint), cs));
-            }
+        for (int j = 0; j < 16; ++j) {
+          const int q = q0 + j;
+          const int s8q = __shfl_sync(0xffffffffu, q < 32 ? s8a : s8b, q & 31);
+          const float sxq = __shfl_sync(0xffffffffu, q < 32 ? sxa : sxb, q & 31);
+          if (q < nb && row < rows) {
+            const int aint = static_cast<int>(acc[j]) - s8q;
+            const float cs = __fmul_rn(sc, sxq);
+            scores[static_cast<int64_t>(q) * score_stride + row] =
+                apply_phi(phi, __fmul_rn(static_cast<float>(aint), cs));
           }
         }
       }
