@@ -68,12 +68,37 @@ __global__ void __launch_bounds__(256, (CPL >= 16 ? 1 : 2)) recompute_fast(
   __syncthreads();
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int64_t pitch_vec = static_cast<int64_t>(d) / E;  // 16-byte vectors per row
-  for (int i = blockIdx.x * 8 + wid; i < n_cand; i += gridDim.x * 8) {
+  // long rows (CPL >= 16, one CTA/SM): the next row's loads are issued
+  // before this row's arithmetic (two rows in flight per warp); the
+  // arithmetic per lane is unchanged (same chunks, same fmaf order)
+  constexpr bool kPrefetch = CPL >= 16;
+  const int step = gridDim.x * 8;
+  auto row_ptr = [&](int i) {
     const int64_t row = cand ? cand[b * cand_stride + i] : i;
-    const uint4* rp = reinterpret_cast<const uint4*>(w) + row * pitch_vec;
-    uint4 v[CPL];
+    return reinterpret_cast<const uint4*>(w) + row * pitch_vec;
+  };
+  uint4 nv[kPrefetch ? CPL : 1];
+  if (kPrefetch && blockIdx.x * 8 + wid < n_cand) {
+    const uint4* rp = row_ptr(blockIdx.x * 8 + wid);
 #pragma unroll
-    for (int c = 0; c < CPL; ++c) v[c] = ldg_stream(rp + lane + 32 * c);
+    for (int c = 0; c < (kPrefetch ? CPL : 1); ++c) nv[c] = ldg_stream(rp + lane + 32 * c);
+  }
+#pragma unroll 1
+  for (int i = blockIdx.x * 8 + wid; i < n_cand; i += step) {
+    uint4 v[CPL];
+    if constexpr (kPrefetch) {
+#pragma unroll
+      for (int c = 0; c < CPL; ++c) v[c] = nv[(kPrefetch ? c : 0)];
+      if (i + step < n_cand) {
+        const uint4* rn = row_ptr(i + step);
+#pragma unroll
+        for (int c = 0; c < (kPrefetch ? CPL : 1); ++c) nv[c] = ldg_stream(rn + lane + 32 * c);
+      }
+    } else {
+      const uint4* rp = row_ptr(i);
+#pragma unroll
+      for (int c = 0; c < CPL; ++c) v[c] = ldg_stream(rp + lane + 32 * c);
+    }
     float acc = 0.0f;
 #pragma unroll
     for (int c = 0; c < CPL; ++c) {
