@@ -85,6 +85,11 @@ typedef struct {
 
 HIRE_API const char* hire_last_error(void);
 HIRE_API int hire_abi_version(void);
+/* 1 when the library was built with -DHIRE_EXPERIMENTS=1: the measured
+ * negative-result kernels (single-launch FFN layer, bulk-copy recompute
+ * ring, cluster / shared-memory selectors, post-proxy single launch) are
+ * then selectable through their environment switches; 0 in the product. */
+HIRE_API int hire_experiments_built(void);
 
 /* ---- context: device, stream, workspace -------------------------------- */
 /* own_stream = 1: the context creates (and owns) a non-blocking stream and

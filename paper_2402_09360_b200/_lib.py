@@ -22,7 +22,7 @@ STAGES = ["proxy", "select", "recompute", "final", "down", "comm", "prep_x", "ff
 
 # Every symbol include/hire_cuda.h declares (checked by tests/test_lib_symbols.py).
 EXPORTS = [
-    "hire_last_error", "hire_abi_version",
+    "hire_last_error", "hire_abi_version", "hire_experiments_built",
     "hire_ctx_create", "hire_ctx_destroy", "hire_ctx_stream", "hire_ctx_synchronize",
     "hire_ctx_launch_count", "hire_ctx_set_profiling", "hire_ctx_profile_read", "hire_ctx_read_trace", "hire_debug_ktrace",
     "hire_device_alloc", "hire_device_free", "hire_copy",
@@ -71,6 +71,8 @@ def _sig(L):
     L.hire_last_error.restype = C.c_char_p
     L.hire_last_error.argtypes = []
     L.hire_abi_version.restype = _i32
+    L.hire_experiments_built.restype = _i32
+    L.hire_experiments_built.argtypes = []
     L.hire_ctx_launch_count.restype = _i64
     L.hire_ctx_launch_count.argtypes = [_vp]
     sigs = {

@@ -4,6 +4,13 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+// Kernels kept only as measured negative results (DESIGN.md "What B200
+// taught this design") are compiled in with -DHIRE_EXPERIMENTS=1; the
+// product library leaves them out.
+#ifndef HIRE_EXPERIMENTS
+#define HIRE_EXPERIMENTS 0
+#endif
+
 namespace hire_dev {
 
 constexpr int kWarp = 32;

@@ -113,6 +113,7 @@ __global__ void __launch_bounds__(256, (CPL >= 16 ? 1 : 2)) recompute_fast(
   }
 }
 
+#if HIRE_EXPERIMENTS
 // Same arithmetic as recompute_fast (lane chunk order, fmaf order, fixed
 // butterfly -> bit-identical values), but the gathered rows are moved by
 // the bulk-copy engine into shared memory (cp.async.bulk + mbarrier), so the
@@ -213,6 +214,7 @@ __global__ void __launch_bounds__(128, 1) recompute_tma(
     }
   }
 }
+#endif  // HIRE_EXPERIMENTS
 
 // strict / generic: one thread per row; any d.
 template <typename T>

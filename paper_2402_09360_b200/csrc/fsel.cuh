@@ -615,6 +615,7 @@ __global__ void __launch_bounds__(kFinThreads) sel_fin_kernel(
                   reinterpret_cast<unsigned*>(fin_smem));
 }
 
+#if HIRE_EXPERIMENTS
 // ---------------------------------------------------------------------
 // One launch for everything after the fused proxy kernel (hire_topk):
 //   CTAs [0, B)   : the finisher of query b (fin_select_emit), then flag[b]
@@ -765,5 +766,7 @@ __global__ void __launch_bounds__(kFinThreads, 1) fsel_post_kernel(
     __syncthreads();  // s_x / s_sel reuse
   }
 }
+
+#endif  // HIRE_EXPERIMENTS
 
 }  // namespace hire_dev

@@ -27,7 +27,9 @@
 #include "../../include/hire_cuda.h"
 #include "common.cuh"
 #include "exact.cuh"
+#if HIRE_EXPERIMENTS
 #include "ffn_fused.cuh"
+#endif
 #include "score.cuh"
 #include "select.cuh"
 #include "select2.cuh"
@@ -339,7 +341,7 @@ int max_blocks(K kernel, int threads, size_t smem) {
 
 // ----------------------------------------------------- selection policy --
 // context counter buffer: fused-kernel barriers, per-query counters, trace
-constexpr int kQcntOff = hire_dev::kCntInts;
+constexpr int kQcntOff = 8 * 16 * 32;  // the fused FFN kernel's barrier counters (ffn_fused.cuh kCntInts)
 constexpr int kTraceOff = kQcntOff + 64;
 constexpr int kCtxCounterInts = kTraceOff + 128;
 
@@ -451,6 +453,7 @@ int run_select(hire_ctx ctx, const float* scores, int64_t score_stride, int64_t 
   StageScope scope(ctx, kStageSelect);
   if (sp.mode == 2) {
     const uint32_t nn = static_cast<uint32_t>(n), K = static_cast<uint32_t>(sp.k_eff);
+#if HIRE_EXPERIMENTS
     // opt-in: one thread-block cluster per query (select2.cuh
     // sel_cluster_kernel). Measured slower than the paths below on B200
     // (a cluster barrier per pass costs more than the counting it splits).
@@ -466,6 +469,7 @@ int run_select(hire_ctx ctx, const float* scores, int64_t score_stride, int64_t 
       HIRE_SC(256, 4) HIRE_SC(256, 8) HIRE_SC(256, 16) HIRE_SC(512, 16) HIRE_SC(512, 32)
 #undef HIRE_SC
     }
+#endif
     if (n <= kSel2Exact) {
       // fewer warps per CTA: the per-pass cost of the order statistic is
       // per-warp overhead, the key counting is cheap
@@ -486,6 +490,7 @@ int run_select(hire_ctx ctx, const float* scores, int64_t score_stride, int64_t 
       CK(cudaGetLastError());
       return HIRE_OK;
     }
+#if HIRE_EXPERIMENTS
     static const bool smem_sel = std::getenv("HIRE_SEL_SMEM") != nullptr;
     if (n <= kSmemRowMax && smem_sel) {
       // opt-in: one CTA per query with the row in shared memory (measured
@@ -495,6 +500,7 @@ int run_select(hire_ctx ctx, const float* scores, int64_t score_stride, int64_t 
       CK(cudaGetLastError());
       return HIRE_OK;
     }
+#endif
     const char* nolist = std::getenv("HIRE_SEL_NOLIST");
     if (!(nolist && nolist[0] == '1') && n <= hire_dev::kFinMaxRows && K <= static_cast<uint32_t>(hire_dev::kFinCap)) {
       // list path: sampled exact lower bound -> every key >= lo appended to
@@ -886,6 +892,7 @@ int launch_recompute_fast(hire_ctx ctx, const void* w, int d, const uint32_t* ca
   return HIRE_OK;
 }
 
+#if HIRE_EXPERIMENTS
 // Bulk-copy ring variant (exact.cuh recompute_tma); *done = false when the
 // rows do not fit two groups of slots.
 template <typename T, int G>
@@ -924,6 +931,8 @@ int launch_recompute_tma(hire_ctx ctx, const void* w, int d, const uint32_t* can
 }
 
 // phi(<W_row, x_b>) for rows cand[b][i] (or i when cand == nullptr).
+#endif
+
 int run_recompute(hire_ctx ctx, const hire_matrix_s* m, const uint32_t* cand, int64_t cand_stride,
                   int64_t n_cand, const float* x, int64_t B, int phi, int strict, float* out,
                   int64_t out_stride) {
@@ -932,6 +941,7 @@ int run_recompute(hire_ctx ctx, const hire_matrix_s* m, const uint32_t* cand, in
   const int d = static_cast<int>(m->d);
   const size_t es = dtype_size(m->dtype);
   const int64_t bytes = static_cast<int64_t>(d) * static_cast<int64_t>(es);
+#if HIRE_EXPERIMENTS
   // bulk-copy ring: opt-in (HIRE_RECOMPUTE_TMA=1). Measured on B200 the
   // register path is faster at every batch (cfg3 B=8: 8.0 vs 12.6 us, B=32:
   // 23 vs 46 us; cfg4: 61 vs 63 us)
@@ -944,6 +954,7 @@ int run_recompute(hire_ctx ctx, const hire_matrix_s* m, const uint32_t* cand, in
       RET(launch_recompute_tma<float>(ctx, m->ptr, d, cand, cand_stride, n_cand, x, B, phi, out, out_stride, &done));
     if (done) return HIRE_OK;
   }
+#endif
   if (!strict && bytes % 512 == 0) {
     const int cpl = static_cast<int>(bytes / 512);
     const bool bf = m->dtype == HIRE_BF16;
@@ -1318,6 +1329,10 @@ struct FselPost {
 bool fsel_post_ok(const hire_matrix_s* w, const hire_topk_params* p, const SelPlan& sp, int64_t B, int num_sms) {
   // opt-in (HIRE_FSEL_POST=1): measured slower than fin -> K4 -> K5 on B200
   // (the recompute workers are latency-bound at 1024 threads / 64 registers)
+#if !HIRE_EXPERIMENTS
+  (void)w; (void)p; (void)sp; (void)B; (void)num_sms;
+  return false;
+#else
   const char* e = std::getenv("HIRE_FSEL_POST");
   if (!e || e[0] != '1' || p->strict) return false;
   const int64_t es = w->dtype == HIRE_BF16 ? 2 : 4;
@@ -1327,8 +1342,10 @@ bool fsel_post_ok(const hire_matrix_s* w, const hire_topk_params* p, const SelPl
   if (cpl != 4 && cpl != 8 && cpl != 16) return false;
   if (p->k > kPostMaxK || sp.k_eff > kFinCap || w->d * 4 > 64 * 1024) return false;
   return B + 8 <= num_sms;
+#endif
 }
 
+#if HIRE_EXPERIMENTS
 template <typename T, int CPL>
 int launch_post_t(hire_ctx ctx, const float* scores, int64_t stride, const FuseSel& fs, uint32_t* cand,
                   int64_t cand_stride, int ordered, int* status, const void* w, int d, const float* x, int phi,
@@ -1344,6 +1361,7 @@ int launch_post_t(hire_ctx ctx, const float* scores, int64_t stride, const FuseS
               po.out_stride, post, R));
   return HIRE_OK;
 }
+#endif
 
 int run_scores_fsel(hire_ctx ctx, const hire_scorer_s* a, const float* x, int64_t B, int phi, const SelPlan& sp,
                     const TopkWs& t, uint32_t* cand, bool ordered, const FselPost* po = nullptr) {
@@ -1390,6 +1408,7 @@ int run_scores_fsel(hire_ctx ctx, const hire_scorer_s* a, const float* x, int64_
 #undef HIRE_FS
   }
   const size_t bm = static_cast<size_t>((a->rows + 31) / 32) * 4;
+#if HIRE_EXPERIMENTS
   if (po && po->w) {
     StageScope scope(ctx, kStageSelect);
     const hire_matrix_s* w = po->w;
@@ -1409,7 +1428,9 @@ int run_scores_fsel(hire_ctx ctx, const hire_scorer_s* a, const float* x, int64_
       if (cpl == 4) HIRE_PO(float, 4); else if (cpl == 8) HIRE_PO(float, 8); else HIRE_PO(float, 16);
     }
 #undef HIRE_PO
-  } else {
+  } else
+#endif
+  {
     StageScope scope(ctx, kStageSelect);
     CK(launch_k(ctx, sel_fin_kernel, static_cast<unsigned>(B), kFinThreads, bm, static_cast<const float*>(t.scores),
                 a->rows, fs, cand, sp.k_eff, ordered ? 1 : 0, t.status));
@@ -1522,6 +1543,10 @@ extern "C" {
 
 const char* hire_last_error(void) { return g_err.c_str(); }
 int hire_abi_version(void) { return HIRE_ABI_VERSION; }
+int hire_experiments_built(void) { return HIRE_EXPERIMENTS; }
+#if HIRE_EXPERIMENTS
+static_assert(kQcntOff >= hire_dev::kCntInts, "context counters overlap the fused FFN barriers");
+#endif
 
 int hire_ctx_create(int device, void* stream, int own_stream, hire_ctx* out) {
   if (!out) return invalid("null out");
@@ -1542,10 +1567,12 @@ int hire_ctx_create(int device, void* stream, int own_stream, hire_ctx* out) {
   // opt-in shared memory for the selectors
   CK(cudaFuncSetAttribute(select_candidates_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                           kPoolKeys * 8));
+#if HIRE_EXPERIMENTS
   for (const void* kf : {(const void*)sel_cluster_kernel<256, 4>, (const void*)sel_cluster_kernel<256, 8>,
                          (const void*)sel_cluster_kernel<256, 16>, (const void*)sel_cluster_kernel<512, 16>,
                          (const void*)sel_cluster_kernel<512, 32>})
     CK(cudaFuncSetAttribute(kf, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+#endif
   {
     const int f2 = kFinalMax * 8;
     CK(cudaFuncSetAttribute(final2_kernel<128, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, f2));
@@ -1563,7 +1590,9 @@ int hire_ctx_create(int device, void* stream, int own_stream, hire_ctx* out) {
   CK(cudaFuncSetAttribute(final_select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                           kFinalMax * 8));
   CK(cudaFuncSetAttribute(sel_fin_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kFinMaxRows / 8));
+#if HIRE_EXPERIMENTS
   CK(cudaFuncSetAttribute(sel_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemRowMax * 4));
+#endif
   CK(cudaFuncSetAttribute(bucket_topt_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                           kBucketMaxWidth * 8));
   // every other kernel with dynamic shared memory: allow up to 200 KB once,
@@ -2200,6 +2229,7 @@ void take_ffn_ws(Arena& ar, FfnWs* fw, const hire_scorer_s* a, int64_t B, int64_
 }  // extern "C"
 
 namespace {
+#if HIRE_EXPERIMENTS
 template <typename T, int NT, int KS>
 int launch_ffn_fused_t(hire_ctx ctx, const FusedFfnArgs& args, size_t smem) {
   auto k = ffn_fused_kernel<T, NT, KS>;
@@ -2246,8 +2276,14 @@ int launch_ffn_fused_nt(hire_ctx ctx, const FusedFfnArgs& args, size_t smem, int
 
 // One cooperative launch for the whole layer (ffn_fused.cuh) when the shape
 // allows it; returns 1 (not taken) otherwise.
+#endif
+
 int try_ffn_fused(hire_ctx ctx, const hire_matrix_s* u, const hire_matrix_s* v, hire_scorer_s* a,
                   const float* x, int64_t B, const hire_ffn_params* p, uint32_t* sel, float* out) {
+#if !HIRE_EXPERIMENTS
+  (void)ctx; (void)u; (void)v; (void)a; (void)x; (void)B; (void)p; (void)sel; (void)out;
+  return 1;  // the kernel chain (the single-launch layer is an experiments-build kernel)
+#else
   if (!ctx->ffn_fused || p->group_size != 1 || p->x_mode != HIRE_X_INT8 || p->strict) return 1;
   if (a->kind != HIRE_SCORER_Q4 || B < 1 || B > 16 || u->d % 64 != 0 || u->d > 8192) return 1;
   if (u->rows > 16384 || p->k_prime > u->rows || p->k > p->k_prime) return 1;
@@ -2303,6 +2339,7 @@ int try_ffn_fused(hire_ctx ctx, const hire_matrix_s* u, const hire_matrix_s* v, 
   StageScope scope(ctx, kStageFused);
   if (u->dtype == HIRE_BF16) return launch_ffn_fused_nt<__nv_bfloat16>(ctx, args, smem, nt, ks);
   return launch_ffn_fused_nt<float>(ctx, args, smem, nt, ks);
+#endif
 }
 }  // namespace
 

@@ -498,6 +498,7 @@ __global__ void __launch_bounds__(NT) sel_exact_kernel(
     if (src.k[j] >= T) out[pos++] = i0 + j;
 }
 
+#if HIRE_EXPERIMENTS
 // ---------------------------------------------------------------------
 // Mid-size rows (kSel2Exact < n <= kSmemRowMax): one 1024-thread CTA per
 // query holds the whole score row in shared memory; T = the K-th largest
@@ -551,6 +552,8 @@ __global__ void __launch_bounds__(1024, 1) sel_smem_kernel(
     pos += __popc(bal);
   }
 }
+
+#endif  // HIRE_EXPERIMENTS
 
 // ---------------------------------------------------------------------
 // S1 (large rows). One 128-thread CTA per query: 2048 sampled keys (512
@@ -1198,6 +1201,7 @@ namespace hire_dev {
 // the same decision. The <= 32 survivors are ranked by every CTA from the
 // cluster's lists; the ordered emit takes its offset from the lower ranks'
 // counts. Rows up to CS * NT * KPT keys in one launch, no global atomics.
+#if HIRE_EXPERIMENTS
 // ---------------------------------------------------------------------
 __device__ __forceinline__ void cluster_sync_all() {
   asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
@@ -1463,5 +1467,7 @@ __global__ void __launch_bounds__(NT) sel_cluster_kernel(const float* __restrict
     if (src.k[j] && src.k[j] >= T) out[pos++] = first + i0 + j;
   cluster_sync_all();  // no CTA leaves while its shared memory may still be read
 }
+
+#endif  // HIRE_EXPERIMENTS
 
 }  // namespace hire_dev
