@@ -514,6 +514,7 @@ int run_select(hire_ctx ctx, const float* scores, int64_t score_stride, int64_t 
       uint64_t* piv = surv;                                              // [B][4]
       uint64_t* lists = surv + 5 * B + B * kWinBins * kWinGroups / 2;    // [B][kFinCap] (>= B x 65536 words)
       fs.lists = lists;
+      // (32 instead of 8 CTAs per SM over the batch: measured the same)
       const int64_t CL = std::max<int64_t>(1, std::min<int64_t>(ceil_div(n, kWinThreads * kScanBatch),
                                                                 std::max<int64_t>(1, 8 * ctx->num_sms / B)));
       const uint32_t perm = sample_perm(static_cast<uint64_t>(n) / 4);

@@ -115,6 +115,39 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, i
       "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
       : "memory");
 }
+// L2 policies (HIRE_UMMA_L2 != 0): the weight stream is read once per call
+// (evict first), the score rows are read again right away by the selector
+// (evict last) — 263 MB of weights would otherwise push the 1 MB-per-query
+// scores out of the 126 MB L2 before the selector reads them.
+#ifndef HIRE_UMMA_L2
+#define HIRE_UMMA_L2 1
+#endif
+__device__ __forceinline__ uint64_t l2_policy_evict_first() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ uint64_t l2_policy_evict_normal() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ uint64_t l2_policy_evict_last() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ void tma_load_2d_hint(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar,
+                                                 uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1, {%2, %3}], "
+      "[%4], %5;" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar)), "l"(pol)
+      : "memory");
+}
+__device__ __forceinline__ void st_hint_f32(float* p, float v, uint64_t pol) {
+  asm volatile("st.global.L2::cache_hint.f32 [%0], %1, %2;" ::"l"(p), "f"(v), "l"(pol) : "memory");
+}
 __device__ __forceinline__ void tma_prefetch_desc(const CUtensorMap* map) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
 }
@@ -185,12 +218,19 @@ __global__ void __launch_bounds__(kUmmaThreads, 1) q4_score_umma(
     // ===== TMA producer: weights are read-only, so it streams before the
     // programmatic-dependency wait (independent prologue)
     if (lane == 0) {
+      const uint64_t pol_w = l2_policy_evict_first();
+      (void)pol_w;
       int it = 0;
       for (int64_t rb = blockIdx.x; rb < n_rb; rb += gridDim.x)
         for (int st = 0; st < n_st; ++st, ++it) {
           const int slot = it % stages;
           if (it >= stages) mbar_wait(&empty[slot], ((it / stages) - 1) & 1);
           mbar_arrive_expect_tx(&full[slot], kUmmaStageBytes);
+#if HIRE_UMMA_L2
+          tma_load_2d_hint(ring + static_cast<size_t>(slot) * kUmmaStageBytes, &wmap, 0,
+                           static_cast<int>(rb * nkc + st * kUmmaStageChunks), &full[slot], pol_w);
+          continue;
+#endif
           tma_load_2d(ring + static_cast<size_t>(slot) * kUmmaStageBytes, &wmap, 0,
                       static_cast<int>(rb * nkc + st * kUmmaStageChunks), &full[slot]);
         }
@@ -287,6 +327,10 @@ __global__ void __launch_bounds__(kUmmaThreads, 1) q4_score_umma(
     // per-query constants in registers (lane l: queries l, l + 32)
     const int s8a = lane < nb ? 8 * sumxq[lane] : 0, s8b = lane + 32 < nb ? 8 * sumxq[lane + 32] : 0;
     const float sxa = lane < nb ? sx[lane] : 0.0f, sxb = lane + 32 < nb ? sx[lane + 32] : 0.0f;
+    // scores kept in L2 for the selector up to 32 queries (32 MB at V=256000);
+    // beyond, evict-last rows would crowd each other out
+    const uint64_t pol_s = nb <= 32 ? l2_policy_evict_last() : l2_policy_evict_normal();
+    (void)pol_s;
     int rbi = 0;
     for (int64_t rb = blockIdx.x; rb < n_rb; rb += gridDim.x, ++rbi) {
       if (rbi % kUmmaEpiGroups != eg) continue;
@@ -318,8 +362,12 @@ __global__ void __launch_bounds__(kUmmaThreads, 1) q4_score_umma(
           if (q < nb && row < rows) {
             const int aint = static_cast<int>(acc[j]) - s8q;
             const float cs = __fmul_rn(sc, sxq);
-            scores[static_cast<int64_t>(q) * score_stride + row] =
-                apply_phi(phi, __fmul_rn(static_cast<float>(aint), cs));
+            const float v = apply_phi(phi, __fmul_rn(static_cast<float>(aint), cs));
+#if HIRE_UMMA_L2
+            st_hint_f32(scores + static_cast<int64_t>(q) * score_stride + row, v, pol_s);
+#else
+            scores[static_cast<int64_t>(q) * score_stride + row] = v;
+#endif
           }
         }
       }
