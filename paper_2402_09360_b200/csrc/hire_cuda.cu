@@ -20,6 +20,7 @@
 #include <cstdio>
 #include <cstring>
 #include <cstdlib>
+#include <memory>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -98,11 +99,24 @@ struct hire_ctx_s {
   // host-buffer calls (*_host): after one eager call per shape, the whole
   // call — H2D copy, kernel chain, D2H copy — replays as one CUDA graph on
   // gstream. An entry is valid while every buffer it captured is unchanged.
+  // The input-fetch kernel node of a captured call: its source pointer is
+  // rewritten per call (the caller's own pinned buffer when it has a device
+  // alias, else the context's staging buffer), so one graph serves every
+  // input buffer. Heap-allocated: kernelParams points into it.
+  struct FetchNode {
+    cudaGraphNode_t node = nullptr;
+    cudaKernelNodeParams params{};
+    const void* src = nullptr;
+    void* dst = nullptr;
+    int64_t n16 = 0;
+    void* args[3] = {nullptr, nullptr, nullptr};
+  };
   struct HostGraph {
     std::vector<int64_t> key;
     std::vector<const void*> bufs;
     cudaGraphExec_t exec = nullptr;
     int64_t out[4] = {0, 0, 0, 0};
+    std::shared_ptr<FetchNode> fetch;
   };
   static constexpr size_t kMaxHostGraphs = 64;
   std::vector<HostGraph> hgraphs;  // least recently used first
@@ -1464,7 +1478,8 @@ namespace {
 // instantiated, launched. Later: launched. The caller synchronises.
 // *done_on = the stream the caller synchronises on.
 template <class Body>
-int run_host_graph(hire_ctx ctx, const std::vector<int64_t>& key, int64_t* out, cudaStream_t* done_on, Body body) {
+int run_host_graph(hire_ctx ctx, const std::vector<int64_t>& key, int64_t* out, cudaStream_t* done_on,
+                   const void* fetch_src, Body body) {
   *done_on = ctx->stream;
   if (!ctx->host_graphs || ctx->prof) return body(out);
   const auto bufs = ctx->buf_snapshot();
@@ -1479,6 +1494,10 @@ int run_host_graph(hire_ctx ctx, const std::vector<int64_t>& key, int64_t* out, 
         cudaGetLastError();
         CK(cudaEventRecord(ctx->gev, ctx->stream));
         CK(cudaStreamWaitEvent(ctx->gstream, ctx->gev, 0));
+      }
+      if (g.fetch && g.fetch->src != fetch_src) {  // this call's input buffer
+        g.fetch->src = fetch_src;
+        CK(cudaGraphExecKernelNodeSetParams(g.exec, g.fetch->node, &g.fetch->params));
       }
       CK(cudaGraphLaunch(g.exec, ctx->gstream));
       *done_on = ctx->gstream;  // the host call blocks on it: no event back
@@ -1524,6 +1543,34 @@ int run_host_graph(hire_ctx ctx, const std::vector<int64_t>& key, int64_t* out, 
     ctx->host_graphs = ec == cudaSuccess;
     return body(out);
   }
+  // the input-fetch node (first fetch_host_kernel node), if any
+  std::shared_ptr<hire_ctx_s::FetchNode> fetch;
+  {
+    size_t nn = 0;
+    if (cudaGraphGetNodes(graph, nullptr, &nn) == cudaSuccess && nn > 0) {
+      std::vector<cudaGraphNode_t> nodes(nn);
+      if (cudaGraphGetNodes(graph, nodes.data(), &nn) == cudaSuccess)
+        for (size_t i = 0; i < nn && !fetch; ++i) {
+          cudaGraphNodeType ty;
+          cudaKernelNodeParams kp{};
+          if (cudaGraphNodeGetType(nodes[i], &ty) != cudaSuccess || ty != cudaGraphNodeTypeKernel) continue;
+          if (cudaGraphKernelNodeGetParams(nodes[i], &kp) != cudaSuccess) continue;
+          if (kp.func != reinterpret_cast<void*>(fetch_host_kernel)) continue;
+          fetch = std::make_shared<hire_ctx_s::FetchNode>();
+          fetch->node = nodes[i];
+          fetch->params = kp;
+          fetch->src = *static_cast<const void* const*>(kp.kernelParams[0]);
+          fetch->dst = *static_cast<void* const*>(kp.kernelParams[1]);
+          fetch->n16 = *static_cast<const int64_t*>(kp.kernelParams[2]);
+          fetch->args[0] = &fetch->src;
+          fetch->args[1] = &fetch->dst;
+          fetch->args[2] = &fetch->n16;
+          fetch->params.kernelParams = fetch->args;
+          fetch->params.extra = nullptr;
+        }
+    }
+    cudaGetLastError();
+  }
   cudaGraphExec_t exec = nullptr;
   const cudaError_t ei = cudaGraphInstantiate(&exec, graph, 0);
   cudaGraphDestroy(graph);
@@ -1532,7 +1579,7 @@ int run_host_graph(hire_ctx ctx, const std::vector<int64_t>& key, int64_t* out, 
     cudaGraphExecDestroy(ctx->hgraphs.front().exec);
     ctx->hgraphs.erase(ctx->hgraphs.begin());
   }
-  ctx->hgraphs.push_back({key, bufs, exec, {out[0], out[1], out[2], out[3]}});
+  ctx->hgraphs.push_back({key, bufs, exec, {out[0], out[1], out[2], out[3]}, fetch});
   CK(cudaGraphLaunch(exec, ctx->gstream));
   *done_on = ctx->gstream;
   return HIRE_OK;
@@ -2097,17 +2144,21 @@ int hire_topk_host(hire_ctx ctx, hire_matrix w, hire_scorer a, const float* x_ho
   RET(ensure_host(&ctx->io_host, &ctx->io_host_cap, in_bytes + out_bytes, ctx->stream));
   char* dv = static_cast<char*>(ctx->io_dev);
   char* hs = static_cast<char*>(ctx->io_host);
-  // the input is staged into the context's mapped buffer (the graph reads it
-  // from there); results are written into the same mapped buffer and copied
+  // the input: read in place when the caller's buffer is pinned (the graph's
+  // fetch node is pointed at it per call), else staged into the context's
+  // mapped buffer; results are written into the mapped buffer and copied
   // out after the synchronise
-  std::memcpy(hs, x_host, xb);
+  const void* xa = host_alias(x_host, xb);
+  if (!xa) std::memcpy(hs, x_host, xb);
+  const void* xsrc = xa ? static_cast<const void*>(x_host) : hs;
+  const void* xdev = xa ? xa : host_alias(hs, align_up(xb));
   const std::vector<int64_t> key = {1, static_cast<int64_t>(w->uid), static_cast<int64_t>(a->uid), B, p->k, p->k_prime,
                                     p->phi, p->x_mode, p->select, p->strict, p->n_buckets, p->bucket_t,
                                     cb ? 1 : 0, pb ? 1 : 0};
   int64_t res[4];
   cudaStream_t done_on = nullptr;
-  RET(run_host_graph(ctx, key, res, &done_on, [&](int64_t* r) -> int {
-    RET(fetch_inputs(ctx, dv, hs, xb));
+  RET(run_host_graph(ctx, key, res, &done_on, xdev, [&](int64_t* r) -> int {
+    RET(fetch_inputs(ctx, dv, xsrc, xb));
     char* o = hs + in_bytes;  // results are written straight into mapped host memory
     uint32_t* dcand = cb ? reinterpret_cast<uint32_t*>(o) : nullptr;
     o += align_up(cb);
@@ -2386,7 +2437,11 @@ int hire_ffn_host(hire_ctx ctx, hire_matrix u, hire_matrix v, hire_scorer a, con
   // would be re-captured for each new buffer
   void* od = host_alias(out_host, ob);
   void* sd = sel_host ? host_alias(sel_host, sb) : nullptr;
-  std::memcpy(hs, x_host, xb);
+  // the input: in place when pinned (the fetch node follows it per call), else staged
+  const void* xa = host_alias(x_host, xb);
+  if (!xa) std::memcpy(hs, x_host, xb);
+  const void* xsrc = xa ? static_cast<const void*>(x_host) : hs;
+  const void* xdev = xa ? xa : host_alias(hs, align_up(xb));
   // the output rows are written straight into mapped host memory; the unit
   // ids stay on the device (the down-projection reads them) and are stored
   // to the host by a small kernel at the end
@@ -2399,8 +2454,8 @@ int hire_ffn_host(hire_ctx ctx, hire_matrix u, hire_matrix v, hire_scorer a, con
                                     reinterpret_cast<int64_t>(sd), sel_host ? 1 : 0};
   int64_t res[4];
   cudaStream_t done_on = nullptr;
-  RET(run_host_graph(ctx, key, res, &done_on, [&](int64_t*) -> int {
-    RET(fetch_inputs(ctx, dv, hs, xb));
+  RET(run_host_graph(ctx, key, res, &done_on, xdev, [&](int64_t*) -> int {
+    RET(fetch_inputs(ctx, dv, xsrc, xb));
     RET(hire_ffn_run(ctx, u, v, a, reinterpret_cast<const float*>(dv), B, p, dsel, dout));
     if (sel_host) {
       if (sb % 16 == 0) {

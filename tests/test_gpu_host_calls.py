@@ -77,3 +77,42 @@ def test_ffn_host_replays_equal_device_path(H, O, monkeypatch):
             want, wsel = H.ffn_group_sparse(f, T(x), a, k, kp, x_mode=H.X_INT8)
             assert np.array_equal(sel, wsel.cpu().numpy().astype(np.uint32)), (graphs, it)
             assert np.array_equal(out.view(np.uint32), want.cpu().numpy().view(np.uint32)), (graphs, it)
+
+
+def test_host_calls_read_pinned_inputs_in_place(H, O):
+    """Pinned caller input buffers are read in place: the captured graph's
+    fetch node is re-pointed per call. Alternating pinned buffers, a pageable
+    one in between, and a recycled handle address must all give the
+    device-path results (no stale pointer in a replayed graph)."""
+    V, d, k, kp, B = 20000, 256, 16, 256, 3
+    w = _data.lowrank_plus_noise(V, d, 16, 7)
+    codes, scales = O.quantize_int4(w)
+    cfg = H.HireConfig(k=k, k_prime=kp, x_mode=H.X_INT8)
+    ctx = H.Context(0)
+    g = np.random.default_rng(3)
+    pins = [torch.empty(B, d, dtype=torch.float32).pin_memory().numpy() for _ in range(2)]
+    for rnd in range(2):  # a second round with fresh handles (addresses may be reused)
+        z = H.ScoreMatrix(T(w))
+        a = H.ApproxScorer.quantized(codes, scales)
+        for it in range(7):
+            x = pins[it % 2] if it != 4 else np.empty((B, d), np.float32)  # it 4: pageable
+            x[:] = (g.standard_normal((B, d)) / np.sqrt(d)).astype(np.float32)
+            cand, idx, val, prob, cl = _topk_host(H, ctx, z, a, x, cfg)
+            r = H.hire_topk(T(x), z, a, cfg)
+            assert np.array_equal(idx, r.top_idx.cpu().numpy().astype(np.uint32)), (rnd, it)
+            assert np.array_equal(val.view(np.uint32), r.top_val.cpu().numpy().view(np.uint32)), (rnd, it)
+        del z, a
+    m, kf, kpf = 2048, 102, 204
+    u, v = _data.ffn_family(m, d, 9, r=16)
+    f = H.GroupedFFN(H.ScoreMatrix(T(u)), H.ScoreMatrix(T(v)))
+    fa = H.ApproxScorer.quantize(f.u)
+    p = H._lib.FfnParams(kf, kpf, 1, 1, H.X_INT8, 0, 0)
+    for it in range(6):
+        x = pins[it % 2] if it != 3 else np.empty((B, d), np.float32)
+        x[:] = g.standard_normal((B, d)).astype(np.float32)
+        sel = np.zeros((B, kf), np.uint32)
+        out = np.zeros((B, d), np.float32)
+        H._lib.check(H.lib().hire_ffn_host(ctx.h, f.u.h, f.v.h, fa.h, x.ctypes.data_as(C.c_void_p), B, C.byref(p),
+                                           sel.ctypes.data_as(C.c_void_p), out.ctypes.data_as(C.c_void_p)))
+        want, wsel = H.ffn_group_sparse(f, T(x), fa, kf, kpf, x_mode=H.X_INT8)
+        assert np.array_equal(out.view(np.uint32), want.cpu().numpy().view(np.uint32)), it
