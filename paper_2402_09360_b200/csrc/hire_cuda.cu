@@ -104,12 +104,19 @@ struct hire_ctx_s {
   // alias, else the context's staging buffer), so one graph serves every
   // input buffer. Heap-allocated: kernelParams points into it.
   struct FetchNode {
+    cudaGraph_t graph = nullptr;  // kept alive: exec-node updates name the node of the source graph
     cudaGraphNode_t node = nullptr;
     cudaKernelNodeParams params{};
     const void* src = nullptr;
     void* dst = nullptr;
     int64_t n16 = 0;
     void* args[3] = {nullptr, nullptr, nullptr};
+    FetchNode() = default;
+    FetchNode(const FetchNode&) = delete;
+    FetchNode& operator=(const FetchNode&) = delete;
+    ~FetchNode() {
+      if (graph) cudaGraphDestroy(graph);
+    }
   };
   struct HostGraph {
     std::vector<int64_t> key;
@@ -1573,7 +1580,8 @@ int run_host_graph(hire_ctx ctx, const std::vector<int64_t>& key, int64_t* out, 
   }
   cudaGraphExec_t exec = nullptr;
   const cudaError_t ei = cudaGraphInstantiate(&exec, graph, 0);
-  cudaGraphDestroy(graph);
+  if (fetch && ei == cudaSuccess) fetch->graph = graph;  // owned by the cache entry from here
+  else cudaGraphDestroy(graph);
   CK(ei);
   if (ctx->hgraphs.size() >= hire_ctx_s::kMaxHostGraphs) {  // bounded: evict the least recently used
     cudaGraphExecDestroy(ctx->hgraphs.front().exec);

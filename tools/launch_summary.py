@@ -8,7 +8,9 @@ import collections
 import csv
 import sys
 
-ONE_TIME = ("quantize_q4_kernel", "q4_to_mma_layout")
+ONE_TIME = ("quantize_q4_kernel", "q4_to_mma_layout", "q4_to_umma_layout")
+OURS = ("q4_", "sel_", "recompute", "final", "prep_x", "lr_", "ffn_", "fetch_host", "add_offset", "bucket_",
+        "select_candidates", "gather_values", "group_", "expand_", "iota", "concat_sel", "sum_parts")
 
 
 def main(path):
@@ -18,7 +20,8 @@ def main(path):
     agg = collections.OrderedDict()
     for r in rows[1:]:
         name = r[ik]
-        if "hire_dev::" not in name and not name.startswith(("ffn_", "add_offset", "gather_values", "group_", "expand_", "iota")):
+        base = name.replace("void ", "").replace("hire_dev::", "")
+        if "hire_dev::" not in name and not base.startswith(OURS):
             continue
         if any(o in name for o in ONE_TIME):
             continue
