@@ -93,6 +93,8 @@ struct hire_ctx_s {
   bool trace = false;
   int* counters = nullptr;  // zeroed hand-off counters of the fused kernels
   unsigned* selc = nullptr;  // zeroed selection counters (select2.cuh qc / agg)
+  unsigned* tickets = nullptr;  // [B] S3 chunk tickets, zero at rest (the last claimer resets)
+  size_t tickets_cap = 0;
   size_t selc_cap = 0;
   void* fzero = nullptr;     // zero-at-rest sample slots + bounds of the fused selector (fsel.cuh)
   size_t fzero_cap = 0;
@@ -131,7 +133,7 @@ struct hire_ctx_s {
   bool host_graphs = true;
   cudaStream_t gstream = nullptr;
   cudaEvent_t gev = nullptr;
-  std::vector<const void*> buf_snapshot() const { return {ws, io_dev, io_host, selc, fzero, counters}; }
+  std::vector<const void*> buf_snapshot() const { return {ws, io_dev, io_host, selc, fzero, counters, tickets}; }
   // stage profiling (hire_ctx_set_profiling): event pairs around each stage
   bool prof = false;
   std::vector<cudaEvent_t> ev_pool;
@@ -313,6 +315,22 @@ int ensure_selc(hire_ctx ctx, size_t words) {
 
 // Zero-at-rest sample slots / bounds / list counts of the fused and list
 // selectors (fsel.cuh): [B][kFselSampleMax] samples, lo[B], cnt[B], ctr.
+// Per-query chunk tickets of the ordered emit (zero at rest; a separate
+// buffer: the selc regions move with the call shape)
+int ensure_tickets(hire_ctx ctx, int64_t B) {
+  if (static_cast<size_t>(B) <= ctx->tickets_cap) return HIRE_OK;
+  if (ctx->tickets) {
+    CK(cudaStreamSynchronize(ctx->stream));
+    CK(cudaFree(ctx->tickets));
+    ctx->tickets = nullptr;
+  }
+  const size_t n = std::max<size_t>(static_cast<size_t>(B), 256);
+  CK(cudaMalloc(&ctx->tickets, n * sizeof(unsigned)));
+  CK(cudaMemsetAsync(ctx->tickets, 0, n * sizeof(unsigned), ctx->stream));
+  ctx->tickets_cap = n;
+  return HIRE_OK;
+}
+
 int ensure_fzero(hire_ctx ctx, int64_t B) {
   const size_t need = static_cast<size_t>(B) * (hire_dev::kFselSampleMax + 2) * 8 + hire_dev::kFselCtr * 32 * 4 +
                       static_cast<size_t>(B) * 8;
@@ -366,7 +384,7 @@ constexpr int kQcntOff = 8 * 16 * 32;  // the fused FFN kernel's barrier counter
 constexpr int kTraceOff = kQcntOff + 64;
 constexpr int kCtxCounterInts = kTraceOff + 128;
 
-constexpr int64_t kSelGridChunks = 4 * 148;  // S2/S3 CTAs over a whole batch (co-resident)
+constexpr int64_t kSelGridChunks = 4 * 160;  // S2/S3 CTAs over a whole batch (workspace bound; 4 per SM used)
 
 struct SelPlan {
   int mode = 0;          // 0 direct, 1 bucket, 2 grid-wide pivot/window/emit (select2.cuh)
@@ -563,6 +581,7 @@ int run_select(hire_ctx ctx, const float* scores, int64_t score_stride, int64_t 
       return invalid("selection: batch too large for the grid-wide selector");
     const uint32_t seg = static_cast<uint32_t>(sp.wseg);
     RET(ensure_selc(ctx, static_cast<size_t>(B * 3 * C)));
+    RET(ensure_tickets(ctx, B));
     unsigned* cnt = ctx->selc;
     unsigned* agg = ctx->selc + B * 2 * C;
     uint64_t* piv = surv;                                        // [B][4]
@@ -580,7 +599,8 @@ int run_select(hire_ctx ctx, const float* scores, int64_t score_stride, int64_t 
                 static_cast<const unsigned*>(cnt), static_cast<const unsigned*>(gh),
                 static_cast<const uint64_t*>(lists), thr, status));
     CK(launch_k(ctx, sel_emit_kernel, dim3(static_cast<unsigned>(C), static_cast<unsigned>(B)), kEmitThreads, 0,
-                scores, score_stride, nn, static_cast<const uint64_t*>(thr), agg, cand, cand_stride));
+                scores, score_stride, nn, static_cast<const uint64_t*>(thr), agg, cand, cand_stride,
+                ctx->tickets));
     CK(cudaGetLastError());
     return HIRE_OK;
   }
@@ -1689,6 +1709,7 @@ int hire_ctx_destroy(hire_ctx c) {
   if (c->ws) cudaFree(c->ws);
   if (c->counters) cudaFree(c->counters);
   if (c->selc) cudaFree(c->selc);
+  if (c->tickets) cudaFree(c->tickets);
   if (c->fzero) cudaFree(c->fzero);
   if (c->io_dev) cudaFree(c->io_dev);
   if (c->io_host) cudaFreeHost(c->io_host);

@@ -967,8 +967,10 @@ __global__ void __launch_bounds__(kWselThreads) sel_wselect_kernel(
 // ---------------------------------------------------------------------
 // S3. grid (C, B), 256 threads. Ordered emit of keys >= thr[b]. Chunk c
 // publishes agg[b][c] = count | 0x80000000 (cleared by S2) and sums the
-// aggregates of chunks < c (decoupled look-back over aggregates only; the
-// grid is sized to be co-resident, so the waits always resolve). Each warp
+// aggregates of chunks < c (decoupled look-back over aggregates only). A
+// CTA's chunk id is a ticket (atomicAdd on ticket[b], zero at rest): lower
+// chunks belong to CTAs that started earlier, so the waits resolve whatever
+// the dispatch order or residency (MPS, green contexts, preemption). Each warp
 // owns a contiguous segment; loads are batched 8 groups of 32 per warp,
 // ballots kept in shared memory for the write pass.
 // ---------------------------------------------------------------------
@@ -977,15 +979,23 @@ constexpr int kEmitBallots = 4096;  // u32 ballots kept in smem (131072 keys)
 
 __global__ void __launch_bounds__(kEmitThreads) sel_emit_kernel(
     const float* __restrict__ scores, int64_t stride, uint32_t n, const uint64_t* __restrict__ thr,
-    unsigned* __restrict__ agg, uint32_t* __restrict__ cand, int64_t cand_stride) {
+    unsigned* __restrict__ agg, uint32_t* __restrict__ cand, int64_t cand_stride, unsigned* __restrict__ ticket) {
   constexpr int NT = kEmitThreads, NW = NT / 32, U = kScanBatch;
   __shared__ unsigned s_bal[kEmitBallots];
   __shared__ int s_scan[40];
   __shared__ unsigned s_pre[NW];
+  __shared__ int s_chunk;
   hire_dev::griddep_wait();
   hire_dev::griddep_launch();
   KTrace kt_(kKtEmit);
-  const int b = blockIdx.y, C = gridDim.x, c = blockIdx.x;
+  const int b = blockIdx.y, C = gridDim.x;
+  if (threadIdx.x == 0) {
+    const unsigned t = atomicAdd(ticket + b, 1u);
+    if (t == static_cast<unsigned>(C) - 1u) ticket[b] = 0u;  // every chunk claimed: back to zero
+    s_chunk = static_cast<int>(t);
+  }
+  __syncthreads();
+  const int c = s_chunk;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   if (g_ktrace && threadIdx.x == 0 && b == 0 && c == C - 1) g_ktrace[39] = gtimer();
   if (g_ktrace && threadIdx.x == 0 && b == 0) atomicMax(&g_ktrace[43], gtimer());
