@@ -586,15 +586,22 @@ class DecoderWorkload(Workload):
     proxy_kernel = "q4_score_mma / q4_score_mma_sel / q4_score_umma (all int4 proxy launches: 18 FFN + vocab)"
     span_kernel = None
 
-    def __init__(self, batch, seed=0):
-        self.B, self.seed = batch, seed
+    def __init__(self, batch, world=1, rank=0, seed=0):
+        self.B, self.seed, self.world, self.rank = batch, seed, world, rank
+        # N > 1: FFN hidden units and vocabulary DA-sharded across the ranks
+        # (BASELINE configs[4]); the batch is decoded once by all ranks
+        self.scaling = "strong" if world > 1 else "weak"
 
     def attach(self, H):
         from paper_2402_09360_b200.decoder import DecoderConfig, HireDecoder
         self.H = H
         self.cfg = DecoderConfig()
         self.d, self.k, self.kp = self.cfg.d, self.cfg.vocab_k, self.cfg.vocab_k_prime
-        self.m = HireDecoder(self.cfg, self.B, seed=self.seed)
+        comm = None
+        if self.world > 1:
+            import paper_2402_09360_b200.parallel as P
+            comm = P.Communicator(self.world, self.rank)
+        self.m = HireDecoder(self.cfg, self.B, seed=self.seed, comm=comm)
         g = torch.Generator(device="cuda").manual_seed(self.seed + 5)
         self.tok = torch.randint(0, self.cfg.vocab, (self.B,), device="cuda", generator=g)
         self.tok0 = self.tok.clone()
@@ -641,6 +648,8 @@ class DecoderWorkload(Workload):
         return self.m.step_bytes(), 0, 0
 
     def recall(self, x):
+        if self.world > 1:
+            return None
         r = self.m.stage_recall(self.tok0)
         self.stage_rec = r
         return r["softmax"]
@@ -667,7 +676,7 @@ def make_workload(args, world=1, rank=0):
     if args.workload == "cfg4":
         return DaSoftmaxWorkload(B, world, rank)
     if args.workload == "cfg5":
-        return DecoderWorkload(B)
+        return DecoderWorkload(B, world, rank)
     return FfnWorkload(B)
 
 

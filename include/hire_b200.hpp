@@ -721,6 +721,44 @@ inline RecallReport recall(const CandidateSet& candidates, const TopKSet& exact)
   return r;
 }
 
+// gather_bench.hpp:18-152 — the group-gather microbenchmark, on the GPU
+// (device buffers, CUDA-event timing; same selection, checksum and messages)
+struct GatherBenchConfig {
+  std::size_t n_groups = 4096;
+  std::size_t g = 8;
+  std::size_t d = 128;
+  double fraction_selected = 0.25;
+  std::size_t repeats = 9;
+  std::uint64_t seed = 0;
+};
+
+struct GatherBenchResult {
+  double sparse_ns = 0.0;
+  double dense_ns = 0.0;
+  double efficiency_paper = 0.0;
+  double efficiency_ratio = 0.0;
+  std::size_t bytes_moved = 0;
+  std::size_t groups_selected = 0;
+  bool checksum_ok = false;
+};
+
+inline GatherBenchResult run_gather_bench(const GatherBenchConfig& cfg) {
+  hire_gather_bench_config c{static_cast<std::int64_t>(cfg.n_groups), static_cast<std::int64_t>(cfg.g),
+                             static_cast<std::int64_t>(cfg.d), cfg.fraction_selected,
+                             static_cast<std::int64_t>(cfg.repeats), cfg.seed};
+  hire_gather_bench_result r{};
+  detail::throw_status(hire_gather_bench(detail::thread_ctx(), &c, &r));
+  GatherBenchResult o;
+  o.sparse_ns = r.sparse_ns;
+  o.dense_ns = r.dense_ns;
+  o.efficiency_paper = r.efficiency_paper;
+  o.efficiency_ratio = r.efficiency_ratio;
+  o.bytes_moved = static_cast<std::size_t>(r.bytes_moved);
+  o.groups_selected = static_cast<std::size_t>(r.groups_selected);
+  o.checksum_ok = r.checksum_ok != 0;
+  return o;
+}
+
 // metrics.hpp:43-64 — the paper's parameter-bytes cost model (host integer
 // arithmetic; like the reference, the int4 term leaves out the scales)
 struct CostReport {

@@ -269,6 +269,37 @@ HIRE_API int hire_da_ffn_emulated(hire_ctx ctx, hire_matrix u, hire_matrix v, hi
                          const float* x, int64_t B, const hire_ffn_params* p, int uneven,
                          uint32_t* sel, float* out);
 
+/* ---- gather microbenchmark (gather_bench.hpp:18-152 on the GPU) --------- */
+/* GatherBenchConfig (gather_bench.hpp:18-25): n_groups groups of g vectors
+ * of dimension d; a seeded random fraction of the groups is gathered. */
+typedef struct {
+  int64_t n_groups;
+  int64_t g;
+  int64_t d;
+  double fraction_selected; /* (0, 1] */
+  int64_t repeats;          /* >= 3 */
+  uint64_t seed;
+} hire_gather_bench_config;
+/* GatherBenchResult (gather_bench.hpp:38-46). */
+typedef struct {
+  double sparse_ns;         /* median over repeats, CUDA events */
+  double dense_ns;
+  double efficiency_paper;  /* sparse / dense */
+  double efficiency_ratio;  /* dense / sparse */
+  int64_t bytes_moved;
+  int64_t groups_selected;
+  int32_t checksum_ok;
+  int32_t reserved;
+} hire_gather_bench_result;
+/* run_gather_bench (gather_bench.hpp:71-150): the selection is the
+ * reference's seeded partial Fisher-Yates (its Rng stream, rng.hpp:20-61, at
+ * the same counter position), kept in draw order; the sparse gather (one
+ * warp per group, 128-bit loads) and a dense copy of the same bytes are timed
+ * on the context stream; the gathered groups are checked against the source
+ * with the reference's FNV-1a checksum. The buffers are device memory
+ * (the reference times host memcpy). */
+HIRE_API int hire_gather_bench(hire_ctx ctx, const hire_gather_bench_config* cfg, hire_gather_bench_result* out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -38,6 +38,7 @@ EXPORTS = [
     "hire_da_topk_run", "hire_da_topk_emulated", "hire_da_ffn_run", "hire_da_ffn_emulated",
     "hire_da_topk_slots", "hire_da_topk_local", "hire_da_topk_merge",
     "hire_da_ffn_slots", "hire_da_ffn_local", "hire_da_ffn_merge",
+    "hire_gather_bench",
 ]
 
 
@@ -61,6 +62,19 @@ class FfnParams(C.Structure):
     _fields_ = [("k", C.c_int64), ("k_prime", C.c_int64), ("group_size", C.c_int64),
                 ("phi", C.c_int32), ("x_mode", C.c_int32), ("strict", C.c_int32),
                 ("reserved", C.c_int32)]
+
+
+class GatherBenchConfig(C.Structure):
+    """hire_gather_bench_config (GatherBenchConfig, gather_bench.hpp:18-25)."""
+    _fields_ = [("n_groups", C.c_int64), ("g", C.c_int64), ("d", C.c_int64), ("fraction_selected", C.c_double),
+                ("repeats", C.c_int64), ("seed", C.c_uint64)]
+
+
+class GatherBenchResult(C.Structure):
+    """hire_gather_bench_result (GatherBenchResult, gather_bench.hpp:38-46)."""
+    _fields_ = [("sparse_ns", C.c_double), ("dense_ns", C.c_double), ("efficiency_paper", C.c_double),
+                ("efficiency_ratio", C.c_double), ("bytes_moved", C.c_int64), ("groups_selected", C.c_int64),
+                ("checksum_ok", C.c_int32), ("reserved", C.c_int32)]
 
 
 _vp, _i64, _i32, _p = C.c_void_p, C.c_int64, C.c_int, C.POINTER
@@ -130,6 +144,7 @@ def _sig(L):
         "hire_da_ffn_slots": [_p(FfnParams), _i32, _p(_i64)],
         "hire_da_ffn_local": [_vp, _vp, _vp, _vp, _i64, _i32, _i32, _vp, _i64, _p(FfnParams), _i32, _vp, _vp],
         "hire_da_ffn_merge": [_vp, _vp, _vp, _i64, _i64, _i32, _i64, _p(FfnParams), _i32, _vp, _vp],
+        "hire_gather_bench": [_vp, _p(GatherBenchConfig), _p(GatherBenchResult)],
     }
     for name, args in sigs.items():
         f = getattr(L, name)

@@ -538,6 +538,42 @@ def roofline_bytes(proxy: str, d: int, l: int, gathered_rows: int, row_bytes: in
     return pb + (gathered_rows + extra_rows) * row_bytes + exchange_bytes
 
 
+@dataclass
+class GatherBenchConfig:
+    """gather_bench.hpp:18-25."""
+    n_groups: int = 4096
+    g: int = 8
+    d: int = 128
+    fraction_selected: float = 0.25
+    repeats: int = 9
+    seed: int = 0
+
+
+@dataclass
+class GatherBenchResult:
+    """gather_bench.hpp:38-46 (times in ns, CUDA events, device memory)."""
+    sparse_ns: float
+    dense_ns: float
+    efficiency_paper: float
+    efficiency_ratio: float
+    bytes_moved: int
+    groups_selected: int
+    checksum_ok: bool
+
+
+def run_gather_bench(cfg: GatherBenchConfig, ctx: Optional[Context] = None) -> GatherBenchResult:
+    """run_gather_bench (gather_bench.hpp:71-152) on the GPU: gather a seeded
+    random subset of groups (the reference's Fisher-Yates selection, draw
+    order) vs a dense copy of the same bytes; the paper's group-size argument
+    (contiguous groups of g rows gather near dense bandwidth)."""
+    ctx = ctx or default_context()
+    c = L.GatherBenchConfig(cfg.n_groups, cfg.g, cfg.d, cfg.fraction_selected, cfg.repeats, cfg.seed)
+    r = L.GatherBenchResult()
+    check(lib().hire_gather_bench(ctx.h, C.byref(c), C.byref(r)))
+    return GatherBenchResult(r.sparse_ns, r.dense_ns, r.efficiency_paper, r.efficiency_ratio, r.bytes_moved,
+                             r.groups_selected, bool(r.checksum_ok))
+
+
 def recall(cand: np.ndarray, exact_idx: np.ndarray):
     """metrics.hpp:23-34 for one query: (recall, intersection_k, top1_agree)."""
     cand = np.asarray(cand)

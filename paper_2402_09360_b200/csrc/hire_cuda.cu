@@ -36,6 +36,7 @@
 #include "select2.cuh"
 #include "fsel.cuh"
 #include "score_umma.cuh"
+#include "gather_bench.cuh"
 
 using namespace hire_dev;
 
@@ -3045,6 +3046,109 @@ int hire_da_ffn_emulated(hire_ctx ctx, hire_matrix u, hire_matrix v, hire_scorer
     // what hire_da_ffn_run computes across ranks: rank-order sum of the partials
     RET(da_ffn_merge(ctx, recv, kg_max, parts, u->d, u->rows, world, B, p, sel, out));
   }
+  return HIRE_OK;
+}
+
+// ------------------------------------------------------ gather benchmark --
+int hire_gather_bench(hire_ctx ctx, const hire_gather_bench_config* cfg, hire_gather_bench_result* out) {
+  if (!ctx || !cfg || !out) return invalid("null argument");
+  // validate (gather_bench.hpp:27-36), the reference's messages
+  if (cfg->n_groups < 1 || cfg->g < 1 || cfg->d < 1) return invalid("GatherBenchConfig: dims must be >= 1");
+  if (!(cfg->fraction_selected > 0.0) || cfg->fraction_selected > 1.0)
+    return invalid("GatherBenchConfig: fraction_selected must be in (0, 1]");
+  if (cfg->repeats < 3) return invalid("GatherBenchConfig: repeats must be >= 3");
+  const int64_t group_elems = cfg->g * cfg->d, total = cfg->n_groups * group_elems;
+  const int64_t n_sel = static_cast<int64_t>(std::ceil(cfg->fraction_selected * static_cast<double>(cfg->n_groups)));
+  // seeded partial Fisher-Yates in draw order (gather_bench.hpp:84-93): the
+  // Rng has produced total Gaussians = 2 * ceil(total / 2) uniforms first
+  std::vector<uint32_t> ids(static_cast<size_t>(cfg->n_groups));
+  for (int64_t i = 0; i < cfg->n_groups; ++i) ids[i] = static_cast<uint32_t>(i);
+  uint64_t counter = 2 * static_cast<uint64_t>((total + 1) / 2);
+  for (int64_t i = 0; i < n_sel; ++i) {
+    const uint64_t r = rng_mix64(cfg->seed, ++counter);
+    const int64_t j = i + static_cast<int64_t>(r % static_cast<uint64_t>(cfg->n_groups - i));
+    std::swap(ids[i], ids[j]);
+  }
+  ids.resize(static_cast<size_t>(n_sel));
+  const int64_t sel_elems = n_sel * group_elems;
+  float *src = nullptr, *dst = nullptr;
+  uint32_t* dids = nullptr;
+  uint64_t* sums = nullptr;
+  auto release = [&] {
+    cudaFree(src);
+    cudaFree(dst);
+    cudaFree(dids);
+    cudaFree(sums);
+  };
+  cudaError_t e = cudaMalloc(&src, static_cast<size_t>(total) * 4);
+  if (e == cudaSuccess) e = cudaMalloc(&dst, static_cast<size_t>(sel_elems) * 4);
+  if (e == cudaSuccess) e = cudaMalloc(&dids, static_cast<size_t>(n_sel) * 4);
+  if (e == cudaSuccess) e = cudaMalloc(&sums, static_cast<size_t>(n_sel) * 16);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(dids, ids.data(), static_cast<size_t>(n_sel) * 4, cudaMemcpyHostToDevice, ctx->stream);
+  if (e != cudaSuccess) {
+    release();
+    return set_err(HIRE_ERR_RUNTIME, std::string("hire_gather_bench: ") + cudaGetErrorString(e));
+  }
+  gb_fill_kernel<<<static_cast<unsigned>(ceil_div(total, 256)), 256, 0, ctx->stream>>>(src, total, cfg->seed);
+  const unsigned grid = static_cast<unsigned>(std::min<int64_t>(ceil_div(sel_elems / 4 + 1, 256), 16LL * ctx->num_sms));
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  auto launch_copy = [&](const uint32_t* sel) {
+    if (sel) {
+      gb_gather_kernel<<<grid, 256, 0, ctx->stream>>>(src, sel, n_sel, group_elems, dst);
+    } else if (sel_elems % 4 == 0) {  // dense: one contiguous copy of the same bytes
+      gb_copy_kernel<<<static_cast<unsigned>(std::min<int64_t>(ceil_div(sel_elems / 4, 256), 16LL * ctx->num_sms)), 256, 0,
+                       ctx->stream>>>(reinterpret_cast<const float4*>(src), reinterpret_cast<float4*>(dst), sel_elems / 4);
+    } else {
+      cudaMemcpyAsync(dst, src, static_cast<size_t>(sel_elems) * 4, cudaMemcpyDeviceToDevice, ctx->stream);
+    }
+  };
+  auto time_copy = [&](const uint32_t* sel, std::vector<double>* ts) {
+    launch_copy(sel);  // warm-up, discarded
+    for (int64_t r = 0; r < cfg->repeats; ++r) {
+      cudaEventRecord(e0, ctx->stream);
+      launch_copy(sel);
+      cudaEventRecord(e1, ctx->stream);
+      cudaEventSynchronize(e1);
+      float ms = 0.0f;
+      cudaEventElapsedTime(&ms, e0, e1);
+      ts->push_back(static_cast<double>(ms) * 1e6);
+    }
+  };
+  auto median = [](std::vector<double> v) {
+    std::sort(v.begin(), v.end());
+    const size_t n = v.size();
+    return n % 2 == 1 ? v[n / 2] : 0.5 * (v[n / 2 - 1] + v[n / 2]);
+  };
+  std::vector<double> sparse_t, dense_t;
+  time_copy(dids, &sparse_t);
+  // verify the gather before the dense baseline reuses the buffer (gather_bench.hpp:116-127)
+  const unsigned cg = static_cast<unsigned>(ceil_div(n_sel, 128));
+  gb_checksum_kernel<<<cg, 128, 0, ctx->stream>>>(dst, nullptr, n_sel, group_elems, sums);
+  gb_checksum_kernel<<<cg, 128, 0, ctx->stream>>>(src, dids, n_sel, group_elems, sums + n_sel);
+  std::vector<uint64_t> hs(static_cast<size_t>(2 * n_sel));
+  e = cudaMemcpyAsync(hs.data(), sums, static_cast<size_t>(2 * n_sel) * 8, cudaMemcpyDeviceToHost, ctx->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
+  uint64_t gathered = 0, expected = 0;
+  for (int64_t i = 0; i < n_sel; ++i) {
+    gathered = gathered * 31 + hs[static_cast<size_t>(i)];
+    expected = expected * 31 + hs[static_cast<size_t>(n_sel + i)];
+  }
+  if (e == cudaSuccess) time_copy(nullptr, &dense_t);
+  if (e == cudaSuccess) e = cudaGetLastError();
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  release();
+  if (e != cudaSuccess) return set_err(HIRE_ERR_RUNTIME, std::string("hire_gather_bench: ") + cudaGetErrorString(e));
+  out->sparse_ns = median(sparse_t);
+  out->dense_ns = median(dense_t);
+  out->efficiency_paper = out->sparse_ns / out->dense_ns;
+  out->efficiency_ratio = out->dense_ns / out->sparse_ns;
+  out->bytes_moved = sel_elems * 4;
+  out->groups_selected = n_sel;
+  out->checksum_ok = gathered == expected ? 1 : 0;
+  out->reserved = 0;
   return HIRE_OK;
 }
 

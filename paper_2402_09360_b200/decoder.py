@@ -5,7 +5,17 @@ the dense parts — RMSNorm, the QKV / output projections (cuBLAS through
 torch.matmul) and attention over a KV cache (torch SDPA / flash) — are
 library code; every HiRE stage runs in libhire_cuda.so. The dense oracle is
 the same model with k = k' = all units / all vocab rows
-(tests/test_decoder.py)."""
+(tests/test_decoder.py).
+
+DA-TOP-k sharding (BASELINE configs[4]: FFN hidden units and vocabulary
+sharded D ways): with a communicator (`comm`, one process per GPU) every FFN
+layer runs `parallel.da_group_sparse` over this rank's hidden-unit shard
+(local quotas, one grouped all-gather of unit ids + partial outputs, rank-
+order sum: every rank ends with the same residual stream) and the output
+layer `parallel.da_topk` over this rank's vocabulary shard (global merge).
+`emulate=D` runs the same D-shard algorithm on one GPU
+(`da_group_sparse_emulated` / `da_topk_emulated`) for tests. Attention and
+the tied embedding are replicated."""
 from __future__ import annotations
 
 from dataclasses import dataclass
@@ -15,7 +25,8 @@ import torch
 import torch.nn.functional as F
 
 from . import _lib as L
-from .api import ApproxScorer, GroupedFFN, HireConfig, ScoreMatrix, ffn_group_sparse, hire_topk
+from .api import (ApproxScorer, GroupedFFN, HireConfig, ScoreMatrix, da_group_sparse_emulated, da_topk_emulated,
+                  ffn_group_sparse, hire_topk)
 
 
 @dataclass
@@ -40,6 +51,8 @@ class _Layer:
     proxy: ApproxScorer
     k_cache: torch.Tensor   # [B, H, T, hd] bf16
     v_cache: torch.Tensor
+    ffn_shard: Optional[GroupedFFN] = None     # this rank's hidden units (comm mode)
+    proxy_shard: Optional[ApproxScorer] = None
 
 
 def _rmsnorm(h: torch.Tensor) -> torch.Tensor:
@@ -52,8 +65,12 @@ class HireDecoder:
     family (N(0, 1/d) + 3x rank-128); vocab rows the cfg3 family (rank-256 +
     0.1 N(0, 1)), tied with the token embedding; KV caches N(0, 1)."""
 
-    def __init__(self, cfg: DecoderConfig, batch: int, seed: int = 0, dtype=torch.bfloat16):
+    def __init__(self, cfg: DecoderConfig, batch: int, seed: int = 0, dtype=torch.bfloat16, comm=None,
+                 emulate: int = 1):
         self.cfg, self.B = cfg, batch
+        self.comm, self.emulate = comm, emulate
+        self.world = comm.world if comm is not None else 1
+        self.rank = comm.rank if comm is not None else 0
         d, hd = cfg.d, cfg.d // cfg.heads
         g = torch.Generator(device="cuda").manual_seed(seed)
 
@@ -83,6 +100,17 @@ class HireDecoder:
         self.vocab_proxy = ApproxScorer.quantize(self.vocab)
         self.embed = W  # tied
         self.softmax_cfg = HireConfig(k=cfg.vocab_k, k_prime=cfg.vocab_k_prime, x_mode=L.X_INT8)
+        if comm is not None:
+            # this rank's shards (width rule, distributed.hpp:53-57): row
+            # views of the replicated weights, each with its own int4 proxy
+            from .parallel import shard_range
+            for lay in self.layers:
+                f0, w0 = shard_range(cfg.ffn, self.world, self.rank)
+                lay.ffn_shard = GroupedFFN(lay.ffn.u.slice_cols(f0, w0), lay.ffn.v.slice_cols(f0, w0), 1, "relu")
+                lay.proxy_shard = ApproxScorer.quantize(lay.ffn_shard.u)
+            v0, vw = shard_range(cfg.vocab, self.world, self.rank)
+            self.vocab_shard = self.vocab.slice_cols(v0, vw)
+            self.vocab_proxy_shard = ApproxScorer.quantize(self.vocab_shard)
 
     def attention(self, lay: _Layer, a: torch.Tensor) -> torch.Tensor:
         """Dense attention for the new token over the KV cache (the newest
@@ -103,14 +131,37 @@ class HireDecoder:
         cfg = self.cfg
         kk = ffn_k or cfg.ffn_k
         kp = ffn_k_prime or cfg.ffn_k_prime
+        sm = softmax_cfg or self.softmax_cfg
         h = self.embed[tokens].float()
         for lay in self.layers:
             h = h + self.attention(lay, _rmsnorm(h)).float()
-            out, _ = ffn_group_sparse(lay.ffn, _rmsnorm(h).contiguous(), lay.proxy, kk, kp, x_mode=L.X_INT8)
-            h = h + out
-        r = hire_topk(_rmsnorm(h).contiguous(), self.vocab, self.vocab_proxy, softmax_cfg or self.softmax_cfg,
-                      want_candidates=False)
+            h = h + self._ffn(lay, _rmsnorm(h).contiguous(), kk, kp)
+        z = _rmsnorm(h).contiguous()
+        if self.comm is not None:
+            from .parallel import da_topk
+            ti, tv, _ = da_topk(self.vocab_shard, self.vocab_proxy_shard, self.cfg.vocab, z, sm, self.comm,
+                                merge=L.MERGE_GLOBAL)
+            return ti[:, 0], ti, tv
+        if self.emulate > 1:
+            ti, tv, _ = da_topk_emulated(self.vocab, self.vocab_proxy, z, self.emulate, sm, merge=L.MERGE_GLOBAL,
+                                         uneven=True)
+            return ti[:, 0], ti, tv
+        r = hire_topk(z, self.vocab, self.vocab_proxy, sm, want_candidates=False)
         return r.top_idx[:, 0], r.top_idx, r.top_val
+
+    def _ffn(self, lay: _Layer, x: torch.Tensor, k: int, kp: int) -> torch.Tensor:
+        """HiRE-FFN of one layer: whole (one GPU), DA-sharded across ranks
+        (da_group_sparse, distributed.hpp:145-206), or its D-shard emulation."""
+        if self.comm is not None:
+            from .parallel import da_group_sparse
+            out, _ = da_group_sparse(lay.ffn_shard, lay.proxy_shard, self.cfg.ffn, x, k, kp, self.comm,
+                                     x_mode=L.X_INT8, uneven=True)
+            return out
+        if self.emulate > 1:
+            out, _ = da_group_sparse_emulated(lay.ffn, x, lay.proxy, k, kp, self.emulate, x_mode=L.X_INT8, uneven=True)
+            return out
+        out, _ = ffn_group_sparse(lay.ffn, x, lay.proxy, k, kp, x_mode=L.X_INT8)
+        return out
 
     def dense_step(self, tokens: torch.Tensor, ffn_k: Optional[int] = None):
         """The dense oracle (fp32 torch arithmetic on the same weights): every

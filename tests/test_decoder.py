@@ -41,3 +41,67 @@ def test_decoder_production_quotas(H):
     # HiRE stages approximate: int4 proxy candidates, then exact top-k)
     rec = sum(len(set(idx[b].tolist()) & set(didx[b].tolist())) for b in range(16)) / (16 * cfg.vocab_k)
     assert rec > 0.8, rec
+
+
+def test_decoder_sharded_one_rank_comm_equals_unsharded(H):
+    """DA-sharded decoder step (da_group_sparse per FFN layer, da_topk over
+    the vocabulary) through a 1-rank NCCL communicator — the full local ->
+    all-gather -> merge chain of every stage — gives the unsharded step."""
+    from paper_2402_09360_b200 import parallel as P
+    from paper_2402_09360_b200.decoder import HireDecoder
+    cfg = _small()
+    comm = P.Communicator(1, 0)
+    m0 = HireDecoder(cfg, batch=8, seed=5)
+    m1 = HireDecoder(cfg, batch=8, seed=5, comm=comm)
+    tok = torch.randint(0, cfg.vocab, (8,), device="cuda", generator=torch.Generator(device="cuda").manual_seed(6))
+    for _ in range(2):
+        n0, i0, v0 = m0.step(tok)
+        n1, i1, v1 = m1.step(tok)
+        assert torch.equal(i0.long(), i1.long()) and torch.equal(v0, v1)
+        tok = n0.long()
+
+
+@pytest.mark.parametrize("shards", [2, 4])
+def test_decoder_emulated_shard_stages(H, shards):
+    """The D-shard stages the sharded decoder runs (local quotas, uneven for
+    k = 51; global merge for the vocabulary), teacher-forced on one hidden
+    state: DA-FFN units and DA-softmax tokens against the exact top-k, and
+    the emulated step runs end to end. (Per-shard quotas approximate the
+    global top-k — distributed.hpp:172-201 — so a free-running sharded
+    decode drifts from the unsharded one over layers.)"""
+    from paper_2402_09360_b200.decoder import HireDecoder, _rmsnorm
+    cfg = _small()
+    m = HireDecoder(cfg, batch=16, seed=3, emulate=shards)
+    g = torch.Generator(device="cuda").manual_seed(4)
+    x = _rmsnorm(torch.randn(16, cfg.d, device="cuda", generator=g)).contiguous()
+    lay = m.layers[0]
+    _, sel = H.da_group_sparse_emulated(lay.ffn, x, lay.proxy, cfg.ffn_k, cfg.ffn_k_prime, shards, x_mode=H.X_INT8,
+                                        uneven=True)
+    act = torch.relu(x @ lay.ffn.u.tensor.float().t())
+    top = torch.topk(act, cfg.ffn_k, dim=-1).indices
+    rec = sum(len(set(sel[b].tolist()) & set(top[b].tolist())) for b in range(16)) / (16 * cfg.ffn_k)
+    assert rec > 0.8, rec
+    ti, tv, _ = H.da_topk_emulated(m.vocab, m.vocab_proxy, x, shards, m.softmax_cfg, merge=H.MERGE_GLOBAL)
+    ex = torch.topk(x @ m.vocab.tensor.float().t(), cfg.vocab_k, dim=-1).indices
+    rec_s = sum(len(set(ti[b].tolist()) & set(ex[b].tolist())) for b in range(16)) / (16 * cfg.vocab_k)
+    assert rec_s > 0.9, rec_s
+    tok = torch.randint(0, cfg.vocab, (16,), device="cuda", generator=g)
+    nxt, idx, val = m.step(tok)
+    assert idx.shape == (16, cfg.vocab_k) and bool(torch.all(val[:, :-1] >= val[:, 1:]))
+
+
+@pytest.mark.parametrize("B", [1, 64])
+def test_decoder_cfg5_full_size_stage_recall(H, B):
+    """BASELINE configs[4] at its own shape (18 layers, d=2048, FFN 8192 at
+    top-5% from 10% int4-proxy candidates, 16 heads x 1024-token KV cache,
+    V=256000 HiRE-softmax k'=1024, k=64): every stage, teacher-forced on the
+    exact-top-k model's hidden states, recovers the exact top-k units /
+    tokens (recall of the FFN units and of the softmax top-k)."""
+    from paper_2402_09360_b200.decoder import DecoderConfig, HireDecoder
+    m = HireDecoder(DecoderConfig(), batch=B, seed=7)
+    tok = torch.randint(0, 256000, (B,), device="cuda", generator=torch.Generator(device="cuda").manual_seed(8))
+    r = m.stage_recall(tok)
+    assert r["ffn_layers_mean"] > 0.98 and r["ffn_layers_min"] > 0.95, r
+    assert r["softmax"] > 0.95, r
+    nxt, idx, val = m.step(tok)
+    assert idx.shape == (B, 64) and bool(torch.all(val[:, :-1] >= val[:, 1:]))
