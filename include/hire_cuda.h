@@ -269,6 +269,15 @@ HIRE_API int hire_da_ffn_emulated(hire_ctx ctx, hire_matrix u, hire_matrix v, hi
                          const float* x, int64_t B, const hire_ffn_params* p, int uneven,
                          uint32_t* sel, float* out);
 
+/* ---- seeded instances (host; rng.hpp:20-67, instance.hpp:16-83) --------- */
+/* The reference's Rng stream, derive_seed, gen_vector and gen_instance with
+ * the same arithmetic (bit-identical inputs for the experiment runner).
+ * gen_instance writes [l][d] row-major (= the reference's d x l column-
+ * major ScoreMatrix); spectrum 0 flat (iid Gaussian), 1 decaying (1/i). */
+HIRE_API uint64_t hire_derive_seed(uint64_t seed, uint64_t stream);
+HIRE_API int hire_gen_vector(uint64_t seed, int64_t n, float* out);
+HIRE_API int hire_gen_instance(int64_t d, int64_t l, uint64_t seed, int spectrum, float* out);
+
 /* ---- gather microbenchmark (gather_bench.hpp:18-152 on the GPU) --------- */
 /* GatherBenchConfig (gather_bench.hpp:18-25): n_groups groups of g vectors
  * of dimension d; a seeded random fraction of the groups is gathered. */

@@ -131,6 +131,8 @@ def ref():
         L.ref_derive_seed.restype = _u64
         L.ref_derive_seed.argtypes = [_u64, _u64]
         L.ref_gen_vector.argtypes = [_u64, _u64, _vp]
+        L.ref_gen_instance.restype = _i32
+        L.ref_gen_instance.argtypes = [_u64, _u64, _u64, _i32, _vp]
         L.ref_matrix_create.restype = _vp
         L.ref_matrix_create.argtypes = [_vp, _u64, _u64]
         L.ref_matrix_destroy.argtypes = [_vp]

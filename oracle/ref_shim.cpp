@@ -19,6 +19,7 @@
 #include <vector>
 
 #include "hire/approx.hpp"
+#include "hire/instance.hpp"
 #include "hire/distributed.hpp"
 #include "hire/ffn.hpp"
 #include "hire/hire.hpp"
@@ -66,6 +67,22 @@ REF_EXPORT uint64_t ref_derive_seed(uint64_t seed, uint64_t stream) {
 REF_EXPORT void ref_gen_vector(uint64_t dim, uint64_t seed, float* out) {
   hire::Rng r(seed);
   for (uint64_t i = 0; i < dim; ++i) out[i] = r.next_gaussian_f();
+}
+
+// gen_instance (instance.hpp:58-83) into [l][d] (column j of Z = row j)
+REF_EXPORT int ref_gen_instance(uint64_t d, uint64_t l, uint64_t seed, int decaying, float* out) {
+  try {
+    const hire::ScoreMatrix z =
+        hire::gen_instance(d, l, seed, decaying ? hire::Spectrum::kDecaying : hire::Spectrum::kFlat);
+    for (uint64_t j = 0; j < l; ++j) {
+      const auto c = z.col(j);
+      std::memcpy(out + j * d, c.data(), d * sizeof(float));
+    }
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return 1;
+  }
 }
 
 // ------------------------------------------------------------- objects --

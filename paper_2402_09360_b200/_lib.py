@@ -38,7 +38,7 @@ EXPORTS = [
     "hire_da_topk_run", "hire_da_topk_emulated", "hire_da_ffn_run", "hire_da_ffn_emulated",
     "hire_da_topk_slots", "hire_da_topk_local", "hire_da_topk_merge",
     "hire_da_ffn_slots", "hire_da_ffn_local", "hire_da_ffn_merge",
-    "hire_gather_bench",
+    "hire_gather_bench", "hire_derive_seed", "hire_gen_vector", "hire_gen_instance",
 ]
 
 
@@ -87,6 +87,8 @@ def _sig(L):
     L.hire_abi_version.restype = _i32
     L.hire_experiments_built.restype = _i32
     L.hire_experiments_built.argtypes = []
+    L.hire_derive_seed.restype = C.c_uint64
+    L.hire_derive_seed.argtypes = [C.c_uint64, C.c_uint64]
     L.hire_ctx_launch_count.restype = _i64
     L.hire_ctx_launch_count.argtypes = [_vp]
     sigs = {
@@ -145,6 +147,8 @@ def _sig(L):
         "hire_da_ffn_local": [_vp, _vp, _vp, _vp, _i64, _i32, _i32, _vp, _i64, _p(FfnParams), _i32, _vp, _vp],
         "hire_da_ffn_merge": [_vp, _vp, _vp, _i64, _i64, _i32, _i64, _p(FfnParams), _i32, _vp, _vp],
         "hire_gather_bench": [_vp, _p(GatherBenchConfig), _p(GatherBenchResult)],
+        "hire_gen_vector": [C.c_uint64, _i64, _vp],
+        "hire_gen_instance": [_i64, _i64, C.c_uint64, _i32, _vp],
     }
     for name, args in sigs.items():
         f = getattr(L, name)

@@ -3049,6 +3049,97 @@ int hire_da_ffn_emulated(hire_ctx ctx, hire_matrix u, hire_matrix v, hire_scorer
   return HIRE_OK;
 }
 
+// ------------------------------------------------ seeded host instances --
+// The reference's input generators (host code: the experiment runner's
+// instances are generated on the host in the reference too): Rng
+// (rng.hpp:20-61, splitmix64 counter stream, Box-Muller with a cached
+// spare, libm log1p / sin / cos), derive_seed (rng.hpp:64-67), gen_vector
+// and gen_instance (instance.hpp:16-83, Gram-Schmidt in double for the
+// decaying spectrum) — the same arithmetic, so the same bits.
+namespace {
+struct HostRng {
+  uint64_t seed, counter = 0;
+  double spare = 0.0;
+  bool has_spare = false;
+  explicit HostRng(uint64_t s) : seed(s) {}
+  uint64_t next_u64() { return rng_mix64(seed, ++counter); }
+  double next_uniform() { return static_cast<double>(next_u64() >> 11) * 0x1.0p-53; }
+  double next_gaussian() {
+    if (has_spare) {
+      has_spare = false;
+      return spare;
+    }
+    const double u1 = next_uniform(), u2 = next_uniform();
+    const double radius = std::sqrt(-2.0 * std::log1p(-u1));
+    const double angle = 2.0 * 3.141592653589793238462643383279502884 * u2;
+    spare = radius * std::sin(angle);
+    has_spare = true;
+    return radius * std::cos(angle);
+  }
+};
+
+// orthonormal columns (instance.hpp:26-50): q[c][0..rows)
+int orthonormal_columns(int64_t rows, int64_t cols, HostRng& rng, std::vector<std::vector<double>>* q) {
+  q->assign(static_cast<size_t>(cols), std::vector<double>(static_cast<size_t>(rows)));
+  for (int64_t c = 0; c < cols; ++c) {
+    auto& qc = (*q)[static_cast<size_t>(c)];
+    for (int attempt = 0;; ++attempt) {
+      for (int64_t i = 0; i < rows; ++i) qc[i] = rng.next_gaussian();
+      for (int64_t p = 0; p < c; ++p) {
+        const auto& qp = (*q)[static_cast<size_t>(p)];
+        double proj = 0.0;
+        for (int64_t i = 0; i < rows; ++i) proj += qc[i] * qp[i];
+        for (int64_t i = 0; i < rows; ++i) qc[i] -= proj * qp[i];
+      }
+      double norm = 0.0;
+      for (double x : qc) norm += x * x;
+      norm = std::sqrt(norm);
+      if (norm > 1e-8) {
+        for (int64_t i = 0; i < rows; ++i) qc[i] /= norm;
+        break;
+      }
+      if (attempt > 16) return set_err(HIRE_ERR_RUNTIME, "orthonormal_columns: degenerate draw");
+    }
+  }
+  return HIRE_OK;
+}
+}  // namespace
+
+uint64_t hire_derive_seed(uint64_t seed, uint64_t stream) {
+  HostRng r(seed ^ (0xA5A5A5A55A5A5A5AULL + stream));
+  return r.next_u64();
+}
+
+int hire_gen_vector(uint64_t seed, int64_t n, float* out) {
+  if (!out || n < 0) return invalid("null argument");
+  HostRng r(seed);
+  for (int64_t i = 0; i < n; ++i) out[i] = static_cast<float>(r.next_gaussian());
+  return HIRE_OK;
+}
+
+int hire_gen_instance(int64_t d, int64_t l, uint64_t seed, int spectrum, float* out) {
+  if (!out) return invalid("null argument");
+  if (d < 1 || l < 1) return invalid("gen_instance: dims must be positive");
+  HostRng rng(seed);
+  if (spectrum == 0) {  // flat: column j (row j here) entries i, j-major
+    for (int64_t j = 0; j < l; ++j)
+      for (int64_t i = 0; i < d; ++i) out[j * d + i] = static_cast<float>(rng.next_gaussian());
+    return HIRE_OK;
+  }
+  const int64_t rank = std::min(d, l);
+  std::vector<std::vector<double>> left, right;
+  RET(orthonormal_columns(d, rank, rng, &left));
+  RET(orthonormal_columns(l, rank, rng, &right));
+  for (int64_t j = 0; j < l; ++j)
+    for (int64_t i = 0; i < d; ++i) {
+      double acc = 0.0;
+      for (int64_t q = 0; q < rank; ++q)
+        acc += left[static_cast<size_t>(q)][i] * right[static_cast<size_t>(q)][j] / static_cast<double>(q + 1);
+      out[j * d + i] = static_cast<float>(acc);
+    }
+  return HIRE_OK;
+}
+
 // ------------------------------------------------------ gather benchmark --
 int hire_gather_bench(hire_ctx ctx, const hire_gather_bench_config* cfg, hire_gather_bench_result* out) {
   if (!ctx || !cfg || !out) return invalid("null argument");
