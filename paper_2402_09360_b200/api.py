@@ -67,9 +67,8 @@ class Context:
         if op != 2:
             check(lib().hire_debug_ktrace(self.h, op, None, 0))
             return None
-        buf = (C.c_ulonglong * 64)()
-        
-        check(lib().hire_debug_ktrace(self.h, 2, buf, 64))
+        buf = (C.c_ulonglong * 96)()
+        check(lib().hire_debug_ktrace(self.h, 2, buf, 96))
         spans = {}
         for i, name in enumerate(self.KT_NAMES):
             a, b = buf[2 * i], buf[2 * i + 1]
@@ -108,6 +107,9 @@ class Context:
         out = {k: (round((a - t0) / 1e3, 2), round((b - t0) / 1e3, 2)) for k, (a, b) in
                sorted(spans.items(), key=lambda t: t[1][0])}
         out.update(counts)
+        probes = {i: round((buf[i] - t0) / 1e3, 2) for i in range(64, 96) if buf[i]}
+        if probes:
+            out["probes_us"] = probes  # ad hoc phase probes (g_ktrace[64..95])
         return out
 
     def profile_read(self) -> dict:

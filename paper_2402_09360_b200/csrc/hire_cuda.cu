@@ -20,9 +20,11 @@
 #include <cstdio>
 #include <cstring>
 #include <cstdlib>
+#include <map>
 #include <memory>
 #include <mutex>
 #include <string>
+#include <tuple>
 #include <vector>
 
 #include "../../include/hire_cuda.h"
@@ -486,6 +488,76 @@ int plan_select(int64_t n, int64_t k_prime, int sel_mode, int64_t nb_req, int64_
   }
 }
 
+// Stream path plan (sel_stream_kernel): C chunks per query, seg list slots per
+// chunk, and the sample rank r_s of each chunk's bound. r_s is the smallest
+// rank with P[Binomial(S, k'/n) >= r_s] <= 1e-9 (S = the chunk's sample
+// size): the chance that a chunk's bound lies above the true k'-th key, which
+// only costs the finisher's slow path, never exactness. The bound may stop
+// early once at most stop_s sample keys lie above it.
+struct StreamPlan {
+  int C = 0, seg = 0;
+  int64_t r_s = 0;
+};
+
+int64_t binom_tail_rank(int64_t S, double p, double eps) {
+  // smallest r with P[X >= r] <= eps, X ~ Binomial(S, p)
+  if (p <= 0.0) return 1;
+  if (p >= 1.0) return S + 1;
+  const double lp = std::log(p), lq = std::log1p(-p);
+  auto logpmf = [&](int64_t x) {
+    return std::lgamma(static_cast<double>(S) + 1.0) - std::lgamma(static_cast<double>(x) + 1.0) -
+           std::lgamma(static_cast<double>(S - x) + 1.0) + static_cast<double>(x) * lp + static_cast<double>(S - x) * lq;
+  };
+  double tail = 0.0;
+  int64_t r = S + 1;
+  for (int64_t x = S; x >= 0; --x) {
+    tail += std::exp(logpmf(x));
+    if (tail > eps) break;
+    r = x;
+  }
+  return r;
+}
+
+bool plan_stream(hire_ctx ctx, int64_t n, uint32_t K, int64_t B, StreamPlan* st) {
+  using namespace hire_dev;
+  static const int occ = max_blocks(sel_stream_kernel, kStrThreads, 0);
+  const char* ce = std::getenv("HIRE_STREAM_C");
+  int64_t C = std::min<int64_t>({ceil_div(n, kStrSample), std::max<int64_t>(1, static_cast<int64_t>(ctx->num_sms) * occ / B),
+                                 static_cast<int64_t>(kStrMaxChunks)});
+  if (ce) C = std::max<int64_t>(1, std::min<int64_t>(std::atoi(ce), kStrMaxChunks));
+  const int64_t G = ceil_div(n, 128);
+  struct Key {
+    int64_t S, n;
+    uint32_t K;
+    bool operator<(const Key& o) const { return std::tie(S, n, K) < std::tie(o.S, o.n, o.K); }
+  };
+  static thread_local std::map<Key, int64_t> memo;
+  for (; C >= 1; C = C > 1 ? (C + 1) / 2 : 0) {
+    const int64_t chunk = ceil_div(G, C) * 128;                 // keys of a full chunk
+    const int64_t S = std::min<int64_t>(kStrSample, chunk);     // its sample
+    const Key key{S, n, K};
+    auto it = memo.find(key);
+    if (it == memo.end()) {
+      if (memo.size() > 256) memo.clear();
+      it = memo.emplace(key, binom_tail_rank(S, static_cast<double>(K) / static_cast<double>(n), 1e-7)).first;
+    }
+    const int64_t r_s = it->second;
+    if (r_s > S) return false;
+    const int64_t seg = std::min<int64_t>(kStrSegMax, kFinCap / C);
+    // keys listed per chunk: about r_s of every S (1.25 x for the bound from
+    // the per-thread maxima), plus six sigma and slack
+    const double per_chunk = (r_s <= kStrFastRank ? 1.25 : 1.0) * static_cast<double>(r_s) / static_cast<double>(S) *
+                             static_cast<double>(chunk);
+    if (per_chunk + 6.0 * std::sqrt(per_chunk) + 16.0 <= static_cast<double>(seg)) {
+      st->C = static_cast<int>(C);
+      st->seg = static_cast<int>(seg);
+      st->r_s = r_s;
+      return true;
+    }
+  }
+  return false;
+}
+
 // Candidate selection over scores [B][n] -> cand [B][cand_stride] ascending.
 int run_select(hire_ctx ctx, const float* scores, int64_t score_stride, int64_t n, int64_t B,
                const SelPlan& sp, uint64_t* surv, uint32_t* cand, int64_t cand_stride,
@@ -554,6 +626,24 @@ int run_select(hire_ctx ctx, const float* scores, int64_t score_stride, int64_t 
       uint64_t* piv = surv;                                              // [B][4]
       uint64_t* lists = surv + 5 * B + B * kWinBins * kWinGroups / 2;    // [B][kFinCap] (>= B x 65536 words)
       fs.lists = lists;
+      // stream path: sample bound + list scan in one launch (sel_stream_kernel)
+      {
+        const char* se = std::getenv("HIRE_SEL_STREAM");
+        const bool aligned = (reinterpret_cast<uintptr_t>(scores) & 15) == 0 && (score_stride & 3) == 0;
+        StreamPlan st;
+        if (!(se && se[0] == '0') && aligned && plan_stream(ctx, n, K, B, &st)) {
+          fs.nslots = st.C * st.seg;
+          RET(ensure_tickets(ctx, B));
+          CK(launch_k(ctx, sel_stream_kernel, dim3(static_cast<unsigned>(st.C), static_cast<unsigned>(B)), kStrThreads,
+                      0, scores, score_stride, nn, static_cast<uint32_t>(st.r_s), static_cast<uint32_t>(st.seg), fs.cnt,
+                      fs.lo, lists, static_cast<int64_t>(hire_dev::kFinCap), ctx->tickets));
+          CK(launch_k(ctx, sel_fin_kernel, static_cast<unsigned>(B), hire_dev::kFinThreads,
+                      static_cast<size_t>((n + 31) / 32) * 4, scores, score_stride, fs, cand, cand_stride,
+                      ordered ? 1 : 0, status));
+          CK(cudaGetLastError());
+          return HIRE_OK;
+        }
+      }
       // (32 instead of 8 CTAs per SM over the batch: measured the same)
       const int64_t CL = std::max<int64_t>(1, std::min<int64_t>(ceil_div(n, kWinThreads * kScanBatch),
                                                                 std::max<int64_t>(1, 8 * ctx->num_sms / B)));
@@ -1418,7 +1508,7 @@ int run_scores_fsel(hire_ctx ctx, const hire_scorer_s* a, const float* x, int64_
     CK(launch_k(ctx, prep_x_int8_kernel, static_cast<unsigned>(B), 256, 0, x, d, t.sw.xq, t.sw.xperm, t.sw.sx,
                 t.sw.sumxq, 0, static_cast<int>(B)));
   }
-  FuseSel fs;
+  FuseSel fs{};
   fs.xf = fold ? x : nullptr;
   fs.n = static_cast<uint32_t>(a->rows);
   fs.K = static_cast<uint32_t>(sp.k_eff);
@@ -1746,10 +1836,10 @@ int hire_ctx_read_trace(hire_ctx c, long long* out, int n) {
 }
 
 int hire_debug_ktrace(hire_ctx c, int op, unsigned long long* out, int n) {
-  // op 1: enable + reset, 2: read n (<= 64) words, 0: disable
+  // op 1: enable + reset, 2: read n (<= 96) words, 0: disable
   if (!c) return invalid("null handle");
   static unsigned long long* buf = nullptr;
-  constexpr int kWords = 2 * hire_dev::kKtNum;
+  constexpr int kWords = 2 * hire_dev::kKtNum + 32;  // + 32 ad hoc probe words (g_ktrace[64..95])
   CK(cudaStreamSynchronize(c->stream));
   if (op == 1) {
     if (!buf) CK(cudaMalloc(&buf, kWords * sizeof(unsigned long long)));

@@ -796,6 +796,270 @@ __global__ void __launch_bounds__(kWinThreads) sel_wlist_kernel(
 }
 
 // ---------------------------------------------------------------------
+// S12 (stream path): sample bound + list scan in ONE launch. grid (C, B),
+// 256 threads. The score row is cut into 128-key granules (512 B, one float4
+// per lane); chunk c owns granules g = c (mod C), a systematic sample of the
+// whole row. The first CTA of a query to arrive (a ticket: atomicAdd on
+// ticket[b], zero at rest) is the query's sampler, so it is running before
+// any CTA that waits on it, whatever the dispatch order. The sampler's first
+// 4096 keys (16 per thread) are the sample: tau <= the sample's rank-r_s key
+// (r_s ~ k'/n * 4096 + margin, chosen on the host so that P[tau > T] ~ 1e-7
+// for exchangeable rows). Small r_s: tau = the r_s-th largest of the 256
+// per-thread sample maxima (r_s distinct threads hold a key >= it; a warp
+// bitonic sort of the maxima, then a rank by binary search over the 8 sorted
+// lists — two barriers). Otherwise the exact order statistic
+// (block_range_select). tau, stripped of its index part, is published with an
+// atomic on qtau[b]; the other CTAs of the query have their first two batches
+// of loads in flight while they poll it. Every key >= tau of a chunk goes to
+// its own list segment lists[b][c*seg ...], zero-padded to seg; qcnt[b] +=
+// keys listed (bit 31: a segment overflowed or the bound never arrived).
+// qcnt / qtau are zero at rest (cleared by sel_fin_kernel), which takes T =
+// the k'-th largest listed key and accepts it when T >= tau (then every key
+// >= T of the row is listed, so T is exact); otherwise it selects over the
+// whole row.
+// ---------------------------------------------------------------------
+constexpr int kStrThreads = 256;
+constexpr int kStrKpt = 16;
+constexpr int kStrSample = kStrThreads * kStrKpt;  // 4096
+constexpr int kStrSegMax = 1024;                   // keys staged per CTA
+constexpr int kStrMaxChunks = 64;
+constexpr int kStrFastRank = 128;                  // r_s up to this: bound from the per-thread maxima
+
+__device__ __forceinline__ unsigned long long ld_relaxed_gpu_u64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ uint64_t shfl_xor_u64(uint64_t v, int m) {
+  return static_cast<uint64_t>(__shfl_xor_sync(0xffffffffu, static_cast<unsigned long long>(v), m));
+}
+
+// r-th largest (1-based, r <= 256) of one key per thread over a 256-thread
+// CTA; s_sorted: [8][32] u64. Keys are unique or 0 (padding, ranks last).
+__device__ __forceinline__ uint64_t block256_rank_of_maxima(uint64_t x, int r, uint64_t* s_sorted, uint64_t* s_res) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+#pragma unroll
+  for (int k = 2; k <= 32; k <<= 1) {
+#pragma unroll
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      const uint64_t o = shfl_xor_u64(x, j);
+      const bool keep_max = ((lane & j) == 0) == ((lane & k) == 0);
+      x = keep_max ? (x > o ? x : o) : (x < o ? x : o);
+    }
+  }
+  s_sorted[wid * 32 + lane] = x;  // descending by lane
+  if (threadIdx.x == 0) *s_res = 0ull;
+  __syncthreads();
+  int rank = lane;  // own list: keys above x
+#pragma unroll
+  for (int w = 0; w < 8; ++w) {  // (unrolled: the 7 searches are independent; rolled measured 0.6 us slower)
+    if (w == wid) continue;
+    const uint64_t* a = s_sorted + w * 32;
+    int pos = 0;
+#pragma unroll
+    for (int step = 16; step > 0; step >>= 1)
+      if (a[pos + step - 1] > x) pos += step;
+    if (a[pos] > x) ++pos;
+    rank += pos;
+  }
+  if (x != 0ull && rank == r - 1) *s_res = x;
+  __syncthreads();
+  return *s_res;
+}
+
+__global__ void __launch_bounds__(kStrThreads, 4) sel_stream_kernel(
+    const float* __restrict__ scores, int64_t stride, uint32_t n, uint32_t r_s, uint32_t seg,
+    unsigned* __restrict__ qcnt, unsigned long long* __restrict__ qtau, uint64_t* __restrict__ lists,
+    int64_t list_stride, unsigned* __restrict__ ticket) {
+  constexpr int NT = kStrThreads, NW = NT / 32, U = kStrKpt / 4;
+  __shared__ RangeScratch rs;
+  __shared__ uint64_t s_keys[kStrSegMax];
+  __shared__ unsigned s_n;
+  __shared__ uint64_t s_res;
+  __shared__ int s_ticket;
+  hire_dev::griddep_wait();
+  KTrace kt_(kKtWindow);
+  const int b = blockIdx.y, C = gridDim.x, c = blockIdx.x;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  bool dbg = g_ktrace && threadIdx.x == 0 && b == 0;
+  const float* row = scores + b * stride;
+  const uint32_t G = (n + 127u) >> 7;
+  // granule q of this warp's sequence: g = c + C * (wid + NW * q)
+  auto gran = [&](uint32_t q) -> uint32_t { return static_cast<uint32_t>(c) + static_cast<uint32_t>(C) * (wid + NW * q); };
+  auto load4 = [&](uint32_t g) -> float4 {
+    const uint32_t i = (g << 7) + (lane << 2);
+    if (g < G && i + 3 < n) return *reinterpret_cast<const float4*>(row + i);
+    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (g < G) {
+      if (i < n) v.x = row[i];
+      if (i + 1 < n) v.y = row[i + 1];
+      if (i + 2 < n) v.z = row[i + 2];
+    }
+    return v;
+  };
+  float4 v0[U], v1[U];
+#pragma unroll
+  for (int u = 0; u < U; ++u) v0[u] = load4(gran(u));
+#pragma unroll
+  for (int u = 0; u < U; ++u) v1[u] = load4(gran(U + u));
+  // element e of granule g held by this lane
+  auto idx_of = [&](uint32_t g, int e) -> uint32_t { return (g << 7) + (lane << 2) + e; };
+  auto elem = [](const float4& v, int e) -> float { return e == 0 ? v.x : e == 1 ? v.y : e == 2 ? v.z : v.w; };
+  // the loads are in flight; now the role: the first CTA of the query to
+  // arrive samples (its own chunk), the others wait for its bound
+  if (threadIdx.x == 0) {
+    const unsigned t = atomicAdd(ticket + b, 1u);
+    if (t == static_cast<unsigned>(C) - 1u) ticket[b] = 0u;  // every CTA of the query arrived: back to zero
+    s_ticket = static_cast<int>(t);
+    s_n = 0;
+  }
+  __syncthreads();
+  const bool sampler = s_ticket == 0;
+  dbg = dbg && sampler;
+  if (dbg) g_ktrace[70] = gtimer();
+  uint64_t tau = 1ull;  // fewer sample keys than the rank: list every key
+  bool late = false;    // the bound never arrived (the sampler always runs first: bounded wait all the same)
+  if (sampler) {
+    // valid sample keys: the chunk's first NW * U granules, all full but
+    // possibly the row's last one
+    long long n_in = 0;
+    if (static_cast<uint32_t>(c) < G) {
+      const uint32_t own = (G - 1u - c) / C + 1u;  // granules of this chunk
+      const uint32_t ns = min(own, static_cast<uint32_t>(NW * U));
+      n_in = static_cast<long long>(ns) * 128;
+      const uint32_t tail = n & 127u;
+      if (tail && (G - 1u - c) % C == 0u && (G - 1u - c) / C < static_cast<uint32_t>(NW * U)) n_in -= 128 - tail;
+    }
+    if (dbg) g_ktrace[71] = gtimer() + (v0[0].x == 77.125f);
+    if (n_in >= static_cast<long long>(r_s)) {
+      if (r_s <= static_cast<uint32_t>(kStrFastRank)) {
+        // this thread's largest sample key: the maximum value, lowest index on ties
+        float best = 0.0f;
+        uint32_t bi = 0xFFFFFFFFu;
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const uint32_t g = gran(u);
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const uint32_t i = idx_of(g, e);
+            const float v = elem(v0[u], e);
+            const bool ok = g < G && i < n;
+            if (ok && (bi == 0xFFFFFFFFu || v > best)) {
+              best = v;
+              bi = i;
+            }
+          }
+        }
+        const uint64_t mx = bi == 0xFFFFFFFFu ? 0ull : make_key(best, bi);
+        tau = block256_rank_of_maxima(mx, static_cast<int>(r_s), rs.ckeys, &s_res);
+      } else {
+        RegKeys<kStrKpt> smp;
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const uint32_t g = gran(u);
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const uint32_t i = idx_of(g, e);
+            smp.k[4 * u + e] = (g < G && i < n) ? make_key(elem(v0[u], e), i) : 0ull;
+          }
+        }
+        tau = block_range_select<NT>(smp, n_in, r_s, &rs);
+      }
+    }
+    // drop the index part: every key with tau's value word is listed, and the
+    // scan needs only a float compare
+    tau = (tau >> 32) << 32;
+    if (tau == 0ull) tau = 1ull;  // (also: fewer than r_s threads held a valid key)
+    if (threadIdx.x == 0) atomicExch(qtau + b, static_cast<unsigned long long>(tau));  // performed at L2
+  } else {
+    if (threadIdx.x == 0) {
+      unsigned long long t = 0ull;
+      const unsigned long long t0 = gtimer();
+      while ((t = ld_relaxed_gpu_u64(qtau + b)) == 0ull) {
+        if (gtimer() - t0 > 20000000ull) break;  // 20 ms
+        __nanosleep(64);
+      }
+      s_res = t;
+    }
+    __syncthreads();
+    tau = s_res;
+    if (tau == 0ull) {
+      late = true;
+      tau = ~0ull;  // the finisher falls back
+    }
+  }
+  if (dbg) g_ktrace[72] = gtimer() + (tau == 77ull);
+  // keys >= tau -> the CTA's stage. tau carries no index part, so for real
+  // scores key >= tau <=> !(x < tv) (NaN is listed too: harmless, the finisher
+  // checks T >= tau). The streaming loop only records hits, one bit per key,
+  // 64 keys (16 granules) per lane at a time; a block's hits are then written
+  // with one warp scan and one shared atomic per warp, their values re-read
+  // by index (L1).
+  const float tv = key_value(tau);
+  uint64_t mask = 0ull;
+  auto hits4 = [&](const float4& v, uint32_t g) -> unsigned {
+    if (g >= G) return 0u;
+    unsigned h = (!(v.x < tv) ? 1u : 0u) | (!(v.y < tv) ? 2u : 0u) | (!(v.z < tv) ? 4u : 0u) | (!(v.w < tv) ? 8u : 0u);
+    if ((g << 7) + 128u > n) {  // the row's last, partial granule
+      const uint32_t i = idx_of(g, 0);
+      h &= i + 3 < n ? 15u : i + 2 < n ? 7u : i + 1 < n ? 3u : i < n ? 1u : 0u;
+    }
+    return h;
+  };
+  auto flush = [&](uint32_t qbase) {  // hits of granules qbase .. qbase + 15 of this warp's sequence
+    const int cn = __popcll(mask);
+    if (__any_sync(0xffffffffu, cn != 0)) {
+      int inc = cn;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int t = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += t;
+      }
+      unsigned base = 0;
+      if (lane == 31) base = atomicAdd(&s_n, static_cast<unsigned>(inc));
+      base = __shfl_sync(0xffffffffu, base, 31);
+      unsigned pos = base + static_cast<unsigned>(inc - cn);
+      while (mask) {
+        const int p = __ffsll(static_cast<long long>(mask)) - 1;
+        mask &= mask - 1ull;
+        const uint32_t i = idx_of(gran(qbase + (p >> 2)), p & 3);
+        if (pos < seg) s_keys[pos] = make_key(row[i], i);
+        ++pos;
+      }
+    }
+    mask = 0ull;
+  };
+#pragma unroll
+  for (int u = 0; u < U; ++u) mask |= static_cast<uint64_t>(hits4(v0[u], gran(u))) << (4 * u);
+  // the rest of the CTA's granules, one batch of loads ahead
+  uint32_t qb = 0;  // first granule of the current 16-granule block
+  for (uint32_t q0 = U; gran(q0) < G; q0 += U) {  // warp-uniform bound: gran() depends on wid and q only
+    if (q0 - qb == 16u) {
+      flush(qb);
+      qb = q0;
+    }
+    float4 cur[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) cur[u] = v1[u];
+#pragma unroll
+    for (int u = 0; u < U; ++u) v1[u] = load4(gran(q0 + U + u));
+#pragma unroll
+    for (int u = 0; u < U; ++u) mask |= static_cast<uint64_t>(hits4(cur[u], gran(q0 + u))) << (4 * (q0 - qb + u));
+  }
+  flush(qb);
+  hire_dev::griddep_launch();  // late: the finisher's 1024-thread CTAs must not take SMs from this grid
+  __syncthreads();
+  if (dbg) g_ktrace[73] = gtimer();
+  const unsigned total = s_n;
+  const unsigned staged = min(total, seg);
+  uint64_t* L = lists + static_cast<int64_t>(b) * list_stride + static_cast<int64_t>(c) * seg;
+  for (unsigned t = threadIdx.x; t < seg; t += NT) L[t] = t < staged ? s_keys[t] : 0ull;
+  if (threadIdx.x == 0) atomicAdd(qcnt + b, (total > seg || late) ? 0x80000000u : total);  // bit 31: fall back
+  if (dbg) g_ktrace[74] = gtimer();
+}
+
+// ---------------------------------------------------------------------
 // S2b. One 256-thread CTA per query: window counts -> r = K - above; the
 // window keys are pulled from the chunk segments (position -> chunk by
 // binary search over the prefix counts) and the r-th largest is T.
@@ -1115,12 +1379,15 @@ __global__ void __launch_bounds__(NT) final2_kernel(
   for (int v = 0; v < NT / 32; ++v) n_valid += s_scan[v];
   __syncthreads();
   const int Kq = min(K, n_valid);
+  const bool dbg = g_ktrace && threadIdx.x == 0 && b == 0;
+  if (dbg) g_ktrace[76] = gtimer();
   // K >= pool: everything is selected (no order statistic needed)
   const uint64_t T = Kq >= n_valid ? 1ull : (Kq >= 1 ? block_range_select<NT>(src, n_valid, Kq, &rs) : ~0ull);
   int c = 0;
 #pragma unroll
   for (int j = 0; j < KPT; ++j) c += (src.k[j] && src.k[j] >= T) ? 1 : 0;
   int total;
+  if (dbg) g_ktrace[77] = gtimer() + (T == 12345ull);
   int pos = block_scan_excl<NT>(c, s_scan, &total);
   if (out_mode == 1) {
 #pragma unroll
@@ -1174,6 +1441,7 @@ __global__ void __launch_bounds__(NT) final2_kernel(
       }
     }
   }
+  if (dbg) g_ktrace[78] = gtimer();
   for (int i = threadIdx.x; i < Kq; i += NT) {
     out_idx[b * out_stride + i] = key_index(s_sel[i]);
     out_val[b * out_stride + i] = key_value(s_sel[i]);
@@ -1195,6 +1463,7 @@ __global__ void __launch_bounds__(NT) final2_kernel(
       out_prob[b * out_stride + j] = static_cast<float>(static_cast<double>(pj) / sum);
     }
   }
+  if (dbg) g_ktrace[79] = gtimer();
 }
 
 }  // namespace hire_dev

@@ -20,14 +20,15 @@ import bench  # noqa: E402
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--workload", default="cfg2", choices=["cfg1", "cfg2", "cfg3", "cfg4"])
+    ap.add_argument("--workload", default="cfg2", choices=["cfg1", "cfg2", "cfg3", "cfg4", "cfg5"])
     ap.add_argument("--batch", type=int, default=0)
     ap.add_argument("--select", default="exact")
     ap.add_argument("--reps", type=int, default=3)
     args = ap.parse_args()
     import paper_2402_09360_b200 as H
     H.lib()
-    wl = bench.make_workload(H, args)
+    wl = bench.make_workload(args)
+    wl.attach(H)
     xs = wl.inputs(8)
     cs = torch.cuda.Stream()
     with torch.cuda.stream(cs):
