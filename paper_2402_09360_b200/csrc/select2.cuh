@@ -804,11 +804,11 @@ __global__ void __launch_bounds__(kWinThreads) sel_wlist_kernel(
 // any CTA that waits on it, whatever the dispatch order. The sampler's first
 // 4096 keys (16 per thread) are the sample: tau <= the sample's rank-r_s key
 // (r_s ~ k'/n * 4096 + margin, chosen on the host so that P[tau > T] ~ 1e-7
-// for exchangeable rows). Small r_s: tau = the r_s-th largest of the 256
-// per-thread sample maxima (r_s distinct threads hold a key >= it; a warp
-// bitonic sort of the maxima, then a rank by binary search over the 8 sorted
-// lists — two barriers). Otherwise the exact order statistic
-// (block_range_select). tau, stripped of its index part, is published with an
+// for exchangeable rows; r_s <= 128, larger ranks take the pivot + list
+// kernels): tau = the r_s-th largest of the 256 per-thread sample maxima
+// (r_s distinct threads hold a key >= it; a warp bitonic sort of the maxima,
+// then a rank by binary search over the 8 sorted lists — two barriers).
+// tau, stripped of its index part, is published with an
 // atomic on qtau[b]; the other CTAs of the query have their first two batches
 // of loads in flight while they poll it. Every key >= tau of a chunk goes to
 // its own list segment lists[b][c*seg ...], zero-padded to seg; qcnt[b] +=
@@ -873,7 +873,7 @@ __global__ void __launch_bounds__(kStrThreads, 4) sel_stream_kernel(
     unsigned* __restrict__ qcnt, unsigned long long* __restrict__ qtau, uint64_t* __restrict__ lists,
     int64_t list_stride, unsigned* __restrict__ ticket) {
   constexpr int NT = kStrThreads, NW = NT / 32, U = kStrKpt / 4;
-  __shared__ RangeScratch rs;
+  __shared__ uint64_t s_sorted[NT];
   __shared__ uint64_t s_keys[kStrSegMax];
   __shared__ unsigned s_n;
   __shared__ uint64_t s_res;
@@ -933,39 +933,25 @@ __global__ void __launch_bounds__(kStrThreads, 4) sel_stream_kernel(
     }
     if (dbg) g_ktrace[71] = gtimer() + (v0[0].x == 77.125f);
     if (n_in >= static_cast<long long>(r_s)) {
-      if (r_s <= static_cast<uint32_t>(kStrFastRank)) {
-        // this thread's largest sample key: the maximum value, lowest index on ties
-        float best = 0.0f;
-        uint32_t bi = 0xFFFFFFFFu;
+      // this thread's largest sample key: the maximum value, lowest index on ties
+      float best = 0.0f;
+      uint32_t bi = 0xFFFFFFFFu;
 #pragma unroll
-        for (int u = 0; u < U; ++u) {
-          const uint32_t g = gran(u);
+      for (int u = 0; u < U; ++u) {
+        const uint32_t g = gran(u);
 #pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            const uint32_t i = idx_of(g, e);
-            const float v = elem(v0[u], e);
-            const bool ok = g < G && i < n;
-            if (ok && (bi == 0xFFFFFFFFu || v > best)) {
-              best = v;
-              bi = i;
-            }
+        for (int e = 0; e < 4; ++e) {
+          const uint32_t i = idx_of(g, e);
+          const float v = elem(v0[u], e);
+          const bool ok = g < G && i < n;
+          if (ok && (bi == 0xFFFFFFFFu || v > best)) {
+            best = v;
+            bi = i;
           }
         }
-        const uint64_t mx = bi == 0xFFFFFFFFu ? 0ull : make_key(best, bi);
-        tau = block256_rank_of_maxima(mx, static_cast<int>(r_s), rs.ckeys, &s_res);
-      } else {
-        RegKeys<kStrKpt> smp;
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-          const uint32_t g = gran(u);
-#pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            const uint32_t i = idx_of(g, e);
-            smp.k[4 * u + e] = (g < G && i < n) ? make_key(elem(v0[u], e), i) : 0ull;
-          }
-        }
-        tau = block_range_select<NT>(smp, n_in, r_s, &rs);
       }
+      const uint64_t mx = bi == 0xFFFFFFFFu ? 0ull : make_key(best, bi);
+      tau = block256_rank_of_maxima(mx, static_cast<int>(r_s), s_sorted, &s_res);
     }
     // drop the index part: every key with tau's value word is listed, and the
     // scan needs only a float compare
@@ -1055,7 +1041,10 @@ __global__ void __launch_bounds__(kStrThreads, 4) sel_stream_kernel(
   const unsigned staged = min(total, seg);
   uint64_t* L = lists + static_cast<int64_t>(b) * list_stride + static_cast<int64_t>(c) * seg;
   for (unsigned t = threadIdx.x; t < seg; t += NT) L[t] = t < staged ? s_keys[t] : 0ull;
-  if (threadIdx.x == 0) atomicAdd(qcnt + b, (total > seg || late) ? 0x80000000u : total);  // bit 31: fall back
+  if (threadIdx.x == 0) {
+    if (total > seg || late) atomicOr(qcnt + b, 0x80000000u);  // the finisher falls back (an Or: several chunks may overflow)
+    else atomicAdd(qcnt + b, total);
+  }
   if (dbg) g_ktrace[74] = gtimer();
 }
 
