@@ -113,6 +113,120 @@ __global__ void __launch_bounds__(256, (CPL >= 16 ? 1 : 2)) recompute_fast(
   }
 }
 
+// ---------------------------------------------------------------------
+// K4U — batch-union gather recompute (the device counterpart of
+// union_group_select's premise, ffn.hpp:237-253: a row selected by several
+// inputs of the batch is fetched once). For batches whose candidate lists
+// overlap heavily (FFN layers: B * k' >> rows) the per-query gather moves
+// every row once per query that selected it through L2; here each unique row
+// leaves L2 once.
+//   U1 union_mark_kernel   rowmask[r] |= 1 << b for every candidate (b, r)
+//   U2 union_dot_kernel    grid (CPL column slices, row tiles). A slice is 512
+//        bytes of every row (one 16-byte vector per lane — the same lane /
+//        column assignment as recompute_fast's chunk c). The CTA holds the
+//        slice of x for all B queries in shared memory (B * 512/sizeof(T) * 4
+//        bytes); a warp takes a row with a non-empty mask, loads its slice
+//        once, and for each query of the mask does the lane FMAs in column
+//        order and the fixed butterfly -> part[b][r][slice].
+//   U3 union_gather_kernel out[b][j] = phi(sum over slices, ascending, of
+//        part[b][cand[b][j]][slice]); clears rowmask (zero at rest).
+// Fixed order, so deterministic and independent of the batch composition;
+// the association differs from recompute_fast's (per-slice butterflies, then
+// the slice sum), so values agree with the per-query path to fp32 rounding
+// (~1e-7 relative), not bit for bit. Fast mode only.
+//
+// Experiments build only (negative result on B200, cfg2 shape, bf16): one
+// FFN layer at B = 8 / 16 / 32 / 64 takes 39 / 50 / 62 / 90 us with the
+// per-query gather and 50 / 66 / 90 / 149 us with this path. The per-query
+// kernels already read each unique row from HBM once — L2 holds the layer
+// (ncu, profiles/r02c_ffn_gather_dram_b*.csv: recompute_fast reads 18.6 MB
+// from DRAM at B=8 for 18.9 MB of unique rows, 34.2 MB at B=64 for 33.5 MB,
+// while L2 serves 40 / 242 MB) — and they amortise the butterfly and the loop
+// overhead over a whole row (~24 instructions per 512-byte slice of a pair)
+// where this kernel pays them per slice (73; ncu: 30.7 M warp instructions,
+// short-scoreboard bound).
+// ---------------------------------------------------------------------
+#if HIRE_EXPERIMENTS
+__global__ void __launch_bounds__(256) union_mark_kernel(const uint32_t* __restrict__ cand, int64_t cand_stride,
+                                                         int n_cand, int B, unsigned long long* __restrict__ rowmask) {
+  hire_dev::griddep_wait();
+  hire_dev::griddep_launch();
+  const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (t >= static_cast<int64_t>(B) * n_cand) return;
+  const int b = static_cast<int>(t / n_cand), j = static_cast<int>(t % n_cand);
+  atomicOr(rowmask + cand[b * cand_stride + j], 1ull << b);
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256) union_dot_kernel(const T* __restrict__ w, int d, int64_t rows,
+                                                        const unsigned long long* __restrict__ rowmask,
+                                                        const float* __restrict__ x, int B, int rows_per_cta,
+                                                        float* __restrict__ part) {
+  constexpr int E = Vec16<T>::kElems;
+  constexpr int DC = 32 * E;  // columns per slice
+  extern __shared__ __align__(16) unsigned char smem[];
+  float* s_x = reinterpret_cast<float*>(smem);  // [B][DC]
+  hire_dev::griddep_wait();
+  hire_dev::griddep_launch();
+  KTrace kt_(kKtRecompute);
+  const int ct = blockIdx.x, nct = gridDim.x;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  for (int i = threadIdx.x; i < B * (DC / 4); i += blockDim.x) {
+    const int b = i / (DC / 4), q = i % (DC / 4);
+    reinterpret_cast<float4*>(s_x)[i] =
+        *reinterpret_cast<const float4*>(x + static_cast<int64_t>(b) * d + static_cast<int64_t>(ct) * DC + 4 * q);
+  }
+  __syncthreads();
+  const int64_t pitch_vec = static_cast<int64_t>(d) / E;
+  const int64_t r0 = static_cast<int64_t>(blockIdx.y) * rows_per_cta;
+  const int64_t r1 = min(rows, r0 + rows_per_cta);
+  // two rows per warp in flight: the next row's mask and slice are fetched
+  // before this row's arithmetic
+  int64_t r = r0 + wid;
+  unsigned long long m_next = r < r1 ? rowmask[r] : 0ull;
+  uint4 v_next = make_uint4(0, 0, 0, 0);
+  if (m_next) v_next = ldg_stream(reinterpret_cast<const uint4*>(w) + r * pitch_vec + static_cast<int64_t>(ct) * 32 + lane);
+  for (; r < r1; r += 8) {
+    unsigned long long m = m_next;
+    const uint4 v = v_next;
+    const int64_t rn = r + 8;
+    m_next = rn < r1 ? rowmask[rn] : 0ull;
+    if (m_next) v_next = ldg_stream(reinterpret_cast<const uint4*>(w) + rn * pitch_vec + static_cast<int64_t>(ct) * 32 + lane);
+    if (!m) continue;
+    float f[E];
+    Vec16<T>::expand(v, f);
+    while (m) {
+      const int b = __ffsll(static_cast<long long>(m)) - 1;
+      m &= m - 1ull;
+      float xv[E];
+      load_x_vec<E>(s_x + b * DC + lane * E, xv);
+      float acc = 0.0f;
+#pragma unroll
+      for (int e = 0; e < E; ++e) acc = fmaf(f[e], xv[e], acc);
+      acc = warp_sum_f32(acc);
+      if (lane == 0) part[(static_cast<int64_t>(b) * rows + r) * nct + ct] = acc;
+    }
+  }
+}
+
+__global__ void __launch_bounds__(256) union_gather_kernel(const float* __restrict__ part, int64_t rows, int nct,
+                                                           const uint32_t* __restrict__ cand, int64_t cand_stride,
+                                                           int n_cand, int B, int phi, float* __restrict__ out,
+                                                           int64_t out_stride, unsigned long long* __restrict__ rowmask) {
+  hire_dev::griddep_wait();
+  hire_dev::griddep_launch();
+  const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (t >= static_cast<int64_t>(B) * n_cand) return;
+  const int b = static_cast<int>(t / n_cand), j = static_cast<int>(t % n_cand);
+  const int64_t r = cand[b * cand_stride + j];
+  const float* p = part + (static_cast<int64_t>(b) * rows + r) * nct;
+  float acc = 0.0f;
+  for (int c = 0; c < nct; ++c) acc = __fadd_rn(acc, __ldcg(p + c));
+  out[b * out_stride + j] = apply_phi(phi, acc);
+  rowmask[r] = 0ull;  // zero at rest (every selecting query writes the same zero)
+}
+#endif  // HIRE_EXPERIMENTS (K4U)
+
 #if HIRE_EXPERIMENTS
 // Same arithmetic as recompute_fast (lane chunk order, fmaf order, fixed
 // butterfly -> bit-identical values), but the gathered rows are moved by

@@ -101,6 +101,10 @@ struct hire_ctx_s {
   size_t selc_cap = 0;
   void* fzero = nullptr;     // zero-at-rest sample slots + bounds of the fused selector (fsel.cuh)
   size_t fzero_cap = 0;
+  unsigned long long* umask = nullptr;  // zero-at-rest row masks of the batch-union gather (exact.cuh K4U)
+  size_t umask_cap = 0;                 // rows
+  void* upart = nullptr;                // its per-slice partial sums [B][rows][slices]
+  size_t upart_cap = 0;
   // host-buffer calls (*_host): after one eager call per shape, the whole
   // call — H2D copy, kernel chain, D2H copy — replays as one CUDA graph on
   // gstream. An entry is valid while every buffer it captured is unchanged.
@@ -136,7 +140,7 @@ struct hire_ctx_s {
   bool host_graphs = true;
   cudaStream_t gstream = nullptr;
   cudaEvent_t gev = nullptr;
-  std::vector<const void*> buf_snapshot() const { return {ws, io_dev, io_host, selc, fzero, counters, tickets}; }
+  std::vector<const void*> buf_snapshot() const { return {ws, io_dev, io_host, selc, fzero, counters, tickets, umask, upart}; }
   // stage profiling (hire_ctx_set_profiling): event pairs around each stage
   bool prof = false;
   std::vector<cudaEvent_t> ev_pool;
@@ -347,6 +351,20 @@ int ensure_fzero(hire_ctx ctx, int64_t B) {
   CK(cudaMalloc(&ctx->fzero, nb));
   CK(cudaMemsetAsync(ctx->fzero, 0, nb, ctx->stream));
   ctx->fzero_cap = nb;
+  return HIRE_OK;
+}
+
+int ensure_umask(hire_ctx ctx, int64_t rows) {
+  if (static_cast<size_t>(rows) <= ctx->umask_cap) return HIRE_OK;
+  if (ctx->umask) {
+    CK(cudaStreamSynchronize(ctx->stream));
+    CK(cudaFree(ctx->umask));
+    ctx->umask = nullptr;
+  }
+  const size_t n = std::max<size_t>(static_cast<size_t>(rows), 2 * ctx->umask_cap);
+  CK(cudaMalloc(&ctx->umask, n * 8));
+  CK(cudaMemsetAsync(ctx->umask, 0, n * 8, ctx->stream));
+  ctx->umask_cap = n;
   return HIRE_OK;
 }
 
@@ -1067,6 +1085,59 @@ int launch_recompute_tma(hire_ctx ctx, const void* w, int d, const uint32_t* can
 // phi(<W_row, x_b>) for rows cand[b][i] (or i when cand == nullptr).
 #endif
 
+#if HIRE_EXPERIMENTS
+// Batch-union gather (exact.cuh K4U), opt-in with HIRE_UNION=1: measured
+// slower than the per-query gather at every batch (see exact.cuh).
+bool union_gather_pays(hire_ctx ctx, const hire_matrix_s* m, int64_t n_cand, int64_t B) {
+  (void)ctx;
+  (void)n_cand;
+  const int64_t nct = m->d * static_cast<int64_t>(dtype_size(m->dtype)) / 512;
+  if (B < 2 || B > 64 || nct < 1 || B * m->rows * nct * 4 > (int64_t{64} << 20)) return false;
+  const char* e = std::getenv("HIRE_UNION");
+  return e && e[0] == '1';
+}
+
+int run_recompute_union(hire_ctx ctx, const hire_matrix_s* m, const uint32_t* cand, int64_t cand_stride,
+                        int64_t n_cand, const float* x, int64_t B, int phi, float* out, int64_t out_stride) {
+  using namespace hire_dev;
+  const int d = static_cast<int>(m->d);
+  const bool bf = m->dtype == HIRE_BF16;
+  const int nct = static_cast<int>(m->d * static_cast<int64_t>(dtype_size(m->dtype)) / 512);
+  const int dc = bf ? 256 : 128;
+  RET(ensure_umask(ctx, m->rows));
+  // the partial sums live behind the caller's arena allocations: a
+  // context-owned grow-only buffer of their own
+  const size_t need = static_cast<size_t>(B) * m->rows * nct * 4;
+  RET(ensure(&ctx->upart, &ctx->upart_cap, need, ctx->stream));
+  float* part = static_cast<float*>(ctx->upart);
+  const unsigned pairs_blocks = static_cast<unsigned>(ceil_div(B * n_cand, 256));
+  CK(launch_k(ctx, union_mark_kernel, pairs_blocks, 256, 0, cand, cand_stride, static_cast<int>(n_cand),
+              static_cast<int>(B), ctx->umask));
+  // row tiles: about 4 CTAs per SM over the nct slices, at least 64 rows each
+  const int64_t tiles = std::max<int64_t>(1, std::min<int64_t>(ceil_div(m->rows, 64), 4 * ctx->num_sms / nct));
+  const int rows_per_cta = static_cast<int>(ceil_div(m->rows, tiles));
+  const size_t smem = static_cast<size_t>(B) * dc * 4;
+  if (bf) {
+    static bool attr = false;
+    if (!attr) {
+      CK(cudaFuncSetAttribute(union_dot_kernel<__nv_bfloat16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 256 * 4));
+      attr = true;
+    }
+    CK(launch_k(ctx, union_dot_kernel<__nv_bfloat16>, dim3(static_cast<unsigned>(nct), static_cast<unsigned>(ceil_div(m->rows, rows_per_cta))),
+                256, smem, static_cast<const __nv_bfloat16*>(m->ptr), d, m->rows,
+                static_cast<const unsigned long long*>(ctx->umask), x, static_cast<int>(B), rows_per_cta, part));
+  } else {
+    CK(launch_k(ctx, union_dot_kernel<float>, dim3(static_cast<unsigned>(nct), static_cast<unsigned>(ceil_div(m->rows, rows_per_cta))),
+                256, smem, static_cast<const float*>(m->ptr), d, m->rows,
+                static_cast<const unsigned long long*>(ctx->umask), x, static_cast<int>(B), rows_per_cta, part));
+  }
+  CK(launch_k(ctx, union_gather_kernel, pairs_blocks, 256, 0, static_cast<const float*>(part), m->rows, nct, cand,
+              cand_stride, static_cast<int>(n_cand), static_cast<int>(B), phi, out, out_stride, ctx->umask));
+  CK(cudaGetLastError());
+  return HIRE_OK;
+}
+#endif  // HIRE_EXPERIMENTS
+
 int run_recompute(hire_ctx ctx, const hire_matrix_s* m, const uint32_t* cand, int64_t cand_stride,
                   int64_t n_cand, const float* x, int64_t B, int phi, int strict, float* out,
                   int64_t out_stride) {
@@ -1088,6 +1159,10 @@ int run_recompute(hire_ctx ctx, const hire_matrix_s* m, const uint32_t* cand, in
       RET(launch_recompute_tma<float>(ctx, m->ptr, d, cand, cand_stride, n_cand, x, B, phi, out, out_stride, &done));
     if (done) return HIRE_OK;
   }
+#endif
+#if HIRE_EXPERIMENTS
+  if (!strict && bytes % 512 == 0 && cand && union_gather_pays(ctx, m, n_cand, B))
+    return run_recompute_union(ctx, m, cand, cand_stride, n_cand, x, B, phi, out, out_stride);
 #endif
   if (!strict && bytes % 512 == 0) {
     const int cpl = static_cast<int>(bytes / 512);
@@ -1803,6 +1878,8 @@ int hire_ctx_destroy(hire_ctx c) {
   if (c->selc) cudaFree(c->selc);
   if (c->tickets) cudaFree(c->tickets);
   if (c->fzero) cudaFree(c->fzero);
+  if (c->umask) cudaFree(c->umask);
+  if (c->upart) cudaFree(c->upart);
   if (c->io_dev) cudaFree(c->io_dev);
   if (c->io_host) cudaFreeHost(c->io_host);
   for (auto& g : c->hgraphs) cudaGraphExecDestroy(g.exec);
