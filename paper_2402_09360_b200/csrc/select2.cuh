@@ -1400,12 +1400,27 @@ __global__ void __launch_bounds__(NT) final2_kernel(
   for (int j = 0; j < KPT; ++j)
     if (src.k[j] && src.k[j] >= T) s_sel[pos++] = src.k[j];
   __syncthreads();
-  if (Kq <= NT && Kq <= 256) {
-    // rank = number of selected keys greater (keys unique)
-    const uint64_t mine = threadIdx.x < Kq ? s_sel[threadIdx.x] : 0ull;
-    int rank = 0;
+  if (Kq >= 1 && Kq <= NT && Kq <= 256) {
+    // rank = number of selected keys greater (keys unique). The Kq x Kq
+    // compares are spread over the whole CTA: thread t takes key t % Kq and
+    // the t / Kq-th segment of the list, partial ranks meet in shared memory
+    // (a single thread per key walks the list at one dependent shared load
+    // per step: 1.8 us for 64 keys, 4.1 us for 128).
+    int* s_rank = reinterpret_cast<int*>(rs.ckeys);  // the select is done with its scratch
+    const int S = NT / Kq, len = (Kq + S - 1) / S;
+    for (int i = threadIdx.x; i < Kq; i += NT) s_rank[i] = 0;
+    __syncthreads();
+    if (threadIdx.x < Kq * S) {
+      const int i = threadIdx.x % Kq, j0 = (threadIdx.x / Kq) * len, j1 = min(Kq, j0 + len);
+      const uint64_t mine = s_sel[i];
+      int r = 0;
 #pragma unroll 4
-    for (int j = 0; j < Kq; ++j) rank += s_sel[j] > mine;
+      for (int j = j0; j < j1; ++j) r += s_sel[j] > mine;
+      if (r) atomicAdd(&s_rank[i], r);
+    }
+    __syncthreads();
+    const uint64_t mine = threadIdx.x < Kq ? s_sel[threadIdx.x] : 0ull;
+    const int rank = threadIdx.x < Kq ? s_rank[threadIdx.x] : 0;
     __syncthreads();
     if (threadIdx.x < Kq) s_sel[rank] = mine;
     __syncthreads();
@@ -1438,8 +1453,17 @@ __global__ void __launch_bounds__(NT) final2_kernel(
   if (out_prob) {
     // hire.hpp:135-142: p_i = float(exp(double(v_i) - v_max)) / double sum
     const double vmax = static_cast<double>(key_value(s_sel[0]));
+    // one exp per element when every thread holds at most one (the usual
+    // case); the sum keeps its order: per-thread terms, butterfly, warps ascending
+    const bool one = Kq <= NT;
+    double mine_e = 0.0;
     double local = 0.0;
-    for (int j = threadIdx.x; j < Kq; j += NT) local += exp(static_cast<double>(key_value(s_sel[j])) - vmax);
+    if (one) {
+      if (threadIdx.x < Kq) mine_e = exp(static_cast<double>(key_value(s_sel[threadIdx.x])) - vmax);
+      local = mine_e;
+    } else {
+      for (int j = threadIdx.x; j < Kq; j += NT) local += exp(static_cast<double>(key_value(s_sel[j])) - vmax);
+    }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) local += __shfl_xor_sync(0xffffffffu, local, o);
     if ((threadIdx.x & 31) == 0) s_red[threadIdx.x >> 5] = local;
@@ -1447,9 +1471,15 @@ __global__ void __launch_bounds__(NT) final2_kernel(
     double sum = 0.0;
 #pragma unroll
     for (int v = 0; v < NT / 32; ++v) sum += s_red[v];
-    for (int j = threadIdx.x; j < Kq; j += NT) {
-      const float pj = static_cast<float>(exp(static_cast<double>(key_value(s_sel[j])) - vmax));
-      out_prob[b * out_stride + j] = static_cast<float>(static_cast<double>(pj) / sum);
+    if (one) {
+      if (threadIdx.x < Kq)
+        out_prob[b * out_stride + threadIdx.x] =
+            static_cast<float>(static_cast<double>(static_cast<float>(mine_e)) / sum);
+    } else {
+      for (int j = threadIdx.x; j < Kq; j += NT) {
+        const float pj = static_cast<float>(exp(static_cast<double>(key_value(s_sel[j])) - vmax));
+        out_prob[b * out_stride + j] = static_cast<float>(static_cast<double>(pj) / sum);
+      }
     }
   }
   if (dbg) g_ktrace[79] = gtimer();
