@@ -1198,6 +1198,24 @@ int run_final(hire_ctx ctx, const float* vals, int64_t vs, const uint32_t* idx, 
   int64_t P = 1;
   while (P < K) P <<= 1;
   const size_t smem = out_mode == 0 ? static_cast<size_t>(P) * 8 : 0;
+  // ranked top-k of a small pool, a few queries: per-warp register sort +
+  // merge tree (final3_kernel). Measured (cfg3, n = 1024, K = 64): B = 1 step
+  // 67.7 -> 65.5 us, but B = 8 83.9 -> 85.7 and B = 32 107.5 -> 109.3 (the
+  // shuffle pipe of 16 sorting warps per SM); K = 128 of 2048 (cfg4) loses 9 us.
+  const char* f3 = std::getenv("HIRE_FINAL3");
+  if (out_mode == 0 && K <= 64 && n <= 2048 && (f3 ? f3[0] == '1' : B <= 4)) {
+    const int np = static_cast<int>(std::max<int64_t>(n_per, 1));
+#define HIRE_F3(NT_, SL_)                                                                                   \
+    if (K <= 32 * SL_ && n <= (NT_ / 32) * 32 * SL_) {                                                      \
+      CK(launch_k(ctx, final3_kernel<NT_, SL_>, static_cast<unsigned>(B), NT_, 0, vals, vs, idx, is, src_keys, np, \
+                  part_stride, static_cast<int>(n), static_cast<int>(K), out_idx, out_val, out_prob, out_stride)); \
+      CK(cudaGetLastError());                                                                               \
+      return HIRE_OK;                                                                                       \
+    }
+    HIRE_F3(32, 1) HIRE_F3(64, 1) HIRE_F3(128, 1) HIRE_F3(256, 1)
+    HIRE_F3(128, 2) HIRE_F3(256, 2) HIRE_F3(512, 2) HIRE_F3(1024, 2)
+#undef HIRE_F3
+  }
   if (n <= kFinal2Max && !std::getenv("HIRE_SELECT_V1")) {
     const int np = static_cast<int>(std::max<int64_t>(n_per, 1));
 #define HIRE_F2(NT_, KPT)                                                                               \

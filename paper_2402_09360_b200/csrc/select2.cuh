@@ -1485,6 +1485,139 @@ __global__ void __launch_bounds__(NT) final2_kernel(
   if (dbg) g_ktrace[79] = gtimer();
 }
 
+// ---------------------------------------------------------------------
+// Final top-K, ranked, for K <= W = 32 * SL keys (hire.hpp:74-80, 135-142):
+// every warp sorts its W pool keys in registers (bitonic network: element
+// e = slot * 32 + lane, partners at distance >= 32 are register swaps, below
+// that shuffles), then a merge tree over the warps: the upper warp of a pair
+// parks its sorted list in shared memory, the lower one takes max(own[e],
+// other[W-1-e]) — a bitonic sequence holding the pair's top W — and re-sorts
+// it with one merge network. log2(warps) barriers in all, against ~20 for the
+// range select + scan + rank sort of final2_kernel, whose CTA-wide barriers
+// dominate at these sizes; the result is the same ordered set (keys are
+// unique). Warp 0 writes indices, values and the softmax.
+// ---------------------------------------------------------------------
+template <int SL>
+struct WarpKeys {
+  static constexpr int W = 32 * SL;
+  uint64_t k[SL];
+  // one compare-exchange stage at distance j inside blocks of size ksz
+  // (descending where (e & ksz) == 0)
+  template <int J, int KSZ>
+  __device__ __forceinline__ void stage(int lane) {
+    if constexpr (J >= 32) {
+      constexpr int DS = J / 32;
+#pragma unroll
+      for (int s = 0; s < SL; ++s) {
+        if ((s & DS) == 0) {
+          const int sp = s | DS;
+          const bool desc = ((s * 32) & KSZ) == 0;
+          const uint64_t a = k[s], c = k[sp];
+          const uint64_t hi = a > c ? a : c, lo = a > c ? c : a;
+          k[s] = desc ? hi : lo;
+          k[sp] = desc ? lo : hi;
+        }
+      }
+    } else {
+#pragma unroll
+      for (int s = 0; s < SL; ++s) {
+        const uint64_t o = static_cast<uint64_t>(__shfl_xor_sync(0xffffffffu, static_cast<unsigned long long>(k[s]), J));
+        const int e = s * 32 + lane;
+        const bool keep_max = ((lane & J) == 0) == ((e & KSZ) == 0);
+        k[s] = keep_max ? (k[s] > o ? k[s] : o) : (k[s] < o ? k[s] : o);
+      }
+    }
+  }
+  template <int J, int KSZ>
+  __device__ __forceinline__ void merge_from(int lane) {
+    stage<J, KSZ>(lane);
+    if constexpr (J > 1) merge_from<J / 2, KSZ>(lane);
+  }
+  template <int KSZ>
+  __device__ __forceinline__ void sort_from(int lane) {
+    merge_from<KSZ / 2, KSZ>(lane);
+    if constexpr (KSZ < W) sort_from<KSZ * 2>(lane);
+  }
+  __device__ __forceinline__ void sort_desc(int lane) { sort_from<2>(lane); }
+  __device__ __forceinline__ void merge_desc(int lane) { merge_from<W / 2, W>(lane); }
+};
+
+template <int NT, int SL>
+__global__ void __launch_bounds__(NT) final3_kernel(
+    const float* __restrict__ vals, int64_t vs, const uint32_t* __restrict__ idx, int64_t is,
+    const uint64_t* __restrict__ src_keys, int n_per, int64_t part_stride, int n, int K,
+    uint32_t* __restrict__ out_idx, float* __restrict__ out_val, float* __restrict__ out_prob, int64_t out_stride) {
+  constexpr int NW = NT / 32, W = 32 * SL;
+  __shared__ uint64_t s_buf[NW * W];
+  hire_dev::griddep_wait();
+  hire_dev::griddep_launch();
+  KTrace kt_(kKtFinal);
+  const int b = blockIdx.x, lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  WarpKeys<SL> wk;
+#pragma unroll
+  for (int s = 0; s < SL; ++s) {
+    const int i = wid * W + s * 32 + lane;
+    uint64_t k = 0;
+    if (i < n) {
+      k = src_keys ? src_keys[static_cast<int64_t>(i / n_per) * part_stride + static_cast<int64_t>(b) * n_per + i % n_per]
+                   : make_key(vals[b * vs + i], idx[b * is + i]);
+    }
+    wk.k[s] = k;
+  }
+  wk.sort_desc(lane);
+#pragma unroll
+  for (int lvl = 1; lvl < NW; lvl <<= 1) {
+    const int m = wid & (2 * lvl - 1);
+    if (m == lvl) {
+#pragma unroll
+      for (int s = 0; s < SL; ++s) s_buf[wid * W + s * 32 + lane] = wk.k[s];
+    }
+    __syncthreads();
+    if (m == 0) {
+      const uint64_t* o = s_buf + (wid + lvl) * W;
+#pragma unroll
+      for (int s = 0; s < SL; ++s) {
+        const uint64_t v = o[W - 1 - (s * 32 + lane)];
+        wk.k[s] = wk.k[s] > v ? wk.k[s] : v;
+      }
+      wk.merge_desc(lane);
+    }
+  }
+  if (wid != 0) return;
+  // zeros (padding) sort last: the valid keys among the first K
+  int nz = 0;
+#pragma unroll
+  for (int s = 0; s < SL; ++s) nz += (s * 32 + lane < K && wk.k[s] != 0ull) ? 1 : 0;
+  const int Kq = __reduce_add_sync(0xffffffffu, nz);
+#pragma unroll
+  for (int s = 0; s < SL; ++s) {
+    const int e = s * 32 + lane;
+    if (e < Kq) {
+      out_idx[b * out_stride + e] = key_index(wk.k[s]);
+      out_val[b * out_stride + e] = key_value(wk.k[s]);
+    }
+  }
+  if (out_prob) {
+    // hire.hpp:135-142: p_i = float(exp(double(v_i) - v_max)) / double sum
+    const double vmax = static_cast<double>(
+        key_value(static_cast<uint64_t>(__shfl_sync(0xffffffffu, static_cast<unsigned long long>(wk.k[0]), 0))));
+    double ex[SL];
+    double local = 0.0;
+#pragma unroll
+    for (int s = 0; s < SL; ++s) {
+      ex[s] = (s * 32 + lane < Kq) ? exp(static_cast<double>(key_value(wk.k[s])) - vmax) : 0.0;
+      local += ex[s];
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) local += __shfl_xor_sync(0xffffffffu, local, o);
+#pragma unroll
+    for (int s = 0; s < SL; ++s)
+      if (s * 32 + lane < Kq)
+        out_prob[b * out_stride + s * 32 + lane] =
+            static_cast<float>(static_cast<double>(static_cast<float>(ex[s])) / local);
+  }
+}
+
 }  // namespace hire_dev
 
 namespace hire_dev {

@@ -158,3 +158,33 @@ def test_list_path_equals_window_chain(H, O, kind, monkeypatch):
     assert torch.equal(r1.top_idx, r0.top_idx)
     want, _, _ = O.topk_select(v, kp)
     assert np.array_equal(N(r1.cand[0]).astype(np.uint32), np.sort(want.astype(np.uint32)))
+
+
+@pytest.mark.parametrize("kp,k", [(33, 1), (64, 5), (100, 32), (1000, 33), (2048, 64), (700, 64)])
+def test_final_topk_warp_sort_equals_range_select(H, O, monkeypatch, kp, k):
+    # the ranked final top-k by per-warp register sorts + a merge tree
+    # (final3_kernel, small batches) against the range-select kernel: same
+    # indices, values and softmax, with duplicate rows (value ties broken by
+    # index) and a pool padded past the candidates
+    V, d, B = 4096, 64, 3
+    g = np.random.default_rng(kp + k)
+    w = g.standard_normal((V, d)).astype(np.float32)
+    w[1::7] = w[0]  # many identical rows: exact-value ties
+    x = g.standard_normal((B, d)).astype(np.float32)
+    z = H.ScoreMatrix(T(w))
+    a = H.ApproxScorer.quantize(z)
+    cfg = H.HireConfig(k=k, k_prime=kp, x_mode=H.X_INT8, strict=True)
+    monkeypatch.setenv("HIRE_FINAL3", "1")
+    r1 = H.hire_topk(T(x), z, a, cfg)
+    i1, p1 = H.softmax_topk(z, T(x), a, cfg)
+    monkeypatch.setenv("HIRE_FINAL3", "0")
+    r0 = H.hire_topk(T(x), z, a, cfg)
+    i0, p0 = H.softmax_topk(z, T(x), a, cfg)
+    assert torch.equal(r1.top_idx, r0.top_idx) and torch.equal(r1.top_val, r0.top_val)
+    assert torch.equal(i1, i0)
+    torch.testing.assert_close(p1, p0, rtol=1e-6, atol=0)
+    codes, scales = a.export_q4()
+    for b in range(B):
+        o = O.hire_topk(w, x[b], O.q4_scores_int8(codes, scales, x[b], 0), k, kp, 0)
+        assert np.array_equal(N(r1.top_idx[b]).astype(np.uint32), o["top_idx"])
+        assert np.array_equal(N(r1.top_val[b]), o["top_val"])
