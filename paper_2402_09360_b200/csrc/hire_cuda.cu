@@ -1940,7 +1940,7 @@ int hire_debug_ktrace(hire_ctx c, int op, unsigned long long* out, int n) {
   if (op == 1) {
     if (!buf) CK(cudaMalloc(&buf, kWords * sizeof(unsigned long long)));
     unsigned long long init[kWords];
-    for (int i = 0; i < kWords; ++i) init[i] = ((i & 1) || i >= 24) && i != 54 ? 0ull : ~0ull;
+    for (int i = 0; i < kWords; ++i) init[i] = (((i & 1) || i >= 24) && i != 54 && i != 83) ? 0ull : ~0ull;
     CK(cudaMemcpy(buf, init, sizeof(init), cudaMemcpyHostToDevice));
     CK(cudaMemcpyToSymbol(hire_dev::g_ktrace, &buf, sizeof(buf)));
   } else if (op == 2) {

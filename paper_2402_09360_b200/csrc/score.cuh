@@ -128,7 +128,7 @@ __global__ void __launch_bounds__(256) q4_score_fast_int8(
     const float* __restrict__ sx, const int* __restrict__ sumxq, int phi,
     float* __restrict__ scores, int64_t score_stride) {
   hire_dev::griddep_wait();
-  hire_dev::griddep_launch();
+  hire_dev::LateTrigger late_trigger_;
   KTrace kt_(kKtProxy);
   const int lane = threadIdx.x & 31;
   const int64_t warp = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
@@ -210,7 +210,7 @@ __global__ void __launch_bounds__(256) q4_score_fast_fpx(
     int64_t rows, int d, const float* __restrict__ x, int phi,
     float* __restrict__ scores) {
   hire_dev::griddep_wait();
-  hire_dev::griddep_launch();
+  hire_dev::LateTrigger late_trigger_;
   KTrace kt_(kKtProxy);
   const int lane = threadIdx.x & 31;
   const int64_t warp = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
@@ -261,7 +261,7 @@ __global__ void __launch_bounds__(128) q4_score_seq(
     const float* __restrict__ sx, int int8_mode, int phi, float* __restrict__ scores,
     int64_t score_stride) {
   hire_dev::griddep_wait();
-  hire_dev::griddep_launch();
+  hire_dev::LateTrigger late_trigger_;
   KTrace kt_(kKtProxy);
   extern __shared__ __align__(16) unsigned char smem[];
   float* s_x = reinterpret_cast<float*>(smem);
@@ -765,7 +765,7 @@ __global__ void __launch_bounds__(256) q4_score_mma(
       if (kb0 + u < kb1) a[u] = ldg_stream(wmma + ((rb * nkb + kb0 + u) * 32 + lane));
   }
   griddep_wait();  // x quantisation (prep_x_int8_kernel) is complete
-  griddep_launch();
+  LateTrigger late_trigger_;
   KTrace kt_(kKtProxy);
   for (int i = threadIdx.x; i < NT * 8 * (d / 16); i += blockDim.x) {
     const int n = i / (d / 16), c = i % (d / 16);

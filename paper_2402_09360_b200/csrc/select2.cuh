@@ -650,7 +650,7 @@ __global__ void __launch_bounds__(kWinThreads) sel_window_kernel(
   __shared__ unsigned s_above, s_wn;
   __shared__ uint64_t s_win[STAGE];
   hire_dev::griddep_wait();
-  hire_dev::griddep_launch();
+  hire_dev::LateTrigger late_trigger_;
   KTrace kt_(kKtWindow);
   const int b = blockIdx.y, C = gridDim.x, c = blockIdx.x;
   const int lane = threadIdx.x & 31;
@@ -742,7 +742,7 @@ __global__ void __launch_bounds__(kWinThreads) sel_wlist_kernel(
   __shared__ uint64_t s_keys[STAGE];
   __shared__ unsigned s_n, s_base;
   hire_dev::griddep_wait();
-  hire_dev::griddep_launch();
+  hire_dev::LateTrigger late_trigger_;
   KTrace kt_(kKtWindow);
   const int b = blockIdx.y, C = gridDim.x, c = blockIdx.x;
   const int lane = threadIdx.x & 31;
@@ -1345,6 +1345,7 @@ __global__ void __launch_bounds__(NT) final2_kernel(
   hire_dev::griddep_launch();
   KTrace kt_(kKtFinal);
   const int b = blockIdx.x;
+  if (g_ktrace && threadIdx.x == 0) atomicMax(&g_ktrace[82], gtimer());  // latest CTA start
   RegKeys<KPT> src;
   const int i0 = threadIdx.x * KPT;
 #pragma unroll
@@ -1483,6 +1484,7 @@ __global__ void __launch_bounds__(NT) final2_kernel(
     }
   }
   if (dbg) g_ktrace[79] = gtimer();
+  if (g_ktrace && threadIdx.x == 0) atomicMin(&g_ktrace[83], gtimer());  // earliest CTA end
 }
 
 // ---------------------------------------------------------------------
