@@ -867,13 +867,19 @@ int launch_q4_umma(hire_ctx ctx, hire_scorer_s* a, const ScoreWs& w, int64_t b0,
   return HIRE_OK;
 }
 
-// the tcgen05 proxy from this many queries per launch up (HIRE_UMMA_MIN_B overrides; 0 = off)
-int64_t umma_min_batch() {
-  static const int64_t v = [] {
+// the tcgen05 proxy from this many queries per launch up (HIRE_UMMA_MIN_B
+// overrides; 0 = off): 9, or 7 when the score row is long enough to keep
+// every SM streaming (>= 4 row blocks of 128 per SM). Measured at cfg3
+// (V = 256000): the fused IMMA kernel takes 54 / 58 / 63 us at B = 1 / 4 / 8,
+// the tcgen05 proxy ~50 us at any batch but needs the stream selector after
+// it: B = 8 step 83.9 -> 77.7 us, B = 4 74.2 -> 81.6 us.
+int64_t umma_min_batch(int64_t rows = 0, int num_sms = 1 << 30) {
+  static const int64_t env = [] {
     const char* e = std::getenv("HIRE_UMMA_MIN_B");
-    return e ? static_cast<int64_t>(std::atoi(e)) : static_cast<int64_t>(9);
+    return e ? static_cast<int64_t>(std::atoi(e)) : static_cast<int64_t>(-1);
   }();
-  return v;
+  if (env >= 0) return env;
+  return rows >= static_cast<int64_t>(4) * 128 * num_sms ? 7 : 9;
 }
 
 template <int NT, int KS>
@@ -928,7 +934,7 @@ int run_scores(hire_ctx ctx, const hire_scorer_s* a, const float* x, int64_t B, 
   // the tcgen05 proxy takes every 64-query chunk of >= umma_min_batch()
   // queries; its x operand is prep's grouped layout (xperm, xg_mode 1)
   const bool umma = a->kind == HIRE_SCORER_Q4 && x_mode == HIRE_X_INT8 && d % 64 == 0 && !ctx->force_dp4a &&
-                    umma_min_batch() > 0 && std::min<int64_t>(B, 64) >= umma_min_batch() &&
+                    umma_min_batch() > 0 && std::min<int64_t>(B, 64) >= umma_min_batch(a->rows, ctx->num_sms) &&
                     umma_shape_ok(a, std::min<int64_t>(B, 64));
   if (a->kind == HIRE_SCORER_Q4 && x_mode == HIRE_X_INT8) {
     StageScope pscope(ctx, kStagePrep);
@@ -943,7 +949,7 @@ int run_scores(hire_ctx ctx, const hire_scorer_s* a, const float* x, int64_t B, 
       int64_t b0 = 0;
       while (b0 < B) {
         const int64_t nb = std::min<int64_t>(64, B - b0);
-        if (umma && nb >= umma_min_batch()) {
+        if (umma && nb >= umma_min_batch(a->rows, ctx->num_sms)) {
           RET(launch_q4_umma(ctx, const_cast<hire_scorer_s*>(a), w, b0, nb, phi, out, stride));
         } else {
           RET(ensure_mma_layout(ctx, const_cast<hire_scorer_s*>(a)));
@@ -1475,6 +1481,8 @@ void plan_fsel(hire_ctx ctx, const hire_scorer_s* a, int64_t B, const hire_topk_
   // B <= 8 (one MMA n-tile): at larger batches the in-flight filter's
   // registers spill and the fused kernel loses to the unfused chain (measured)
   if (a->d % 64 != 0 || ctx->force_dp4a || B < 1 || B > 8) return;
+  // from umma_min_batch() queries up the tcgen05 proxy + stream selector win
+  if (umma_min_batch() != 0 && B >= umma_min_batch(a->rows, ctx->num_sms) && umma_shape_ok(a, B)) return;
   const int64_t n = a->rows, K = sp.k_eff, n_rb = ceil_div(n, 16);
   f->nt = B <= 8 ? 1 : B <= 16 ? 2 : B <= 32 ? 4 : 8;
   f->ks = n_rb < 32LL * ctx->num_sms ? 2 : 1;
@@ -2968,7 +2976,7 @@ int hire_da_topk_emulated(hire_ctx ctx, hire_matrix w, hire_scorer a, int world,
   uint64_t* recv = static_cast<uint64_t*>(ctx->io_dev);
   // shard slices share the parent's tensor-core layouts (built here once)
   if (a->kind == HIRE_SCORER_Q4 && p->x_mode == HIRE_X_INT8 && !p->strict && umma_min_batch() > 0 &&
-      B >= umma_min_batch() && umma_shape_ok(a, std::min<int64_t>(B, 64)))
+      B >= 7 && umma_shape_ok(a, std::min<int64_t>(B, 64)))
     RET(ensure_umma_layout(ctx, a));
   for (int r = 0; r < world; ++r) {
     int64_t f, wd;
