@@ -603,7 +603,15 @@ int run_select(hire_ctx ctx, const float* scores, int64_t score_stride, int64_t 
       // fewer warps per CTA: the per-pass cost of the order statistic is
       // per-warp overhead, the key counting is cheap
       const char* v = std::getenv("HIRE_SEL_EXACT");
-      const int variant = v ? std::atoi(v) : (n <= 4096 ? 1 : 0);
+      // mid ranks over long rows: the histogram select (variant 4) needs ~10
+      // barriers whatever the rank; the 16-way range select wins near the top
+      const int variant = v ? std::atoi(v) : (n <= 4096 ? 1 : (K * 64 >= nn ? 4 : 0));
+      if (variant == 4 && K <= nn) {
+        CK(launch_k(ctx, hire_dev::sel_exact_fast_kernel, static_cast<unsigned>(B), hire_dev::kFinThreads, 0, scores,
+                    score_stride, nn, K, cand, cand_stride));
+        CK(cudaGetLastError());
+        return HIRE_OK;
+      }
       if (variant == 1)
         CK(launch_k(ctx, sel_exact_kernel<256, 16>, static_cast<unsigned>(B), 256, 0, scores, score_stride, nn, K,
                     cand, cand_stride));

@@ -188,3 +188,14 @@ def test_final_topk_warp_sort_equals_range_select(H, O, monkeypatch, kp, k):
         o = O.hire_topk(w, x[b], O.q4_scores_int8(codes, scales, x[b], 0), k, kp, 0)
         assert np.array_equal(N(r1.top_idx[b]).astype(np.uint32), o["top_idx"])
         assert np.array_equal(N(r1.top_val[b]), o["top_val"])
+
+
+@pytest.mark.parametrize("n", [4097, 8191, 8192])
+@pytest.mark.parametrize("k", [1, 100, 820, 8000])
+def test_small_row_histogram_select(H, O, monkeypatch, n, k):
+    # sel_exact_fast_kernel (mid ranks over rows <= 8192, the FFN layers'
+    # top-k' of 8192 units): forced for every rank, every distribution
+    monkeypatch.setenv("HIRE_SEL_EXACT", "4")
+    rows = _rows(n, 17)
+    v = np.stack([rows[kind] for kind in sorted(rows)])
+    _check(H, O, v, min(k, n))
