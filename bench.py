@@ -227,7 +227,7 @@ class SoftmaxWorkload(Workload):
 
     @property
     def proxy_kernel(self):
-        if self.B >= 7:
+        if self.B >= 5:
             return "q4_score_umma (K1 on tcgen05: TMA ring -> TMEM A operand -> kind::i8 MMA)"
         return "q4_score_mma_sel (K1F: IMMA proxy GEMV + fused candidate pre-selection)"
 

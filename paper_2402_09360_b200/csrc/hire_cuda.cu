@@ -876,18 +876,18 @@ int launch_q4_umma(hire_ctx ctx, hire_scorer_s* a, const ScoreWs& w, int64_t b0,
 }
 
 // the tcgen05 proxy from this many queries per launch up (HIRE_UMMA_MIN_B
-// overrides; 0 = off): 9, or 7 when the score row is long enough to keep
+// overrides; 0 = off): 9, or 5 when the score row is long enough to keep
 // every SM streaming (>= 4 row blocks of 128 per SM). Measured at cfg3
 // (V = 256000): the fused IMMA kernel takes 54 / 58 / 63 us at B = 1 / 4 / 8,
 // the tcgen05 proxy ~50 us at any batch but needs the stream selector after
-// it: B = 8 step 83.9 -> 77.7 us, B = 4 74.2 -> 81.6 us.
+// it: B = 8 step 83.9 -> 77.7 us, B = 6 80.1 -> 75.9, B = 5 78.8 -> 75.5, B = 4 about equal (74.3).
 int64_t umma_min_batch(int64_t rows = 0, int num_sms = 1 << 30) {
   static const int64_t env = [] {
     const char* e = std::getenv("HIRE_UMMA_MIN_B");
     return e ? static_cast<int64_t>(std::atoi(e)) : static_cast<int64_t>(-1);
   }();
   if (env >= 0) return env;
-  return rows >= static_cast<int64_t>(4) * 128 * num_sms ? 7 : 9;
+  return rows >= static_cast<int64_t>(4) * 128 * num_sms ? 5 : 9;
 }
 
 template <int NT, int KS>
@@ -2984,7 +2984,7 @@ int hire_da_topk_emulated(hire_ctx ctx, hire_matrix w, hire_scorer a, int world,
   uint64_t* recv = static_cast<uint64_t*>(ctx->io_dev);
   // shard slices share the parent's tensor-core layouts (built here once)
   if (a->kind == HIRE_SCORER_Q4 && p->x_mode == HIRE_X_INT8 && !p->strict && umma_min_batch() > 0 &&
-      B >= 7 && umma_shape_ok(a, std::min<int64_t>(B, 64)))
+      B >= 5 && umma_shape_ok(a, std::min<int64_t>(B, 64)))
     RET(ensure_umma_layout(ctx, a));
   for (int r = 0; r < world; ++r) {
     int64_t f, wd;
