@@ -27,13 +27,20 @@ def wall(fn, n=200):
 
 
 class A:
-    workload, batch, select = "cfg3", 1, "exact"
+    workload, batch, select = "cfg3", int(os.environ.get("B", "1")), "exact"
 
 
-wl = bench.make_workload(H, A)
-xh = np.ascontiguousarray(wl.inputs(1)[0].cpu().numpy())
-oa = np.empty((wl.B, wl.k), np.uint32)
-ob = np.empty((wl.B, wl.k), np.float32)
+def pin(shape, dt):
+    return torch.empty(shape, dtype=dt).pin_memory().numpy()
+
+
+wl = bench.make_workload(A)
+wl.attach(H)
+wl.host_buffers(pin)
+xh = pin((wl.B, wl.d), torch.float32)
+xh[:] = wl.inputs(1)[0].cpu().numpy()
+oa = pin((wl.B, wl.k), torch.int32).view(np.uint32)
+ob = pin((wl.B, wl.k), torch.float32)
 res = {}
 for own in (0, 1):
     ctx = H.Context(0) if not own else None
@@ -50,7 +57,7 @@ a = torch.zeros(1, device="cuda")
 with torch.cuda.graph(g, stream=s):
     a.add_(1)
 res["tiny_graph_launch_sync_us"] = wall(lambda: (g.replay(), torch.cuda.current_stream().synchronize()))
-hp = torch.empty(wl.B * 2048, dtype=torch.float32).pin_memory()
+hp = torch.empty(wl.B * wl.d, dtype=torch.float32).pin_memory()
 dp = torch.empty_like(hp, device="cuda")
 ho = torch.empty(wl.B * 128, dtype=torch.float32).pin_memory()
 do = torch.empty_like(ho, device="cuda")
@@ -62,5 +69,5 @@ def copies():
     torch.cuda.current_stream().synchronize()
 
 
-res["h2d_8KB_d2h_512B_sync_us"] = wall(copies)
+res["h2d_x_d2h_result_sync_us"] = wall(copies)
 print(res)

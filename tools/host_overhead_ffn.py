@@ -31,7 +31,8 @@ class A:
 
 
 def main():
-    wl = bench.make_workload(H, A)
+    wl = bench.make_workload(A)
+    wl.attach(H)
     ctx = H.Context(0)
     pin = lambda shape, dt: torch.empty(shape, dtype=dt).pin_memory().numpy()
     xh = pin((wl.B, wl.d), torch.float32)
