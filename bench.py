@@ -975,6 +975,7 @@ def run_ours(args):
                 "path": "C-ABI host call (hire_topk_host / hire_ffn_host) with pinned host buffers"
                         if world == 1 else "python parallel.da_topk with pinned copies"},
         "gpu_launches": int(launches),
+        "select_fallbacks": int(ctx.select_fallbacks()),  # queries that took the slow exact path (whole run)
         "clocks": clk.summary(),
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline and wl.name != "cfg5":

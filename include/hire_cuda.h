@@ -116,6 +116,11 @@ HIRE_API int hire_ctx_read_trace(hire_ctx ctx, long long* out, int n);
  * (pairs per kernel id, see common.cuh KtId), 0 disable. */
 HIRE_API int hire_debug_ktrace(hire_ctx ctx, int op, unsigned long long* out, int n);
 HIRE_API int hire_ctx_profile_read(hire_ctx ctx, double* ms, int64_t* counts, int n_stages);
+/* Queries whose exact top-k' selection took the slow whole-row path since the
+ * context was created (a sampled bound missed, a list segment overflowed, a
+ * sorted or constant score row): results are exact either way, this counts
+ * the time cliff. Synchronises the context stream. */
+HIRE_API int hire_ctx_select_fallbacks(hire_ctx ctx, long long* count);
 
 /* ---- device buffers (for wrappers that start from host data) ------------ */
 HIRE_API int hire_device_alloc(int64_t bytes, void** out);

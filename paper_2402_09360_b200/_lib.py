@@ -25,6 +25,7 @@ EXPORTS = [
     "hire_last_error", "hire_abi_version", "hire_experiments_built",
     "hire_ctx_create", "hire_ctx_destroy", "hire_ctx_stream", "hire_ctx_synchronize",
     "hire_ctx_launch_count", "hire_ctx_set_profiling", "hire_ctx_profile_read", "hire_ctx_read_trace", "hire_debug_ktrace",
+    "hire_ctx_select_fallbacks",
     "hire_device_alloc", "hire_device_free", "hire_copy",
     "hire_matrix_create", "hire_matrix_view", "hire_matrix_slice", "hire_matrix_destroy",
     "hire_matrix_info",
@@ -98,6 +99,7 @@ def _sig(L):
         "hire_ctx_synchronize": [_vp],
         "hire_ctx_set_profiling": [_vp, _i32],
         "hire_ctx_read_trace": [_vp, _vp, _i32],
+        "hire_ctx_select_fallbacks": [_vp, _vp],
         "hire_debug_ktrace": [_vp, _i32, _vp, _i32],
         "hire_ctx_profile_read": [_vp, _vp, _vp, _i32],
         "hire_device_alloc": [_i64, _p(_vp)],

@@ -55,6 +55,13 @@ class Context:
     def synchronize(self):
         check(lib().hire_ctx_synchronize(self.h))
 
+    def select_fallbacks(self) -> int:
+        """Queries whose exact top-k' selection took the slow whole-row path so
+        far (hire_ctx_select_fallbacks): a time cliff, never a wrong result."""
+        n = C.c_longlong()
+        check(lib().hire_ctx_select_fallbacks(self.h, C.byref(n)))
+        return int(n.value)
+
     def set_profiling(self, on: bool):
         check(lib().hire_ctx_set_profiling(self.h, int(on)))
 

@@ -403,7 +403,8 @@ int max_blocks(K kernel, int threads, size_t smem) {
 // context counter buffer: fused-kernel barriers, per-query counters, trace
 constexpr int kQcntOff = 8 * 16 * 32;  // the fused FFN kernel's barrier counters (ffn_fused.cuh kCntInts)
 constexpr int kTraceOff = kQcntOff + 64;
-constexpr int kCtxCounterInts = kTraceOff + 128;
+constexpr int kFallbackOff = kTraceOff + 128;  // selection fallbacks since the context was created
+constexpr int kCtxCounterInts = kFallbackOff + 16;
 
 constexpr int64_t kSelGridChunks = 4 * 160;  // S2/S3 CTAs over a whole batch (workspace bound; 4 per SM used)
 
@@ -580,6 +581,7 @@ int run_select(hire_ctx ctx, const float* scores, int64_t score_stride, int64_t 
                const SelPlan& sp, uint64_t* surv, uint32_t* cand, int64_t cand_stride,
                int* status, bool ordered = true) {
   StageScope scope(ctx, kStageSelect);
+  status = ctx->counters + kFallbackOff;  // context-lifetime count (hire_ctx_select_fallbacks)
   if (sp.mode == 2) {
     const uint32_t nn = static_cast<uint32_t>(n), K = static_cast<uint32_t>(sp.k_eff);
 #if HIRE_EXPERIMENTS
@@ -1676,7 +1678,7 @@ int run_scores_fsel(hire_ctx ctx, const hire_scorer_s* a, const float* x, int64_
   {
     StageScope scope(ctx, kStageSelect);
     CK(launch_k(ctx, sel_fin_kernel, static_cast<unsigned>(B), kFinThreads, bm, static_cast<const float*>(t.scores),
-                a->rows, fs, cand, sp.k_eff, ordered ? 1 : 0, t.status));
+                a->rows, fs, cand, sp.k_eff, ordered ? 1 : 0, ctx->counters + kFallbackOff));
   }
   CK(cudaGetLastError());
   return HIRE_OK;
@@ -1944,6 +1946,15 @@ int hire_ctx_read_trace(hire_ctx c, long long* out, int n) {
   if (!c || !out || n > 64) return invalid("bad trace request");
   CK(cudaStreamSynchronize(c->stream));
   CK(cudaMemcpy(out, c->counters + kTraceOff, static_cast<size_t>(n) * 8, cudaMemcpyDeviceToHost));
+  return HIRE_OK;
+}
+
+int hire_ctx_select_fallbacks(hire_ctx c, long long* count) {
+  if (!c || !count) return invalid("null argument");
+  CK(cudaStreamSynchronize(c->stream));
+  int v = 0;
+  CK(cudaMemcpy(&v, c->counters + kFallbackOff, sizeof(int), cudaMemcpyDeviceToHost));
+  *count = v;
   return HIRE_OK;
 }
 

@@ -130,3 +130,25 @@ def test_stream_no_fallback_on_benign_rows(H, stream):
         assert sp.get("fin_fallback", 0) == 0
         assert k <= sp.get("fin_listed", 0) <= 8192
         assert "pivot" not in sp  # one launch for bound + scan
+
+
+def test_fallback_counter_and_bound_rate(H, stream):
+    # hire_ctx_select_fallbacks: the slow whole-row path is counted per query.
+    # A constant row overflows every list segment (one fallback per query);
+    # exchangeable rows (normal, heavy-tailed, bimodal) never miss the bound:
+    # 60 batches x 32 queries without a single fallback (designed rate 1e-7 per query)
+    ctx = H.default_context()
+    n, k, B = 256000, 1024, 32
+    f0 = ctx.select_fallbacks()
+    H.topk_select(torch.zeros(3, 150000, device="cuda"), 500)
+    assert ctx.select_fallbacks() - f0 == 3
+    g = torch.Generator(device="cuda").manual_seed(7)
+    f1 = ctx.select_fallbacks()
+    for it in range(60):
+        v = torch.randn(B, n, device="cuda", generator=g)
+        if it % 3 == 1:
+            v = torch.exp(1.5 * v)  # log-normal
+        elif it % 3 == 2:
+            v = v + 3.0 * (torch.rand(B, n, device="cuda", generator=g) < 0.01)  # 1 % of the rows shifted up
+        H.topk_select(v, k)
+    assert ctx.select_fallbacks() - f1 == 0
