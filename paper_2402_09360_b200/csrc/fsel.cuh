@@ -71,10 +71,9 @@ struct FuseSel {
   int n_static;      // rounds scheduled statically (>= 1; the rest is claimed, KS == 1)
   const float* xf;   // non-null: quantise x here (prep_x_int8_kernel folded in; small B)
   uint64_t* lists;   // [B][kFinCap] listed keys (unordered)
-  // stream path (sel_stream_kernel): the list is nslots zero-padded slots,
-  // cnt[b] = keys listed (bit 31: a segment overflowed), lo[b] = the largest
-  // chunk bound (both cleared by sel_fin_kernel)
-  int nslots;
+  // stream path (sel_stream_kernel): lo[b] = the query's bound tau (the
+  // finisher accepts T only if T >= tau), cnt[b] as above
+  int stream;
 };
 
 // Sample keys rebuilt from value words staged in shared memory: slot j of
@@ -512,7 +511,7 @@ __device__ __noinline__ void fin_select_emit(const float* __restrict__ scores, i
   RangeScratch& rs = u.rs;
   const uint32_t n = fs.n, K = fs.K;
   const unsigned total_raw = __ldcg(fs.cnt + b);
-  const unsigned long long tau_max = fs.nslots > 0 ? __ldcg(fs.lo + b) : 0ull;
+  const unsigned long long tau_max = fs.stream ? __ldcg(fs.lo + b) : 0ull;
   const bool dbg = g_ktrace && threadIdx.x == 0 && b == 0;
   if (dbg) g_ktrace[57] = gtimer();
   __syncthreads();  // everyone has read the count before it is cleared
@@ -527,15 +526,14 @@ __device__ __noinline__ void fin_select_emit(const float* __restrict__ scores, i
   }
   uint32_t* out = cand + static_cast<int64_t>(b) * cand_stride;
   const int total = static_cast<int>(total_raw & 0x7FFFFFFFu);
-  const bool stream = fs.nslots > 0;
+  const bool stream = fs.stream != 0;
   if (!(total_raw & 0x80000000u) && total >= static_cast<int>(K) && total <= kFinCap) {
     const unsigned long long* L = reinterpret_cast<const unsigned long long*>(fs.lists) + static_cast<int64_t>(b) * kFinCap;
-    const int nload = stream ? fs.nslots : total;  // stream path: zero-padded segments
     uint64_t k[KPT];
 #pragma unroll
     for (int j = 0; j < KPT; ++j) {
       const int e = threadIdx.x + j * NT;
-      k[j] = e < nload ? __ldcg(L + e) : 0ull;
+      k[j] = e < total ? __ldcg(L + e) : 0ull;
     }
     const int nw = static_cast<int>((n + 31) / 32);
     for (int i = threadIdx.x; i < nw; i += NT) s_bm[i] = 0u;
@@ -543,7 +541,10 @@ __device__ __noinline__ void fin_select_emit(const float* __restrict__ scores, i
     const uint64_t T = block_fast_select<NT, KPT>(k, K, &u.fss, (g_ktrace && b == 0) ? g_ktrace + 24 : nullptr);
     if (dbg) { g_ktrace[59] = gtimer(); g_ktrace[61] = total; }
     // stream path: T is exact only if no chunk's bound lies above it
-    if (stream && tau_max > T) goto fallback;
+    if (stream && tau_max > T) {
+      if (g_ktrace && threadIdx.x == 0) { g_ktrace[84] = total_raw; g_ktrace[85] = tau_max; g_ktrace[86] = T; g_ktrace[87] = 4; g_ktrace[88] = b; }
+      goto fallback;
+    }
     if (!ordered) {
       // the caller does not return the candidate list: any order will do
       // (the exact recompute and the final top-k are order-independent)
@@ -585,6 +586,7 @@ __device__ __noinline__ void fin_select_emit(const float* __restrict__ scores, i
     if (dbg) g_ktrace[60] = gtimer();
     return;
   }
+  if (g_ktrace && threadIdx.x == 0) { g_ktrace[84] = total_raw; g_ktrace[85] = tau_max; g_ktrace[87] = 1; g_ktrace[88] = b; }
 fallback:
   // fallback: exact select over the whole row, then an ordered emit
   __syncthreads();  // the scratch union changes hands

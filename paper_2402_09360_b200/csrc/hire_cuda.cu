@@ -508,11 +508,15 @@ int plan_select(int64_t n, int64_t k_prime, int sel_mode, int64_t nb_req, int64_
 }
 
 // Stream path plan (sel_stream_kernel): C chunks per query, seg list slots per
-// chunk, and the sample rank r_s of each chunk's bound. r_s is the smallest
-// rank with P[Binomial(S, k'/n) >= r_s] <= 1e-9 (S = the chunk's sample
-// size): the chance that a chunk's bound lies above the true k'-th key, which
-// only costs the finisher's slow path, never exactness. The bound may stop
-// early once at most stop_s sample keys lie above it.
+// chunk, and the sample rank r_s of the query's bound. r_s is the smallest
+// rank with P[Binomial(S, k'/n) >= r_s] <= 1e-7 (S = the sampler's sample
+// size): the chance that the bound lies above the true k'-th key. C is the
+// largest chunk count (up to one wave of CTAs) for which the modelled chance
+// of an overflow (a CTA's 1024-key stage, or the query's 8192-key list) stays
+// below 1e-6 per query; failing that the safest C if below 1e-4 (cfg4, k' =
+// 2048 of 256000: 4e-6, the list is small for the bound's spread), else the
+// pivot + list kernels. Either event only costs the finisher's slow path,
+// never exactness.
 struct StreamPlan {
   int C = 0, seg = 0;
   int64_t r_s = 0;
@@ -537,6 +541,52 @@ int64_t binom_tail_rank(int64_t S, double p, double eps) {
   return r;
 }
 
+// P[X >= r], X ~ Binomial(n, p) (pmf recurrence from x = r).
+double binom_sf_ge(int n, double p, int r) {
+  if (r <= 0) return 1.0;
+  if (r > n || p <= 0.0) return 0.0;
+  if (p >= 1.0) return 1.0;
+  double pmf = std::exp(std::lgamma(n + 1.0) - std::lgamma(r + 1.0) - std::lgamma(n - r + 1.0) + r * std::log(p) +
+                        (n - r) * std::log1p(-p));
+  const double ratio = p / (1.0 - p);
+  double sum = 0.0;
+  for (int x = r; x <= n; ++x) {
+    sum += pmf;
+    pmf *= ratio * static_cast<double>(n - x) / static_cast<double>(x + 1);
+  }
+  return std::min(sum, 1.0);
+}
+
+inline double normal_sf(double z) { return 0.5 * std::erfc(z / std::sqrt(2.0)); }
+
+// Probability that a query of the stream selector ends on the finisher's slow
+// path because a list segment (or the whole list) overflows. The bound tau is
+// the r_s-th largest of 256 per-thread maxima of kpt sample keys each, so the
+// fraction Q of the row above tau has the distribution P[Q <= q] =
+// P[Binomial(256, 1 - (1 - q)^kpt) >= r_s] — wider than an order statistic of
+// the sample itself (measured: cfg4, k' = 2048, C = 19 chunks, 6.6e-5 per
+// query against this model's 7.8e-5). Given Q = q a chunk lists about
+// Binomial(chunk, q) keys; integrate over q.
+double stream_overflow_prob(int64_t n, int64_t r_s, int kpt, int64_t C, int64_t chunk, int64_t seg, int64_t cap) {
+  const double S = 256.0 * kpt;
+  const double q0 = 0.4 * static_cast<double>(r_s) / S, q1 = std::min(0.5, 8.0 * static_cast<double>(r_s) / S);
+  constexpr int N = 240;
+  double pf = 0.0, prev = 0.0;
+  for (int i = 0; i <= N; ++i) {
+    const double q = q0 * std::pow(q1 / q0, static_cast<double>(i) / N);
+    const double pt = 1.0 - std::pow(1.0 - q, static_cast<double>(kpt));
+    const double F = binom_sf_ge(256, pt, static_cast<int>(r_s));
+    const double dF = std::max(F - prev, 0.0);
+    prev = std::max(prev, F);
+    const double mc = q * static_cast<double>(chunk), sd = std::sqrt(mc * (1.0 - q));
+    const double tot = q * static_cast<double>(n);
+    const double g = static_cast<double>(C) * normal_sf((static_cast<double>(seg) + 0.5 - mc) / sd) +
+                     normal_sf((static_cast<double>(cap) + 0.5 - tot) / std::sqrt(tot));
+    pf += dF * std::min(1.0, g);
+  }
+  return pf + (1.0 - prev);
+}
+
 bool plan_stream(hire_ctx ctx, int64_t n, uint32_t K, int64_t B, StreamPlan* st) {
   using namespace hire_dev;
   static const int occ = max_blocks(sel_stream_kernel, kStrThreads, 0);
@@ -545,35 +595,40 @@ bool plan_stream(hire_ctx ctx, int64_t n, uint32_t K, int64_t B, StreamPlan* st)
                                  static_cast<int64_t>(kStrMaxChunks)});
   if (ce) C = std::max<int64_t>(1, std::min<int64_t>(std::atoi(ce), kStrMaxChunks));
   const int64_t G = ceil_div(n, 128);
-  struct Key {
-    int64_t S, n;
-    uint32_t K;
-    bool operator<(const Key& o) const { return std::tie(S, n, K) < std::tie(o.S, o.n, o.K); }
-  };
-  static thread_local std::map<Key, int64_t> memo;
+  // the plan of a shape is computed once (the overflow model costs ~1 ms)
+  using Key = std::tuple<int64_t, uint32_t, int64_t>;
+  static thread_local std::map<Key, StreamPlan> memo;
+  const Key key{n, K, C};
+  auto it = memo.find(key);
+  if (it != memo.end()) {
+    *st = it->second;
+    return st->C > 0;
+  }
+  StreamPlan plan;  // C == 0: the stream path does not apply
+  // the largest C with at most one query in a million on the slow path; else
+  // the safest C if that is at most one in 10^4 (the slow path costs ~150 us
+  // for the step it hits: below 0.1 us per step on average)
+  double best = 1e-4;
   for (; C >= 1; C = C > 1 ? (C + 1) / 2 : 0) {
     const int64_t chunk = ceil_div(G, C) * 128;                 // keys of a full chunk
     const int64_t S = std::min<int64_t>(kStrSample, chunk);     // its sample
-    const Key key{S, n, K};
-    auto it = memo.find(key);
-    if (it == memo.end()) {
-      if (memo.size() > 256) memo.clear();
-      it = memo.emplace(key, binom_tail_rank(S, static_cast<double>(K) / static_cast<double>(n), 1e-7)).first;
+    const int64_t r_s = binom_tail_rank(S, static_cast<double>(K) / static_cast<double>(n), 1e-7);
+    if (r_s > S || r_s > kStrFastRank) break;  // larger ranks: pivot + list kernels
+    const int64_t seg = kStrSegMax;  // keys a CTA can stage; the query's list holds kFinCap
+    const int kpt = static_cast<int>(std::max<int64_t>(1, S / kStrThreads));
+    const double pf = stream_overflow_prob(n, r_s, kpt, C, chunk, seg, kFinCap);
+    if (pf < best) {
+      best = pf;
+      plan.C = static_cast<int>(C);
+      plan.seg = static_cast<int>(seg);
+      plan.r_s = r_s;
     }
-    const int64_t r_s = it->second;
-    if (r_s > S || r_s > kStrFastRank) return false;  // larger ranks: pivot + list kernels
-    const int64_t seg = std::min<int64_t>(kStrSegMax, kFinCap / C);
-    // keys listed per chunk: about r_s of every S (1.25 x for the bound from
-    // the per-thread maxima), plus six sigma and slack
-    const double per_chunk = 1.25 * static_cast<double>(r_s) / static_cast<double>(S) * static_cast<double>(chunk);
-    if (per_chunk + 6.0 * std::sqrt(per_chunk) + 16.0 <= static_cast<double>(seg)) {
-      st->C = static_cast<int>(C);
-      st->seg = static_cast<int>(seg);
-      st->r_s = r_s;
-      return true;
-    }
+    if (pf <= 1e-6) break;
   }
-  return false;
+  if (memo.size() > 256) memo.clear();
+  memo.emplace(key, plan);
+  *st = plan;
+  return plan.C > 0;
 }
 
 // Candidate selection over scores [B][n] -> cand [B][cand_stride] ascending.
@@ -661,7 +716,7 @@ int run_select(hire_ctx ctx, const float* scores, int64_t score_stride, int64_t 
         // (a single short row keeps the two small launches: cfg1, 32768 keys, 28.6 vs 29.9 us per step)
         const bool big = (se && se[0] == '1') || n * B >= (1 << 20);
         if (!(se && se[0] == '0') && big && aligned && plan_stream(ctx, n, K, B, &st)) {
-          fs.nslots = st.C * st.seg;
+          fs.stream = 1;
           RET(ensure_tickets(ctx, B));
           CK(launch_k(ctx, sel_stream_kernel, dim3(static_cast<unsigned>(st.C), static_cast<unsigned>(B)), kStrThreads,
                       0, scores, score_stride, nn, static_cast<uint32_t>(st.r_s), static_cast<uint32_t>(st.seg), fs.cnt,

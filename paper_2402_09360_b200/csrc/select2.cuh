@@ -810,9 +810,10 @@ __global__ void __launch_bounds__(kWinThreads) sel_wlist_kernel(
 // then a rank by binary search over the 8 sorted lists — two barriers).
 // tau, stripped of its index part, is published with an
 // atomic on qtau[b]; the other CTAs of the query have their first two batches
-// of loads in flight while they poll it. Every key >= tau of a chunk goes to
-// its own list segment lists[b][c*seg ...], zero-padded to seg; qcnt[b] +=
-// keys listed (bit 31: a segment overflowed or the bound never arrived).
+// of loads in flight while they poll it. Every key >= tau of a chunk is staged
+// in shared memory (seg slots) and appended to the query's compact list with
+// one reservation atomic per CTA on qcnt[b] (bit 31: a stage or the list
+// overflowed, or the bound never arrived).
 // qcnt / qtau are zero at rest (cleared by sel_fin_kernel), which takes T =
 // the k'-th largest listed key and accepts it when T >= tau (then every key
 // >= T of the row is listed, so T is exact); otherwise it selects over the
@@ -875,7 +876,7 @@ __global__ void __launch_bounds__(kStrThreads, 4) sel_stream_kernel(
   constexpr int NT = kStrThreads, NW = NT / 32, U = kStrKpt / 4;
   __shared__ uint64_t s_sorted[NT];
   __shared__ uint64_t s_keys[kStrSegMax];
-  __shared__ unsigned s_n;
+  __shared__ unsigned s_n, s_base;
   __shared__ uint64_t s_res;
   __shared__ int s_ticket;
   hire_dev::griddep_wait();
@@ -1037,13 +1038,27 @@ __global__ void __launch_bounds__(kStrThreads, 4) sel_stream_kernel(
   hire_dev::griddep_launch();  // late: the finisher's 1024-thread CTAs must not take SMs from this grid
   __syncthreads();
   if (dbg) g_ktrace[73] = gtimer();
+  // one reservation per CTA in the query's compact list (bit 31 of the count:
+  // the finisher falls back — stage or list overflow, or the bound never came)
   const unsigned total = s_n;
-  const unsigned staged = min(total, seg);
-  uint64_t* L = lists + static_cast<int64_t>(b) * list_stride + static_cast<int64_t>(c) * seg;
-  for (unsigned t = threadIdx.x; t < seg; t += NT) L[t] = t < staged ? s_keys[t] : 0ull;
   if (threadIdx.x == 0) {
-    if (total > seg || late) atomicOr(qcnt + b, 0x80000000u);  // the finisher falls back (an Or: several chunks may overflow)
-    else atomicAdd(qcnt + b, total);
+    unsigned base = 0xFFFFFFFFu;
+    if (total > seg || late) {
+      atomicOr(qcnt + b, 0x80000000u);
+    } else if (total) {
+      base = atomicAdd(qcnt + b, total) & 0x7FFFFFFFu;
+      if (base + total > static_cast<unsigned>(list_stride)) {
+        atomicOr(qcnt + b, 0x80000000u);
+        base = 0xFFFFFFFFu;
+      }
+    }
+    s_base = base;
+  }
+  __syncthreads();
+  const unsigned base = s_base;
+  if (base != 0xFFFFFFFFu) {
+    uint64_t* L = lists + static_cast<int64_t>(b) * list_stride + base;
+    for (unsigned t = threadIdx.x; t < total; t += NT) L[t] = s_keys[t];
   }
   if (dbg) g_ktrace[74] = gtimer();
 }
