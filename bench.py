@@ -38,6 +38,20 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0}
+_ADDR = {}
+
+
+def _addr(a):
+    """Address of a long-lived (pinned) numpy buffer, looked up once: numpy's
+    `.ctypes.data` costs 1-2 us per access, a serving loop binds its buffers
+    once (INTEGRATION.md, "per-call Python marshalling")."""
+    k = id(a)
+    v = _ADDR.get(k)
+    if v is None or v[0] is not a:
+        v = _ADDR[k] = (a, a.ctypes.data)
+    return v[1]
+
+
 METRIC = "HiRE decode tokens/s (µs/token, HBM roofline fraction, recall@k)"
 
 
@@ -254,8 +268,8 @@ class SoftmaxWorkload(Workload):
             self._hn = (C.c_int64(), C.c_int64(), C.c_int())
             self._hr = tuple(C.byref(v) for v in self._hn)
         # softmax_topk through the C ABI: top-k indices and probabilities
-        H._lib.check(H.lib().hire_topk_host(ctx.h, self.W.h, self.A.h, x_host.ctypes.data, self.B, self._hp, None,
-                                            idx_host.ctypes.data, self._hv.ctypes.data, val_host.ctypes.data,
+        H._lib.check(H.lib().hire_topk_host(ctx.h, self.W.h, self.A.h, _addr(x_host), self.B, self._hp, None,
+                                            _addr(idx_host), _addr(self._hv), _addr(val_host),
                                             *self._hr))
 
     def host_buffers(self, pinned):
@@ -342,8 +356,8 @@ class FfnWorkload(Workload):
         f, a = self.layers[i % len(self.layers)]
         if not hasattr(self, "_hp"):
             self._hp = C.byref(H._lib.FfnParams(self.k, self.kp, 1, 1, H.X_INT8, 0, 0))
-        H._lib.check(H.lib().hire_ffn_host(ctx.h, f.u.h, f.v.h, a.h, x_host.ctypes.data, self.B, self._hp,
-                                           sel_host.ctypes.data, out_host.ctypes.data))
+        H._lib.check(H.lib().hire_ffn_host(ctx.h, f.u.h, f.v.h, a.h, _addr(x_host), self.B, self._hp,
+                                           _addr(sel_host), _addr(out_host)))
 
     def host_buffers(self, pinned):
         pass
@@ -430,8 +444,8 @@ class LowRankSoftmaxWorkload(Workload):
             self._hp = C.byref(self.cfg.params())
             self._hn = (C.c_int64(), C.c_int64(), C.c_int())
             self._hr = tuple(C.byref(v) for v in self._hn)
-        H._lib.check(H.lib().hire_topk_host(ctx.h, z.h, a.h, x_host.ctypes.data, self.B, self._hp, None,
-                                            idx_host.ctypes.data, self._hv.ctypes.data, val_host.ctypes.data,
+        H._lib.check(H.lib().hire_topk_host(ctx.h, z.h, a.h, _addr(x_host), self.B, self._hp, None,
+                                            _addr(idx_host), _addr(self._hv), _addr(val_host),
                                             *self._hr))
 
     def host_buffers(self, pinned):
@@ -519,9 +533,9 @@ class DaSoftmaxWorkload(Workload):
                 self._hp = C.byref(self.cfg.params())
                 self._hn = (C.c_int64(), C.c_int64(), C.c_int())
                 self._hr = tuple(C.byref(v) for v in self._hn)
-            H._lib.check(H.lib().hire_topk_host(ctx.h, self.W.h, self.A.h, x_host.ctypes.data, self.B, self._hp,
-                                                None, idx_host.ctypes.data, self._hv.ctypes.data,
-                                                val_host.ctypes.data, *self._hr))
+            H._lib.check(H.lib().hire_topk_host(ctx.h, self.W.h, self.A.h, _addr(x_host), self.B, self._hp,
+                                                None, _addr(idx_host), _addr(self._hv),
+                                                _addr(val_host), *self._hr))
             return
         if not hasattr(self, "_xd"):
             self._xd = torch.empty(self.B, self.d, device="cuda")

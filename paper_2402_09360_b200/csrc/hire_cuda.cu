@@ -713,9 +713,10 @@ int run_select(hire_ctx ctx, const float* scores, int64_t score_stride, int64_t 
         const char* se = std::getenv("HIRE_SEL_STREAM");
         const bool aligned = (reinterpret_cast<uintptr_t>(scores) & 15) == 0 && (score_stride & 3) == 0;
         StreamPlan st;
-        // (a single short row keeps the two small launches: cfg1, 32768 keys, 28.6 vs 29.9 us per step)
-        const bool big = (se && se[0] == '1') || n * B >= (1 << 20);
-        if (!(se && se[0] == '0') && big && aligned && plan_stream(ctx, n, K, B, &st)) {
+        // whenever the planner accepts the shape: one launch instead of pivot +
+        // list scan is 2.5-4.5 us faster from 9000-key rows up at every batch
+        // (tools/bench_select.py; cfg1, 32768 keys, B=1: step 28.5 -> 25.7 us)
+        if (!(se && se[0] == '0') && aligned && plan_stream(ctx, n, K, B, &st)) {
           fs.stream = 1;
           RET(ensure_tickets(ctx, B));
           CK(launch_k(ctx, sel_stream_kernel, dim3(static_cast<unsigned>(st.C), static_cast<unsigned>(B)), kStrThreads,
