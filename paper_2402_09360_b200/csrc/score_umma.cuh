@@ -98,7 +98,11 @@ struct UmmaSmem {
     return x_off(stages) + static_cast<size_t>(nq) * d;
   }
   static __host__ __device__ size_t bytes(int stages, int nq, int d) {
-    return bar_off(stages, nq, d) + (2 * kUmmaMaxStages + 2 * kUmmaABufs + 5) * 8 + 16;
+    return qc_off(stages, nq, d) + 64 * 8;
+  }
+  // per-query epilogue constants: float sx[64], int 8 * sum(xq)[64]
+  static __host__ __device__ size_t qc_off(int stages, int nq, int d) {
+    return (bar_off(stages, nq, d) + (2 * kUmmaMaxStages + 2 * kUmmaABufs + 5) * 8 + 16 + 15) & ~static_cast<size_t>(15);
   }
   // deepest ring that fits next to an x operand of nq queries
   static __host__ int stages_for(int nq, int d, size_t smem_max) {
@@ -321,53 +325,90 @@ __global__ void __launch_bounds__(kUmmaThreads, 1) q4_score_umma(
     // ===== epilogue (warp w reads TMEM lanes 32 (w % 4) ..): accumulators
     // -> scale, phi -> scores [q][row]. With two warpgroups, group eg takes
     // the row blocks rbi % 2 == eg, i.e. accumulator buffer db = eg.
+    // The per-row-block work is a dependent scalar chain in 4 warps, and the
+    // last block's epilogue is the kernel's tail, so it is kept short: the
+    // per-query constants come from shared memory (two broadcast LDS.128 per
+    // 4 queries, no shuffles or selects), the row's scale is fetched before
+    // the accumulator wait, the partial sums are read two at a time, and the
+    // store address is a running pointer (ncu, cfg3 B=32: the epilogue warps
+    // were busy 88 % of the kernel, ~6.8 us per row block, before this).
     griddep_wait();  // scores / sx / sum(xq) of this call: after the producer grids
     const int ew = (warp - kUmmaEpiWarp) & 3, eg = (warp - kUmmaEpiWarp) >> 2;
     const uint32_t lane_off = static_cast<uint32_t>(32 * ew) << 16;
-    // per-query constants in registers (lane l: queries l, l + 32)
-    const int s8a = lane < nb ? 8 * sumxq[lane] : 0, s8b = lane + 32 < nb ? 8 * sumxq[lane + 32] : 0;
-    const float sxa = lane < nb ? sx[lane] : 0.0f, sxb = lane + 32 < nb ? sx[lane + 32] : 0.0f;
+    float* s_qsx = reinterpret_cast<float*>(smem + UmmaSmem::qc_off(stages, nq, d));
+    int* s_qs8 = reinterpret_cast<int*>(s_qsx + 64);
+    {
+      const int et = tid - 32 * kUmmaEpiWarp;
+      if (et < 64) {
+        s_qsx[et] = et < nb ? sx[et] : 0.0f;
+        s_qs8[et] = et < nb ? 8 * sumxq[et] : 0;
+      }
+      asm volatile("bar.sync 1, %0;" ::"r"(128 * kUmmaEpiGroups) : "memory");
+    }
     // scores kept in L2 for the selector up to 32 queries (32 MB at V=256000);
     // beyond, evict-last rows would crowd each other out
     const uint64_t pol_s = nb <= 32 ? l2_policy_evict_last() : l2_policy_evict_normal();
     (void)pol_s;
+    auto store = [&](float* p, float v) {
+#if HIRE_UMMA_L2
+      st_hint_f32(p, v, pol_s);
+#else
+      *p = v;
+#endif
+    };
     int rbi = 0;
     for (int64_t rb = blockIdx.x; rb < n_rb; rb += gridDim.x, ++rbi) {
       if (rbi % kUmmaEpiGroups != eg) continue;
       const int db = rbi & 1;
+      const int64_t row = rb * kUmmaRows + 32 * ew + lane;
+      const float sc = row < rows ? scales[row] : 0.0f;  // in flight during the accumulator wait
       mbar_wait(&dfull[db], (rbi >> 1) & 1);
       umma::fence_after();
-      const int64_t row = rb * kUmmaRows + 32 * ew + lane;
-      const float sc = row < rows ? scales[row] : 0.0f;
       for (int q0 = 0; q0 < nq; q0 += 16) {
         uint32_t acc[16];
-        umma::ld_32x32b_x16(tmem + lane_off + kColD + db * nq + q0, acc);
-        for (int i = 1; i < n_iss; ++i) {  // the other issuers' partial sums
-          uint32_t part[16];
-          umma::ld_32x32b_x16(tmem + lane_off + kColD + (2 * i + db) * nq + q0, part);
+        const uint32_t t0 = tmem + lane_off + kColD + db * nq + q0;
+        umma::ld_32x32b_x16(t0, acc);
+        if (n_iss > 1) {  // the other issuers' partial sums (n_iss is 1, 2 or 4)
+          uint32_t p1[16];
+          umma::ld_32x32b_x16(t0 + 2 * nq, p1);
           umma::wait_ld();
 #pragma unroll
-          for (int e = 0; e < 16; ++e) acc[e] += part[e];
+          for (int e = 0; e < 16; ++e) acc[e] += p1[e];
+          if (n_iss > 2) {
+            uint32_t p2[16];
+            umma::ld_32x32b_x16(t0 + 4 * nq, p1);
+            umma::ld_32x32b_x16(t0 + 6 * nq, p2);
+            umma::wait_ld();
+#pragma unroll
+            for (int e = 0; e < 16; ++e) acc[e] += p1[e] + p2[e];
+          }
+        } else {
+          umma::wait_ld();
         }
-        umma::wait_ld();
         if (q0 + 16 >= nq) {
           umma::fence_before();
           umma::mbar_arrive(&dempty[db]);
         }
+        const int jn = nb - q0;  // queries of this block that exist (may be <= 0: padding)
+        if (row < rows && jn > 0) {
+          float* p = scores + static_cast<int64_t>(q0) * score_stride + row;
 #pragma unroll
-        for (int j = 0; j < 16; ++j) {
-          const int q = q0 + j;
-          const int s8q = __shfl_sync(0xffffffffu, q < 32 ? s8a : s8b, q & 31);
-          const float sxq = __shfl_sync(0xffffffffu, q < 32 ? sxa : sxb, q & 31);
-          if (q < nb && row < rows) {
-            const int aint = static_cast<int>(acc[j]) - s8q;
-            const float cs = __fmul_rn(sc, sxq);
-            const float v = apply_phi(phi, __fmul_rn(static_cast<float>(aint), cs));
-#if HIRE_UMMA_L2
-            st_hint_f32(scores + static_cast<int64_t>(q) * score_stride + row, v, pol_s);
-#else
-            scores[static_cast<int64_t>(q) * score_stride + row] = v;
-#endif
+          for (int j4 = 0; j4 < 16; j4 += 4) {
+            const float4 sx4 = *reinterpret_cast<const float4*>(s_qsx + q0 + j4);
+            const int4 s84 = *reinterpret_cast<const int4*>(s_qs8 + q0 + j4);
+            const float sxv[4] = {sx4.x, sx4.y, sx4.z, sx4.w};
+            const int s8v[4] = {s84.x, s84.y, s84.z, s84.w};
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const int j = j4 + e;
+              if (j < jn) {
+                const int aint = static_cast<int>(acc[j]) - s8v[e];
+                const float cs = __fmul_rn(sc, sxv[e]);
+                const float z = __fmul_rn(static_cast<float>(aint), cs);
+                store(p, phi == kIdentity ? z : apply_phi(phi, z));
+              }
+              p += score_stride;
+            }
           }
         }
       }
