@@ -173,6 +173,8 @@ __device__ __forceinline__ uint64_t block_fast_select(const uint64_t (&keys)[KPT
           if (cum < r && cum + c[j] >= r) {
             s->bstar = static_cast<unsigned>(kFsBins - 1 - (tid * BPT + j));
             s->above = cum;
+            s->m = c[j];
+            s->ncand = 0u;
           }
           cum += c[j];
         }
@@ -180,6 +182,33 @@ __device__ __forceinline__ uint64_t block_fast_select(const uint64_t (&keys)[KPT
       __syncthreads();
       const unsigned bstar = s->bstar;
       r -= s->above;
+      if (s->m <= 32u) {
+        // the usual case for the HiRE score rows: the bin holds a handful of
+        // keys — gather them by bin number and rank them directly (no range
+        // pass, no separate compaction: two barriers and a pass fewer)
+        each([&](uint64_t k) {
+          const bool in = k != 0 && vbin(k) == bstar;
+          const unsigned bal = __ballot_sync(0xffffffffu, in);
+          if (bal) {
+            const int leader = __ffs(bal) - 1;
+            unsigned base = 0;
+            if (lane == leader) base = atomicAdd(&s->ncand, static_cast<unsigned>(__popc(bal)));
+            base = __shfl_sync(0xffffffffu, base, leader);
+            if (in) s->cand[0][base + __popc(bal & ((1u << lane) - 1u))] = k;
+          }
+        });
+        __syncthreads();
+        stamp();
+        const unsigned m = s->ncand;
+        if (wid == 0) {
+          const uint64_t mine = lane < static_cast<int>(m) ? s->cand[0][lane] : 0ull;
+          int gt = 0;
+          for (unsigned j = 0; j < m; ++j) gt += s->cand[0][j] > mine ? 1 : 0;
+          if (lane < static_cast<int>(m) && gt == r - 1) s->result = mine;
+        }
+        __syncthreads();
+        return s->result;
+      }
       // the chosen bin's keys are one contiguous ord range: find it
       unsigned a = 0xFFFFFFFFu, b = 0u, nn = 0u;
       each([&](uint64_t k) {

@@ -1,8 +1,8 @@
 """GPU: the stream selector (select2.cuh sel_stream_kernel + sel_fin_kernel:
 sample bound and list scan in one launch) against the oracle's topk_select
 (linalg.hpp:157-176) and against the pivot + list kernels it replaces.
-HIRE_SEL_STREAM=1 forces the path on rows shorter than its default gate;
-=0 disables it. Bit-exact indices and values, ties by ascending index, on
+HIRE_SEL_STREAM=0 disables the path (pivot + list kernels instead); the
+default takes it whenever the planner accepts the shape. Bit-exact indices and values, ties by ascending index, on
 adversarial rows (the sampler's chunk sees none of the large keys, all keys
 equal, ReLU plateaus), ragged lengths (not a multiple of 4 / 128), many
 queries, CUDA-graph replay (zero-at-rest counters and tickets)."""
@@ -64,12 +64,24 @@ def test_stream_select_matches_oracle(H, O, stream, kind, n, k):
 
 @pytest.mark.parametrize("B", [1, 16, 40])
 def test_stream_select_batches_and_default_gate(H, O, B):
-    # B * n >= 2^20 takes the stream path by default (no env)
+    # the stream path by default (no env)
     n, k = 70000, 512
     g = np.random.default_rng(3)
     v = g.standard_normal((B, n)).astype(np.float32)
     v[B // 2] = np.round(v[B // 2] * 4) / 4  # one row full of ties
     _check(H, O, v, k)
+
+
+@pytest.mark.parametrize("n,k,B", [(9000, 128, 1), (32768, 256, 1), (32000, 128, 16), (64000, 1024, 4)])
+def test_stream_default_gate_short_rows(H, O, n, k, B):
+    # short rows and small batches take the stream path too (no size gate since
+    # round 2d); random rows stay off the finisher's slow path
+    g = np.random.default_rng(21)
+    v = g.standard_normal((B, n)).astype(np.float32)
+    ctx = H.default_context()
+    before = ctx.select_fallbacks()
+    _check(H, O, v, k)
+    assert ctx.select_fallbacks() == before
 
 
 def test_stream_equals_pivot_list_path(H, O, monkeypatch):
