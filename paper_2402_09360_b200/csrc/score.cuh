@@ -780,6 +780,14 @@ __global__ void __launch_bounds__(256) q4_score_mma(
     int acc[NT][4];
 #pragma unroll
     for (int nt = 0; nt < NT; ++nt) acc[nt][0] = acc[nt][1] = acc[nt][2] = acc[nt][3] = 0;
+    // the two row scales of this lane: in flight during the k loop (loaded at
+    // their use they stalled the epilogue on an L2 round trip per row block)
+    float rs_lo = 0.0f, rs_hi = 0.0f;
+    if (ks == 0 && rb < n_rb) {
+      const int64_t r0 = rb * 16 + g;
+      if (r0 < rows) rs_lo = scales[r0];
+      if (r0 + 8 < rows) rs_hi = scales[r0 + 8];
+    }
     if (rb < n_rb) {
       for (int kb = kb0; kb < kb1; kb += U) {
         uint4 nxt[U];
@@ -843,7 +851,7 @@ __global__ void __launch_bounds__(256) q4_score_mma(
           const int n = nt * 8 + 2 * t + (e & 1);
           if (row < rows && n < B) {
             const int aint = acc[nt][e] - 8 * sumxq[n];
-            const float cs = __fmul_rn(scales[row], sx[n]);
+            const float cs = __fmul_rn((e & 2) ? rs_hi : rs_lo, sx[n]);
             scores[static_cast<int64_t>(n) * score_stride + row] =
                 apply_phi(phi, __fmul_rn(static_cast<float>(aint), cs));
           }
