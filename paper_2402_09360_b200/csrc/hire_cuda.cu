@@ -1290,11 +1290,16 @@ int run_final(hire_ctx ctx, const float* vals, int64_t vs, const uint32_t* idx, 
   }
   if (n <= kFinal2Max && !std::getenv("HIRE_SELECT_V1")) {
     const int np = static_cast<int>(std::max<int64_t>(n_per, 1));
+    // the K-th key by the histogram select (HIRE_F2_FAST=0: 16-way range
+    // splits). Measured: cfg4 (128 of 2048) step 86.5 -> 84.7 us, cfg2 (410
+    // of 820) 36.7 -> 36.0, cfg3 B=32 (64 of 1024) 99.6 -> 99.2
+    const char* f2e = std::getenv("HIRE_F2_FAST");
+    const int f2_fast = f2e ? std::atoi(f2e) : 1;
 #define HIRE_F2(NT_, KPT)                                                                               \
     if (n <= NT_ * KPT) {                                                                               \
       CK(launch_k(ctx, final2_kernel<NT_, KPT>, static_cast<unsigned>(B), NT_, smem, vals, vs, idx, is, \
                   src_keys, np, part_stride, static_cast<int>(n), static_cast<int>(K), out_mode, out_idx,   \
-                  out_val, out_prob, out_keys, out_stride));                                            \
+                  out_val, out_prob, out_keys, out_stride, f2_fast));                                   \
       CK(cudaGetLastError());                                                                           \
       return HIRE_OK;                                                                                   \
     }

@@ -1355,10 +1355,14 @@ __global__ void __launch_bounds__(NT) final2_kernel(
     const float* __restrict__ vals, int64_t vs, const uint32_t* __restrict__ idx, int64_t is,
     const uint64_t* __restrict__ src_keys, int n_per, int64_t part_stride, int n, int K,
     int out_mode, uint32_t* __restrict__ out_idx, float* __restrict__ out_val,
-    float* __restrict__ out_prob, uint64_t* __restrict__ out_keys, int64_t out_stride) {
-  __shared__ RangeScratch rs;
+    float* __restrict__ out_prob, uint64_t* __restrict__ out_keys, int64_t out_stride, int fast_sel) {
+  __shared__ union {
+    RangeScratch rs;
+    FastSelScratch fss;
+  } u_;
+  RangeScratch& rs = u_.rs;
   __shared__ double s_red[NT / 32];
-  int* const s_scan = rs.scan;
+  __shared__ int s_scan[40];
   extern __shared__ __align__(16) unsigned char smem_f2[];
   uint64_t* s_sel = reinterpret_cast<uint64_t*>(smem_f2);
   hire_dev::griddep_wait();
@@ -1392,7 +1396,15 @@ __global__ void __launch_bounds__(NT) final2_kernel(
   const bool dbg = g_ktrace && threadIdx.x == 0 && b == 0;
   if (dbg) g_ktrace[76] = gtimer();
   // K >= pool: everything is selected (no order statistic needed)
-  const uint64_t T = Kq >= n_valid ? 1ull : (Kq >= 1 ? block_range_select<NT>(src, n_valid, Kq, &rs) : ~0ull);
+  // the K-th largest key: histogram select (fastsel.cuh, ~8 barriers whatever
+  // the rank) or 16-way range splits (one barrier per split)
+  uint64_t T;
+  if (Kq >= n_valid) T = 1ull;
+  else if (Kq < 1) T = ~0ull;
+  else if (fast_sel) {
+    T = block_fast_select<NT, KPT>(src.k, Kq, &u_.fss);
+    __syncthreads();  // the scratch union changes hands
+  } else T = block_range_select<NT>(src, n_valid, Kq, &rs);
   int c = 0;
 #pragma unroll
   for (int j = 0; j < KPT; ++j) c += (src.k[j] && src.k[j] >= T) ? 1 : 0;
