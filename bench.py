@@ -82,6 +82,14 @@ def max_over_ranks(v: float, world: int) -> float:
     return float(t.item())
 
 
+def da_path(world):
+    """DA-TOP-k through hire_da_topk_run + NCCL: always at N > 1. HIRE_BENCH_DA=1
+    takes the same code path on one GPU with a 1-rank communicator (validation
+    of the N > 1 flow — graph capture of the ncclAllGather included — where
+    only one GPU is available; not a bench configuration)."""
+    return world > 1 or os.environ.get("HIRE_BENCH_DA") == "1"
+
+
 def barrier(world):
     if world > 1:
         import torch.distributed as dist
@@ -221,6 +229,7 @@ class SoftmaxWorkload(Workload):
     def __init__(self, batch, select="exact", world=1, rank=0, seed=0):
         self.V, self.d, self.kp, self.k, self.B = 256000, 2048, 1024, 64, batch
         self.world, self.rank, self.select = world, rank, select
+        self.da = da_path(world)
         self.first, self.width = shard_range(self.V, world, rank)
         self.Wt, _, _ = gen_vocab_rows(self.V, self.d, 256, self.first, self.width, seed=1 + seed)
         self.gen = torch.Generator(device="cuda").manual_seed(seed + 99)
@@ -236,7 +245,7 @@ class SoftmaxWorkload(Workload):
         if self.select == "bucketed":
             kw.update(select=H.SELECT_BUCKETED, n_buckets=1024, bucket_t=1)
         self.cfg = H.HireConfig(**kw)
-        self.comm = P.Communicator(self.world, self.rank) if self.world > 1 else None
+        self.comm = P.Communicator(self.world, self.rank) if self.da else None
         torch.cuda.synchronize()
 
     @property
@@ -246,14 +255,14 @@ class SoftmaxWorkload(Workload):
         return "q4_score_mma_sel (K1F: IMMA proxy GEMV + fused candidate pre-selection)"
 
     def step(self, i, x):
-        if self.world > 1:
+        if self.da:
             return self.P.da_topk(self.W, self.A, self.V, x, self.cfg, self.comm, merge=self.H.MERGE_GLOBAL)
         # softmax_topk (hire.hpp:123-144): top-k indices + probabilities
         return self.H.softmax_topk(self.W, x, self.A, self.cfg)
 
     def host_step(self, i, x_host, idx_host, val_host, ctx):
         H = self.H
-        if self.world > 1:
+        if self.da:
             if not hasattr(self, "_xd"):
                 self._xd = torch.empty(self.B, self.d, device="cuda")
             self._xd.copy_(torch.from_numpy(x_host), non_blocking=True)
@@ -298,7 +307,7 @@ class SoftmaxWorkload(Workload):
         return self.H.roofline_bytes("q4", self.d, self.width, nu, self.d * 2, exchange_bytes=xb), nu, 0
 
     def recall(self, x):
-        if self.world > 1:
+        if self.da:
             return None
         H = self.H
         r = H.hire_topk(x, self.W, self.A, self.cfg)
@@ -310,7 +319,7 @@ class SoftmaxWorkload(Workload):
         return {"workload": "cfg3 HiRE-softmax (BASELINE.json configs[2])", "V": self.V, "d": self.d,
                 "k_prime": self.kp, "k": self.k, "global_batch": self.B,
                 "api": "softmax_topk (hire.hpp:123-144): top-k indices + softmax probabilities"
-                       + (" via DA-TOP-k, global merge" if self.world > 1 else ""),
+                       + (" via DA-TOP-k, global merge" if self.da else ""),
                 "proxy": "int4 per-row absmax (device K9) x int8-quantised x",
                 "weights": "bf16 W = rank-256 (unit entry variance) + 0.1 N(0,1)",
                 "shard_rows": self.width,
@@ -504,6 +513,7 @@ class DaSoftmaxWorkload(Workload):
     def __init__(self, batch, world=1, rank=0, seed=0):
         self.V, self.d, self.r, self.kp, self.k, self.B = 256000, 4096, 64, 2048, 128, batch
         self.world, self.rank = world, rank
+        self.da = da_path(world)
         self.first, self.width = shard_range(self.V, world, rank)
         self.Wt, A, Bm = gen_vocab_rows(self.V, self.d, self.r, self.first, self.width, seed=4 + seed)
         self.z1 = (Bm / self.r ** 0.5).to(torch.bfloat16).contiguous()   # [r, d]
@@ -518,17 +528,17 @@ class DaSoftmaxWorkload(Workload):
         self.W = H.ScoreMatrix(self.Wt)
         self.A = H.ApproxScorer.low_rank(self.z1, self.z2)
         self.cfg = H.HireConfig(k=self.k, k_prime=self.kp)
-        self.comm = P.Communicator(self.world, self.rank) if self.world > 1 else None
+        self.comm = P.Communicator(self.world, self.rank) if self.da else None
         torch.cuda.synchronize()
 
     def step(self, i, x):
-        if self.world == 1:
+        if not self.da:
             return self.H.softmax_topk(self.W, x, self.A, self.cfg)
         return self.P.da_topk(self.W, self.A, self.V, x, self.cfg, self.comm, merge=self.H.MERGE_GLOBAL)
 
     def host_step(self, i, x_host, idx_host, val_host, ctx):
         H = self.H
-        if self.world == 1:
+        if not self.da:
             if not hasattr(self, "_hp"):
                 self._hp = C.byref(self.cfg.params())
                 self._hn = (C.c_int64(), C.c_int64(), C.c_int())
@@ -569,7 +579,7 @@ class DaSoftmaxWorkload(Workload):
                                      exchange_bytes=xb), nu, 0
 
     def recall(self, x):
-        if self.world > 1:
+        if self.da:
             return None
         H = self.H
         r = H.hire_topk(x, self.W, self.A, self.cfg)
@@ -951,7 +961,8 @@ def run_ours(args):
     e2e_s = max_over_ranks(time.perf_counter() - t0, world)
     e2e = wl.B * K * (1 if wl.scaling == "strong" else world) / e2e_s
 
-    par = "single GPU" if world == 1 else (
+    par = ("single GPU" + (" (HIRE_BENCH_DA=1: da_topk with a 1-rank NCCL communicator — validation run)"
+                           if getattr(wl, "da", False) else "")) if world == 1 else (
         f"DA-TOP-k over {world} GPUs (rows sharded, ncclAllGather of keys)" if wl.scaling == "strong"
         else f"replicas x{world}")
     uniq = nu if not isinstance(nu, tuple) else {"u_rows": nu[0], "v_rows": nu[1]}
@@ -987,7 +998,7 @@ def run_ours(args):
         "e2e": {"value": round(e2e, 2), "unit": "tokens/s", "h2d_bytes_per_step": bi,
                 "d2h_bytes_per_step": bo,
                 "path": "C-ABI host call (hire_topk_host / hire_ffn_host) with pinned host buffers"
-                        if world == 1 else "python parallel.da_topk with pinned copies"},
+                        if not getattr(wl, "da", world > 1) else "python parallel.da_topk with pinned copies"},
         "gpu_launches": int(launches),
         "select_fallbacks": int(ctx.select_fallbacks()),  # queries that took the slow exact path (whole run)
         "clocks": clk.summary(),

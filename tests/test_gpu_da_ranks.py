@@ -175,3 +175,25 @@ def test_da_two_processes_exchange_on_host(H, O):
         ids, want = O.da_group_sparse(u, v, xf[b], O.q4_scores_int8(uc, us, xf[b], 1), kf, kpf, world)
         assert np.array_equal(got[0]["ffn_sel"][b].astype(np.uint32), ids)
         np.testing.assert_allclose(got[0]["ffn_out"][b], want, rtol=1e-4, atol=1e-4 * np.abs(want).max())
+
+
+def test_bench_da_flow_one_rank_nccl():
+    """bench.py's N > 1 flow (da_topk -> ncclAllGather -> merge captured in a CUDA
+    graph, staged profiling, device timeline, e2e with pinned copies) on one
+    GPU with a 1-rank communicator (HIRE_BENCH_DA=1): the line must carry
+    every contract key and the DA step must not lose more than the merge to
+    the single-GPU call."""
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, HIRE_BENCH_DA="1")
+    p = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--steps", "4", "--warmup", "3",
+                        "--no-cpu-baseline"], env=env, capture_output=True, text=True, timeout=600)
+    assert p.returncode == 0, p.stderr[-2000:]
+    line = json.loads(p.stdout.strip().splitlines()[-1])
+    for key in ("metric", "value", "unit", "n_gpus", "ms_per_step", "roofline", "e2e", "gpu_launches", "clocks"):
+        assert key in line, key
+    assert "1-rank NCCL" in line["config"]["parallelism"]
+    assert line["value"] > 0 and line["gpu_launches"] > 0
+    assert line["e2e"]["path"].startswith("python parallel.da_topk")
