@@ -108,31 +108,24 @@ struct hire_ctx_s {
   // host-buffer calls (*_host): after one eager call per shape, the whole
   // call — H2D copy, kernel chain, D2H copy — replays as one CUDA graph on
   // gstream. An entry is valid while every buffer it captured is unchanged.
-  // The input-fetch kernel node of a captured call: its source pointer is
-  // rewritten per call (the caller's own pinned buffer when it has a device
-  // alias, else the context's staging buffer), so one graph serves every
-  // input buffer. Heap-allocated: kernelParams points into it.
-  struct FetchNode {
-    cudaGraph_t graph = nullptr;  // kept alive: exec-node updates name the node of the source graph
-    cudaGraphNode_t node = nullptr;
-    cudaKernelNodeParams params{};
-    const void* src = nullptr;
-    void* dst = nullptr;
-    int64_t n16 = 0;
-    void* args[3] = {nullptr, nullptr, nullptr};
-    FetchNode() = default;
-    FetchNode(const FetchNode&) = delete;
-    FetchNode& operator=(const FetchNode&) = delete;
-    ~FetchNode() {
-      if (graph) cudaGraphDestroy(graph);
-    }
-  };
+  // The input-fetch kernel of a host call reads its source address from
+  // fetch_slot (one word of mapped host memory the host stores before every
+  // launch: the caller's own pinned buffer when it has a device alias, else
+  // the context's staging buffer), so one captured graph serves every input
+  // buffer and a replay never edits the executable graph. (Round 2e: the
+  // earlier scheme re-pointed the fetch node with
+  // cudaGraphExecKernelNodeSetParams per call; two contexts replaying their
+  // graphs from two host threads then hit illegal-address faults — see
+  // tools/probes/concurrent_host_calls.py.)
+  unsigned long long* fetch_slot = nullptr;      // host view
+  unsigned long long* fetch_slot_dev = nullptr;  // device alias
+  bool fetch_by_slot = false;                    // set by fetch_inputs when it launched the slot kernel
   struct HostGraph {
     std::vector<int64_t> key;
     std::vector<const void*> bufs;
     cudaGraphExec_t exec = nullptr;
     int64_t out[4] = {0, 0, 0, 0};
-    std::shared_ptr<FetchNode> fetch;
+    bool uses_slot = false;  // its fetch kernel reads the input address from fetch_slot
   };
   static constexpr size_t kMaxHostGraphs = 64;
   std::vector<HostGraph> hgraphs;  // least recently used first
@@ -1331,14 +1324,63 @@ __global__ void fetch_host_kernel(const uint4* __restrict__ src, uint4* __restri
     dst[i] = src[i];
 }
 
-// H2D of a host call's inputs: the fetch kernel when aligned, else a copy.
+constexpr int kFetchCtas = 64;         // grid bound of the fetch kernels
+constexpr int kFetchSlotStride = 16;   // u64 words between the CTAs' copies of the slot (128 B)
+
+// The same copy with the source address read from a word of mapped host
+// memory (hire_ctx_s::fetch_slot): system-scope load, never a cached copy.
+__global__ void fetch_host_slot_kernel(const unsigned long long* __restrict__ slot, uint4* __restrict__ dst,
+                                       int64_t n16) {
+  hire_dev::griddep_wait();
+  hire_dev::griddep_launch();
+  // one PCIe read per CTA, each CTA from a line of its own: system-scope loads
+  // of one address are served one after the other (~0.8 us each: 64 CTAs on
+  // one word cost 52 us, a load per thread ~450 us)
+  __shared__ unsigned long long s_src;
+  if (threadIdx.x == 0) {
+    unsigned long long p;
+    asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(p) : "l"(slot + blockIdx.x * kFetchSlotStride) : "memory");
+    s_src = p;
+  }
+  __syncthreads();
+  // read-only path (ld.global.nc, as the compiler picks for a const __restrict__
+  // parameter): whole lines per request over PCIe. Plain generic loads through a
+  // pointer the compiler cannot classify took 60 us for 256 KB instead of 10.
+  const uint4* src = reinterpret_cast<const uint4*>(s_src);
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n16;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    dst[i] = __ldg(src + i);
+}
+
+// A host thread that has made no CUDA call yet has no current device: its
+// first cudaPointerGetAttributes fails (found with two threads calling
+// hire_topk_host on two contexts: the input then had "no device alias"). Every
+// entry point that takes host buffers binds the context's device once per thread.
+void bind_thread(hire_ctx ctx) {
+  static thread_local int bound = -1;
+  if (bound != ctx->device) {
+    cudaSetDevice(ctx->device);
+    bound = ctx->device;
+  }
+}
+
+void store_fetch_slot(hire_ctx ctx, const void* dsrc) {
+  volatile unsigned long long* sl = ctx->fetch_slot;
+  for (int c = 0; c < kFetchCtas; ++c) sl[c * kFetchSlotStride] = reinterpret_cast<unsigned long long>(dsrc);
+}
+
+// H2D of a host call's inputs: the fetch kernel when aligned (source address
+// through the context's slot), else a copy.
 int fetch_inputs(hire_ctx ctx, void* dst, const void* host_src, size_t bytes) {
   void* dsrc = nullptr;
-  if (bytes % 16 == 0 && (reinterpret_cast<uintptr_t>(host_src) & 15) == 0 &&
+  if (ctx->fetch_slot && bytes % 16 == 0 && (reinterpret_cast<uintptr_t>(host_src) & 15) == 0 &&
       cudaHostGetDevicePointer(&dsrc, const_cast<void*>(host_src), 0) == cudaSuccess && dsrc) {
     const int64_t n16 = static_cast<int64_t>(bytes / 16);
-    const unsigned grid = static_cast<unsigned>(std::min<int64_t>(ceil_div(n16, 256), 64));
-    CK(launch_k(ctx, fetch_host_kernel, grid, 256, 0, static_cast<const uint4*>(dsrc), static_cast<uint4*>(dst), n16));
+    const unsigned grid = static_cast<unsigned>(std::min<int64_t>(ceil_div(n16, 256), kFetchCtas));
+    store_fetch_slot(ctx, dsrc);
+    ctx->fetch_by_slot = true;
+    CK(launch_k(ctx, fetch_host_slot_kernel, grid, 256, 0, static_cast<const unsigned long long*>(ctx->fetch_slot_dev),
+                static_cast<uint4*>(dst), n16));
     return HIRE_OK;
   }
   cudaGetLastError();
@@ -1786,9 +1828,11 @@ int run_host_graph(hire_ctx ctx, const std::vector<int64_t>& key, int64_t* out, 
         CK(cudaEventRecord(ctx->gev, ctx->stream));
         CK(cudaStreamWaitEvent(ctx->gstream, ctx->gev, 0));
       }
-      if (g.fetch && g.fetch->src != fetch_src) {  // this call's input buffer
-        g.fetch->src = fetch_src;
-        CK(cudaGraphExecKernelNodeSetParams(g.exec, g.fetch->node, &g.fetch->params));
+      // this call's input buffer (read by the fetch kernel through the slot);
+      // without a device address for it the call runs eagerly
+      if (g.uses_slot) {
+        if (!fetch_src) return body(out);
+        store_fetch_slot(ctx, fetch_src);
       }
       CK(cudaGraphLaunch(g.exec, ctx->gstream));
       *done_on = ctx->gstream;  // the host call blocks on it: no event back
@@ -1819,6 +1863,7 @@ int run_host_graph(hire_ctx ctx, const std::vector<int64_t>& key, int64_t* out, 
   ctx->stream = ctx->gstream;
   CK(cudaStreamBeginCapture(ctx->gstream, cudaStreamCaptureModeThreadLocal));
   const int64_t launches0 = ctx->launches;
+  ctx->fetch_by_slot = false;
   const int rc = body(out);
   cudaGraph_t graph = nullptr;
   const cudaError_t ec = cudaStreamEndCapture(ctx->gstream, &graph);
@@ -1834,44 +1879,15 @@ int run_host_graph(hire_ctx ctx, const std::vector<int64_t>& key, int64_t* out, 
     ctx->host_graphs = ec == cudaSuccess;
     return body(out);
   }
-  // the input-fetch node (first fetch_host_kernel node), if any
-  std::shared_ptr<hire_ctx_s::FetchNode> fetch;
-  {
-    size_t nn = 0;
-    if (cudaGraphGetNodes(graph, nullptr, &nn) == cudaSuccess && nn > 0) {
-      std::vector<cudaGraphNode_t> nodes(nn);
-      if (cudaGraphGetNodes(graph, nodes.data(), &nn) == cudaSuccess)
-        for (size_t i = 0; i < nn && !fetch; ++i) {
-          cudaGraphNodeType ty;
-          cudaKernelNodeParams kp{};
-          if (cudaGraphNodeGetType(nodes[i], &ty) != cudaSuccess || ty != cudaGraphNodeTypeKernel) continue;
-          if (cudaGraphKernelNodeGetParams(nodes[i], &kp) != cudaSuccess) continue;
-          if (kp.func != reinterpret_cast<void*>(fetch_host_kernel)) continue;
-          fetch = std::make_shared<hire_ctx_s::FetchNode>();
-          fetch->node = nodes[i];
-          fetch->params = kp;
-          fetch->src = *static_cast<const void* const*>(kp.kernelParams[0]);
-          fetch->dst = *static_cast<void* const*>(kp.kernelParams[1]);
-          fetch->n16 = *static_cast<const int64_t*>(kp.kernelParams[2]);
-          fetch->args[0] = &fetch->src;
-          fetch->args[1] = &fetch->dst;
-          fetch->args[2] = &fetch->n16;
-          fetch->params.kernelParams = fetch->args;
-          fetch->params.extra = nullptr;
-        }
-    }
-    cudaGetLastError();
-  }
   cudaGraphExec_t exec = nullptr;
   const cudaError_t ei = cudaGraphInstantiate(&exec, graph, 0);
-  if (fetch && ei == cudaSuccess) fetch->graph = graph;  // owned by the cache entry from here
-  else cudaGraphDestroy(graph);
+  cudaGraphDestroy(graph);
   CK(ei);
   if (ctx->hgraphs.size() >= hire_ctx_s::kMaxHostGraphs) {  // bounded: evict the least recently used
     cudaGraphExecDestroy(ctx->hgraphs.front().exec);
     ctx->hgraphs.erase(ctx->hgraphs.begin());
   }
-  ctx->hgraphs.push_back({key, bufs, exec, {out[0], out[1], out[2], out[3]}, fetch});
+  ctx->hgraphs.push_back({key, bufs, exec, {out[0], out[1], out[2], out[3]}, ctx->fetch_by_slot});
   CK(cudaGraphLaunch(exec, ctx->gstream));
   *done_on = ctx->gstream;
   return HIRE_OK;
@@ -1959,6 +1975,19 @@ int hire_ctx_create(int device, void* stream, int own_stream, hire_ctx* out) {
   if (const char* e = getenv("HIRE_PROXY_KERNEL")) c->force_dp4a = std::strcmp(e, "dp4a") == 0;
   if (const char* e = getenv("HIRE_FFN_FUSED")) c->ffn_fused = std::strcmp(e, "1") == 0;
   if (const char* e = getenv("HIRE_FUSED_TRACE")) c->trace = std::strcmp(e, "1") == 0;
+  {
+    void* hp = nullptr;
+    void* dp = nullptr;
+    if (cudaHostAlloc(&hp, kFetchCtas * kFetchSlotStride * 8, cudaHostAllocMapped | cudaHostAllocPortable) == cudaSuccess &&
+        cudaHostGetDevicePointer(&dp, hp, 0) == cudaSuccess && dp) {
+      c->fetch_slot = static_cast<unsigned long long*>(hp);
+      c->fetch_slot_dev = static_cast<unsigned long long*>(dp);
+      std::memset(hp, 0, kFetchCtas * kFetchSlotStride * 8);
+    } else {  // no mapped memory: host calls stage their inputs with a copy
+      if (hp) cudaFreeHost(hp);
+      cudaGetLastError();
+    }
+  }
   CK(cudaMalloc(&c->counters, kCtxCounterInts * sizeof(int)));
   CK(cudaMemset(c->counters, 0, kCtxCounterInts * sizeof(int)));
   if (const char* e = getenv("HIRE_NO_PDL")) c->pdl = std::strcmp(e, "1") != 0;
@@ -1979,6 +2008,7 @@ int hire_ctx_destroy(hire_ctx c) {
   if (c->upart) cudaFree(c->upart);
   if (c->io_dev) cudaFree(c->io_dev);
   if (c->io_host) cudaFreeHost(c->io_host);
+  if (c->fetch_slot) cudaFreeHost(c->fetch_slot);
   for (auto& g : c->hgraphs) cudaGraphExecDestroy(g.exec);
   if (c->gstream) cudaStreamDestroy(c->gstream);
   if (c->gev) cudaEventDestroy(c->gev);
@@ -2434,6 +2464,7 @@ int hire_topk_host(hire_ctx ctx, hire_matrix w, hire_scorer a, const float* x_ho
                    float* top_val_host, float* top_prob_host, int64_t* n_cand, int64_t* n_top,
                    int* clamped) {
   if (!ctx || !x_host || !top_idx_host || !top_val_host) return invalid("null argument");
+  bind_thread(ctx);
   RET(validate_topk(w, a, B, p));
   SelPlan sp;
   RET(plan_select(w->rows, p->k_prime, p->select, p->n_buckets, p->bucket_t, &sp));
@@ -2463,6 +2494,7 @@ int hire_topk_host(hire_ctx ctx, hire_matrix w, hire_scorer a, const float* x_ho
   cudaStream_t done_on = nullptr;
   RET(run_host_graph(ctx, key, res, &done_on, xdev, [&](int64_t* r) -> int {
     RET(fetch_inputs(ctx, dv, xsrc, xb));
+    // results are written straight into mapped host memory (through its device alias)
     char* o = hs + in_bytes;  // results are written straight into mapped host memory
     uint32_t* dcand = cb ? reinterpret_cast<uint32_t*>(o) : nullptr;
     o += align_up(cb);
@@ -2725,6 +2757,7 @@ int hire_ffn_run(hire_ctx ctx, hire_matrix u, hire_matrix v, hire_scorer a, cons
 int hire_ffn_host(hire_ctx ctx, hire_matrix u, hire_matrix v, hire_scorer a, const float* x_host,
                   int64_t B, const hire_ffn_params* p, uint32_t* sel_host, float* out_host) {
   if (!ctx || !x_host || !out_host) return invalid("null argument");
+  bind_thread(ctx);
   RET(validate_ffn(u, v, a, B, p));
   const int64_t kg = p->k / p->group_size;
   const size_t xb = static_cast<size_t>(B * u->d) * 4;

@@ -81,7 +81,7 @@ def test_ffn_host_replays_equal_device_path(H, O, monkeypatch):
 
 def test_host_calls_read_pinned_inputs_in_place(H, O):
     """Pinned caller input buffers are read in place: the captured graph's
-    fetch node is re-pointed per call. Alternating pinned buffers, a pageable
+    fetch kernel takes the address from the context's slot. Alternating pinned buffers, a pageable
     one in between, and a recycled handle address must all give the
     device-path results (no stale pointer in a replayed graph)."""
     V, d, k, kp, B = 20000, 256, 16, 256, 3
@@ -116,3 +116,72 @@ def test_host_calls_read_pinned_inputs_in_place(H, O):
                                            sel.ctypes.data_as(C.c_void_p), out.ctypes.data_as(C.c_void_p)))
         want, wsel = H.ffn_group_sparse(f, T(x), fa, kf, kpf, x_mode=H.X_INT8)
         assert np.array_equal(out.view(np.uint32), want.cpu().numpy().view(np.uint32)), it
+
+
+def test_host_calls_from_two_threads_two_contexts(H, O):
+    """Two host threads, one context each (own stream, workspaces and graphs),
+    calling hire_topk_host / hire_ffn_host at the same time on shared matrix
+    and scorer handles with alternating pinned inputs — the serving pattern
+    bench.py's e2e uses. Every call must equal the device-path result of its
+    own input: a thread's first call (no CUDA call made on it before) must see
+    its buffer's device address, and one context's replay must not disturb
+    the other's (round 2e: this pattern faulted when the fetch node was
+    re-pointed with cudaGraphExecKernelNodeSetParams)."""
+    import threading
+    V, d, k, kp, B, lanes, calls = 20000, 256, 16, 256, 4, 2, 60
+    w = _data.lowrank_plus_noise(V, d, 16, 11)
+    codes, scales = O.quantize_int4(w)
+    z = H.ScoreMatrix(T(w))
+    a = H.ApproxScorer.quantized(codes, scales)
+    cfg = H.HireConfig(k=k, k_prime=kp, x_mode=H.X_INT8)
+    m, kf, kpf = 2048, 102, 204
+    u, v = _data.ffn_family(m, d, 12, r=16)
+    f = H.GroupedFFN(H.ScoreMatrix(T(u)), H.ScoreMatrix(T(v)))
+    fa = H.ApproxScorer.quantize(f.u)
+    fp = H._lib.FfnParams(kf, kpf, 1, 1, H.X_INT8, 0, 0)
+    g = np.random.default_rng(5)
+
+    def pin(shape, dt=torch.float32):
+        return torch.empty(shape, dtype=dt).pin_memory().numpy()
+    xs, want = [], []
+    for i in range(5):
+        x = pin((B, d))
+        x[:] = (g.standard_normal((B, d)) / np.sqrt(d)).astype(np.float32)
+        xs.append(x)
+        r = H.hire_topk(T(x), z, a, cfg)
+        fo, fs = H.ffn_group_sparse(f, T(x), fa, kf, kpf, x_mode=H.X_INT8)
+        want.append((r.top_idx.cpu().numpy().astype(np.uint32), r.top_val.cpu().numpy(), fo.cpu().numpy()))
+    torch.cuda.synchronize()
+    ctxs = [H.Context(0, torch.cuda.Stream()) for _ in range(lanes)]
+    for c in ctxs:  # eager + capture per context, one at a time
+        for i in range(3):
+            _topk_host(H, c, z, a, xs[i], cfg)
+    bad = []
+
+    def lane(l):
+        ctx = ctxs[l]
+        idx, val, prob = pin((B, k), torch.int32).view(np.uint32), pin((B, k)), pin((B, k))
+        sel, out = pin((B, kf), torch.int32).view(np.uint32), pin((B, d))
+        p = cfg.params()
+        n = (C.c_int64(), C.c_int64(), C.c_int())
+        ptr = lambda arr: arr.ctypes.data_as(C.c_void_p)  # noqa: E731
+        try:
+            for i in range(calls):
+                j = (i + 2 * l) % len(xs)
+                H._lib.check(H.lib().hire_topk_host(ctx.h, z.h, a.h, ptr(xs[j]), B, C.byref(p), None, ptr(idx),
+                                                    ptr(val), ptr(prob), *[C.byref(t) for t in n]))
+                if not (np.array_equal(idx, want[j][0]) and np.array_equal(val.view(np.uint32), want[j][1].view(np.uint32))):
+                    bad.append(("topk", l, i))
+                H._lib.check(H.lib().hire_ffn_host(ctx.h, f.u.h, f.v.h, fa.h, ptr(xs[j]), B, C.byref(fp), ptr(sel),
+                                                   ptr(out)))
+                if not np.array_equal(out.view(np.uint32), want[j][2].view(np.uint32)):
+                    bad.append(("ffn", l, i))
+        except Exception as e:  # surfaces in the assert below
+            bad.append(("error", l, repr(e)))
+    th = [threading.Thread(target=lane, args=(l,)) for l in range(lanes)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    torch.cuda.synchronize()
+    assert not bad, bad[:5]
