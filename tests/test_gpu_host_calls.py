@@ -156,6 +156,10 @@ def test_host_calls_from_two_threads_two_contexts(H, O):
     for c in ctxs:  # eager + capture per context, one at a time
         for i in range(3):
             _topk_host(H, c, z, a, xs[i], cfg)
+            so, oo = pin((B, kf), torch.int32), pin((B, d))
+            H._lib.check(H.lib().hire_ffn_host(c.h, f.u.h, f.v.h, fa.h, xs[i].ctypes.data_as(C.c_void_p), B,
+                                               C.byref(fp), so.ctypes.data_as(C.c_void_p),
+                                               oo.ctypes.data_as(C.c_void_p)))
     bad = []
 
     def lane(l):
