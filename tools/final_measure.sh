@@ -9,7 +9,8 @@ for w in "cfg3 --batch 64" "cfg3 --batch 8" "cfg3 --batch 1" "cfg4" "cfg2" "cfg1
   timeout 400 python bench.py --workload $w > gpurun_out/b.log 2>&1; tail -1 gpurun_out/b.log >> gpurun_out/bench_lines.jsonl
 done
 timeout 400 python bench.py --impl reference > gpurun_out/b_ref.log 2>&1; tail -1 gpurun_out/b_ref.log >> gpurun_out/bench_lines.jsonl
-timeout 400 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches_cfg3_b32.csv python bench.py --steps 3 --warmup 3 > gpurun_out/ncu1.log 2>&1
+# -s 440: the weight generators (torch kernels, 63 row blocks) come first
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -s 440 -c 700 --csv --log-file gpurun_out/launches_cfg3_b32.csv python bench.py --steps 3 --warmup 3 > gpurun_out/ncu1.log 2>&1
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:q4_score_umma -s 6 -c 1 -o /tmp/umma_cfg3_b32 python bench.py --steps 2 --warmup 3 > gpurun_out/ncu2.log 2>&1
 ncu -i /tmp/umma_cfg3_b32.ncu-rep --page raw --csv > gpurun_out/umma_cfg3_b32_raw.csv 2>/dev/null
 ncu -i /tmp/umma_cfg3_b32.ncu-rep --page details > gpurun_out/umma_cfg3_b32_details.txt 2>/dev/null
