@@ -1194,9 +1194,9 @@ def main():
     ap.add_argument("--select", default="exact", choices=["exact", "bucketed"])
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--streams", type=int, default=4,
+    ap.add_argument("--streams", type=int, default=6,
                     help="streams the K timed steps are dealt over inside the graph (independent batches)")
-    ap.add_argument("--in-flight", type=int, default=4,
+    ap.add_argument("--in-flight", type=int, default=6,
                     help="host calls in flight for the e2e number (1: one blocking call at a time)")
     args = ap.parse_args()
     if args.warmup < 3:
