@@ -94,7 +94,13 @@ HIRE_API int hire_experiments_built(void);
 /* ---- context: device, stream, workspace -------------------------------- */
 /* own_stream = 1: the context creates (and owns) a non-blocking stream and
  * ignores cuda_stream; otherwise kernels go to cuda_stream (NULL = the
- * legacy default stream). */
+ * legacy default stream).
+ * Threading: a context serves one call at a time (its workspaces, host-call
+ * graphs and input slot belong to that call). Matrix and scorer handles are
+ * read-only after construction and may be shared by any number of contexts.
+ * For several calls in flight give each host thread its own context; the
+ * *_host calls bind the context's device on a thread's first call
+ * (tests/test_gpu_host_calls.py: two threads, two contexts, shared handles). */
 HIRE_API int hire_ctx_create(int device, void* cuda_stream, int own_stream, hire_ctx* out);
 HIRE_API int hire_ctx_destroy(hire_ctx ctx);
 HIRE_API int hire_ctx_stream(hire_ctx ctx, void** cuda_stream);
