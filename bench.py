@@ -817,6 +817,9 @@ def pipelined_e2e(wl, H, device, xh, K, n_warm, pinned, lanes, serial):
     serial call on the same input."""
     import copy
     import threading
+    lanes = min(lanes, K)  # every lane gets at least one step
+    if lanes < 2:
+        return None
     oa0, ob0, hctx0 = serial
     lw = []
     for l in range(lanes):
@@ -910,7 +913,7 @@ def run_ours(args):
     tokens = wl.B * K * (1 if wl.scaling == "strong" else world)
     value = tokens / (ms / 1e3)
     single = {"ms_per_step": round(ms_step, 5), "value": round(value, 2)}
-    S = args.streams if (world == 1 and not getattr(wl, "da", False) and wl.name != "cfg5") else 1
+    S = min(args.streams, K) if (world == 1 and not getattr(wl, "da", False) and wl.name != "cfg5") else 1
     if S > 1:
         # The same K steps dealt over S streams (one hire context and workspace
         # set per stream) inside one graph: independent batches, so one
